@@ -1,0 +1,183 @@
+/*
+ * qfca_b200.h -- C-ABI of the B200-native QFCA scoring path (sm_100a).
+ *
+ * The reference (arxiv 2510.15602, /root/reference/pkg/src/qfca) is pure
+ * Python; it has no C FFI.  Its closest native surface is the pair of Numba
+ * kernels that a binding would replace:
+ *   _channel_score_kernel(idx, nbins, t, pad_code, refw, centers, score_out)
+ *       scoring.py:205-260           -> qfca_score (+ qfca_select_reference)
+ *   mismatch_batch(Pb, R, Q, out)      transport.py:310-325 -> qfca_mismatch_pixels
+ * and the NumPy stages around them, each of which gets an entry point below
+ * (file:line of the function it replaces in the comment).  libqfca_b200.so
+ * exports exactly these symbols.
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers and sizes, no framework types; the caller owns
+ *     and allocates every buffer (the library allocates nothing persistent);
+ *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default)
+ *     and is asynchronous; no host synchronisation except where stated;
+ *   - return value: QFCA_OK (0) or an error code (QFCA_ERR_*); argument
+ *     errors are detected before anything is enqueued;
+ *   - feature planes are float32, contiguous (images, channels, h, w); a
+ *     "plane" is one (image, channel) h x w map; bins are uint8 (n_bins <=
+ *     256), uint16 (<= 65536) or int32 (bins_bytes = 1, 2, 4);
+ *   - pad codes follow scoring.py:183: 0 zero, 1 reflect, 2 wrap.
+ */
+#ifndef QFCA_B200_H
+#define QFCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QFCA_OK 0
+#define QFCA_ERR_ARG 1
+#define QFCA_ERR_CUDA 2
+#define QFCA_ERR_UNSUPPORTED 3
+
+#define QFCA_REF_MEDIAN_QUAN 0 /* quantize.py:174-183 (default) */
+#define QFCA_REF_QUAN_MEDIAN 2 /* quantize.py:184-199 */
+#define QFCA_REF_QUAN_MEAN 3   /* quantize.py:184-199 */
+
+int qfca_abi_version(void);
+/* number of kernels this library has launched since it was loaded */
+int64_t qfca_launch_count(void);
+const char* qfca_status_str(int status);
+
+/* fit_quantizer (quantize.py:61-68) + FeatureMap finiteness (features.py:36-37):
+ * per-plane min -> lo, max -> hi; *nonfinite |= 1 if any value is not finite. */
+int qfca_fit_quantizer(const float* x, int64_t planes, int64_t plane_len, float* lo, float* hi,
+                       int32_t* nonfinite, void* stream);
+
+/* bin_indices (quantize.py:71-82), bit-exact fp64 rule; degenerate -> 0 */
+int qfca_bin_indices(const float* x, int64_t planes, int64_t plane_len, const float* lo,
+                     const float* hi, int32_t n_bins, void* bins, int32_t bins_bytes,
+                     void* stream);
+
+/* _sample_grid stride (quantize.py:109-116); host-only helper */
+int qfca_sample_stride(int32_t h, int32_t w, int32_t sample_budget);
+
+/* select_reference (quantize.py:150-200), sort-free.  stats is (planes, n_bins)
+ * int32:  mode 0 (median-quan): cumulative reference counts V_i, so the
+ *         reference weights are R_i = V_i - V_{i-1} (exact integers);
+ *         mode 2 (quan-median): per-bin lower median of the window counts;
+ *         mode 3 (quan-mean): per-bin sum of the window counts over samples.
+ * Degenerate planes: mode 0 -> V = T^2; modes 2/3 -> bin 0 only. */
+int qfca_select_reference(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
+                          int64_t planes, int32_t h, int32_t w, int32_t n_bins,
+                          int32_t patch_size, int32_t pad, int32_t sample_budget, int32_t mode,
+                          int32_t* stats, void* stream);
+
+/* patch_histograms (quantize.py:85-106): window counts (planes, n_bins, h, w),
+ * counts_kind 0 = float32, 1 = uint16.  scratch: planes*n_bins*h*w uint16. */
+int qfca_window_counts(const void* bins, int32_t bins_bytes, int64_t planes, int32_t h,
+                       int32_t w, int32_t n_bins, int32_t patch_size, int32_t pad,
+                       uint16_t* scratch, void* counts, int32_t counts_kind, void* stream);
+
+/* mismatch_batch (transport.py:310-325) over every pixel of every plane:
+ * counts (planes, n_bins, hw) uint16, ref_weights / centers (planes, n_bins)
+ * fp64, err (planes, n_bins, hw) fp64.  skip[plane] != 0 -> zero errors. */
+int qfca_mismatch_pixels(const uint16_t* counts, int64_t planes, int64_t hw, int32_t n_bins,
+                         const double* ref_weights, const double* centers, const uint8_t* skip,
+                         double* err, void* stream);
+
+/* mismatch_batch (transport.py:310-325) verbatim: Pb (rows, n_bins) fp64
+ * row-major, R / Q (n_bins) fp64, out (rows, n_bins) fp64 */
+int qfca_mismatch_rows(const double* Pb, int64_t rows, int32_t n_bins, const double* R,
+                       const double* Q, double* out, void* stream);
+
+/* _smooth_error_planes + own-bin gather (scoring.py:116-140): separable filter
+ * of the error planes with taps (host array, patch_size taps: ones for the
+ * box, the normalised Gaussian for finite sigma_p), times post_scale, read at
+ * each pixel's own bin.  scratch: planes*n_bins*h*w fp64; score: planes*h*w. */
+int qfca_smooth_gather(const double* err, const void* bins, int32_t bins_bytes, int64_t planes,
+                       int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, int32_t pad,
+                       const double* taps_host, double post_scale, double* scratch,
+                       double* score, void* stream);
+
+/* fixed-order channel sum (scoring.py:292-309) of per-channel scores */
+int qfca_channel_sum(const double* score, int64_t images, int32_t channels, int64_t hw,
+                     const uint8_t* skip, int32_t accumulate, double* acc, int32_t* used,
+                     void* stream);
+
+/* number of non-degenerate channels per image (scoring.py:309 `used`) */
+int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t channels,
+                    int32_t* used, void* stream);
+
+/* channel groups qfca_score will use (host-only) for groups_hint (<= 0: auto) */
+int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, int32_t channels,
+                      int64_t images, int32_t groups_hint);
+
+/* THE HOT PATH: _channel_score_kernel + channel accumulation
+ * (scoring.py:205-260, 286-309) fused, for uniform sigma_p, median-quan and
+ * reflect / wrap padding.  ref_cum = qfca_select_reference mode-0 stats.
+ * partial: (images, groups, h, w) float32, must be zeroed by the caller; each
+ * group adds its channels' scores in fixed channel order. */
+int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
+               const int32_t* ref_cum, int64_t images, int32_t channels, int32_t h, int32_t w,
+               int32_t n_bins, int32_t patch_size, int32_t pad, int32_t groups, float* partial,
+               void* stream);
+
+/* agg = (sum over groups, fixed order, fp64) / used   (scoring.py:311-317) */
+int qfca_reduce_partials(const float* partial, int64_t images, int32_t groups, int64_t hw,
+                         const int32_t* used, double* agg, void* stream);
+int qfca_divide_used(const double* acc, int64_t images, int64_t hw, const int32_t* used,
+                     double* agg, void* stream);
+
+/* one separable pass of gaussian_blur (features.py:56-77); axis 0 = rows */
+int qfca_sep_conv(const double* in, int64_t images, int32_t h, int32_t w, int32_t axis,
+                  const double* taps_host, int32_t ntaps, int32_t pad, double* out, void* stream);
+
+/* image_score_of (scoring.py:169-174) */
+int qfca_image_score(const double* scores, int64_t images, int32_t h, int32_t w, int32_t border,
+                     double* image_score, void* stream);
+
+/* upsample_scores (scoring.py:177-180, tensor_io.py:127-151) -> float32 */
+int qfca_upsample(const double* in, int64_t images, int32_t h, int32_t w, int32_t out_h,
+                  int32_t out_w, float* out, void* stream);
+
+/* pca_fit pieces (features.py:157-180): per-plane fp64 mean, centred fp32 copy */
+int qfca_plane_mean(const float* x, int64_t planes, int64_t plane_len, double* mean, void* stream);
+int qfca_center(const float* x, int64_t planes, int64_t plane_len, const double* mean, float* out,
+                void* stream);
+
+/* pca_residual (features.py:183-193): r = (x-mu) - V^T V (x-mu), fp64 math,
+ * float32 out.  mean (C) / comps (k, C) fp64, per image if per_image_model. */
+int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t hw,
+                      const double* mean, const double* comps, int32_t k,
+                      int32_t per_image_model, float* out, void* stream);
+
+/* ---- one-call detect (scoring.py:263-327) for the fused configuration ---- */
+typedef struct qfca_config {
+    int32_t n_bins;        /* PipelineConfig.n_bins (16) */
+    int32_t patch_size;    /* PipelineConfig.patch_size (9) */
+    int32_t pad;           /* 1 reflect (default) or 2 wrap */
+    int32_t sample_budget; /* 4096 */
+    int32_t border;        /* border exclusion (patch_size / 2 by default) */
+    int32_t groups;        /* channel groups (<= 0: auto) */
+    double sigma_s;        /* 1.0 */
+} qfca_config;
+
+int64_t qfca_detect_workspace_bytes(int64_t images, int32_t channels, int32_t h, int32_t w,
+                                    const qfca_config* cfg);
+
+/* features (images, channels, h, w) -> scores (images, h, w) fp64,
+ * image_scores (images) fp64, used (images) int32, *nonfinite (device int32). */
+int qfca_detect(const float* features, int64_t images, int32_t channels, int32_t h, int32_t w,
+                const qfca_config* cfg, void* workspace, int64_t workspace_bytes, double* scores,
+                double* image_scores, int32_t* used, int32_t* nonfinite, void* stream);
+
+/* qfca_detect with optional timing hooks: stage_events[0] / [1] (cudaEvent_t
+ * or NULL) are recorded on `stream` right before / after the fused scoring
+ * kernel (qfca_score). */
+int qfca_detect_ex(const float* features, int64_t images, int32_t channels, int32_t h, int32_t w,
+                   const qfca_config* cfg, void* workspace, int64_t workspace_bytes,
+                   double* scores, double* image_scores, int32_t* used, int32_t* nonfinite,
+                   void* const* stage_events, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QFCA_B200_H */

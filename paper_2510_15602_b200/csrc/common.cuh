@@ -1,0 +1,89 @@
+// common.cuh -- shared device helpers for the QFCA B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define QFCA_PAD_ZERO 0
+#define QFCA_PAD_REFLECT 1
+#define QFCA_PAD_WRAP 2
+
+// status codes returned through the C-ABI (include/qfca_b200.h)
+#define QFCA_OK 0
+#define QFCA_ERR_ARG 1
+#define QFCA_ERR_CUDA 2
+#define QFCA_ERR_UNSUPPORTED 3
+
+namespace qfca {
+
+// filter taps passed by value (kernel parameter space), at most 255 taps
+constexpr int QFCA_MAX_TAPS = 255;
+struct Taps {
+    double k[QFCA_MAX_TAPS];
+    int n;
+};
+
+// Padded-plane coordinate -> source index, -1 for zero padding.
+// Restates scoring.py:186-202 (_map_coord): reflect without edge repeat,
+// repeated for large margins; n == 1 -> 0; wrap is toroidal.
+__host__ __device__ __forceinline__ int map_coord(int c, int n, int pad) {
+    if (c >= 0 && c < n) return c;
+    if (pad == QFCA_PAD_ZERO) return -1;
+    if (pad == QFCA_PAD_WRAP) {
+        int m = c % n;
+        return m < 0 ? m + n : m;
+    }
+    if (n == 1) return 0;
+    while (c < 0 || c >= n) {
+        if (c < 0) c = -c;
+        if (c >= n) c = 2 * n - 2 - c;
+    }
+    return c;
+}
+
+// np.pad index as used by pooling.py:20-38 (pad_plane): identical to
+// map_coord except that reflect switches to 'edge' on both axes when either
+// axis has length 1 (pooling.py:31-35).  Used only by reference selection
+// (quantize.py:119-132).  Zero padding returns -1 (value 0.0).
+__host__ __device__ __forceinline__ int pad_plane_index(int c, int n, int pad, bool edge) {
+    if (c >= 0 && c < n) return c;
+    if (pad == QFCA_PAD_ZERO) return -1;
+    if (pad == QFCA_PAD_WRAP) {
+        int m = c % n;
+        return m < 0 ? m + n : m;
+    }
+    if (edge || n == 1) return c < 0 ? 0 : n - 1;
+    return map_coord(c, n, pad);
+}
+
+// The reference bin rule (quantize.py:79-81), evaluated exactly as NumPy does
+// it: fp64 ((v - lo) * N) / safe, floor, clip to [0, N-1].
+__device__ __forceinline__ int bin_of(float v, double lo, double safe, int n_bins) {
+    double q = ((double)v - lo) * (double)n_bins / safe;
+    double f = floor(q);
+    if (!(f > 0.0)) return 0;  // also maps NaN to 0
+    if (f > (double)(n_bins - 1)) return n_bins - 1;
+    return (int)f;
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace qfca

@@ -1,0 +1,152 @@
+// quantize.cu -- K1 (per-plane min/max + finiteness) and K2 (bin indices).
+//
+// K1 restates quantize.py:61-68 (fit_quantizer) and the FeatureMap finiteness
+// check (features.py:36-37); K2 restates quantize.py:71-82 (bin_indices) bit
+// for bit: the fp64 expression is evaluated exactly as NumPy evaluates it.
+// Both are streaming, HBM-bound passes: one CTA per plane for K1 (float4
+// loads), a flat grid for K2 (float4 in, 4 bins out per thread).
+#include "common.cuh"
+
+namespace qfca {
+
+constexpr int MINMAX_THREADS = 512;
+
+__global__ void __launch_bounds__(MINMAX_THREADS)
+k_minmax(const float* __restrict__ x, int64_t plane_len, float* __restrict__ lo,
+         float* __restrict__ hi, int* __restrict__ nonfinite) {
+    const int64_t plane = blockIdx.x;
+    const float* p = x + plane * plane_len;
+    float mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
+    const bool vec = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+    int64_t n4 = vec ? plane_len / 4 : 0;
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) {
+        float4 v = __ldg(p4 + i);
+        mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    for (int64_t i = n4 * 4 + threadIdx.x; i < plane_len; i += blockDim.x) {
+        float v = __ldg(p + i);
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+        bad |= !isfinite(v);
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    bad = __any_sync(0xffffffffu, bad);
+    __shared__ float smn[32], smx[32];
+    __shared__ int sbad;
+    if (threadIdx.x == 0) sbad = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        smn[warp] = mn;
+        smx[warp] = mx;
+        if (bad) sbad = 1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        mn = lane < nw ? smn[lane] : INFINITY;
+        mx = lane < nw ? smx[lane] : -INFINITY;
+        mn = warp_min(mn);
+        mx = warp_max(mx);
+        if (lane == 0) {
+            lo[plane] = mn;
+            hi[plane] = mx;
+            if (sbad && nonfinite) atomicOr(nonfinite, 1);
+        }
+    }
+}
+
+template <typename BT>
+__global__ void __launch_bounds__(256)
+k_bin(const float* __restrict__ x, int64_t plane_len, int64_t blocks_per_plane,
+      const float* __restrict__ lo, const float* __restrict__ hi, int n_bins,
+      BT* __restrict__ out) {
+    const int64_t plane = blockIdx.x / blocks_per_plane;
+    const int64_t blk = blockIdx.x % blocks_per_plane;
+    const double l = lo[plane], h = hi[plane];
+    const bool degen = !(h > l);
+    const double span = h - l;
+    const double safe = span > 0 ? span : 1.0;
+    const float* p = x + plane * plane_len;
+    BT* o = out + plane * plane_len;
+    const int64_t base = (blk * blockDim.x + threadIdx.x) * 4;
+    if (base >= plane_len) return;
+    if (base + 4 <= plane_len && ((reinterpret_cast<uintptr_t>(p + base) & 15) == 0)) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(p + base));
+        int b0 = degen ? 0 : bin_of(v.x, l, safe, n_bins);
+        int b1 = degen ? 0 : bin_of(v.y, l, safe, n_bins);
+        int b2 = degen ? 0 : bin_of(v.z, l, safe, n_bins);
+        int b3 = degen ? 0 : bin_of(v.w, l, safe, n_bins);
+        o[base] = (BT)b0;
+        o[base + 1] = (BT)b1;
+        o[base + 2] = (BT)b2;
+        o[base + 3] = (BT)b3;
+    } else {
+        for (int64_t i = base; i < base + 4 && i < plane_len; ++i)
+            o[i] = (BT)(degen ? 0 : bin_of(__ldg(p + i), l, safe, n_bins));
+    }
+}
+
+// per-plane mean in fp64 (pca_fit, features.py:170) -- one CTA per plane
+__global__ void __launch_bounds__(256)
+k_plane_mean(const float* __restrict__ x, int64_t plane_len, double* __restrict__ mean) {
+    const int64_t plane = blockIdx.x;
+    const float* p = x + plane * plane_len;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < plane_len; i += blockDim.x) s += (double)__ldg(p + i);
+    s = warp_sum(s);
+    __shared__ double sh[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+        s = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) mean[plane] = s / (double)plane_len;
+    }
+}
+
+int launch_minmax(const float* x, int64_t planes, int64_t plane_len, float* lo, float* hi,
+                  int* nonfinite, cudaStream_t st) {
+    if (planes <= 0 || plane_len <= 0) return QFCA_ERR_ARG;
+    k_minmax<<<(unsigned)planes, MINMAX_THREADS, 0, st>>>(x, plane_len, lo, hi, nonfinite);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int launch_bin(const float* x, int64_t planes, int64_t plane_len, const float* lo,
+               const float* hi, int n_bins, void* out, int out_bytes, cudaStream_t st) {
+    if (planes <= 0 || plane_len <= 0 || n_bins < 1) return QFCA_ERR_ARG;
+    const int64_t per = 256 * 4;
+    const int64_t bpp = (plane_len + per - 1) / per;
+    const int64_t grid = bpp * planes;
+    if (grid > 0x7fffffffLL) return QFCA_ERR_ARG;
+    if (out_bytes == 1) {
+        if (n_bins > 256) return QFCA_ERR_ARG;
+        k_bin<uint8_t><<<(unsigned)grid, 256, 0, st>>>(x, plane_len, bpp, lo, hi, n_bins,
+                                                        (uint8_t*)out);
+    } else if (out_bytes == 2) {
+        if (n_bins > 65536) return QFCA_ERR_ARG;
+        k_bin<uint16_t><<<(unsigned)grid, 256, 0, st>>>(x, plane_len, bpp, lo, hi, n_bins,
+                                                         (uint16_t*)out);
+    } else if (out_bytes == 4) {
+        k_bin<int32_t><<<(unsigned)grid, 256, 0, st>>>(x, plane_len, bpp, lo, hi, n_bins,
+                                                        (int32_t*)out);
+    } else {
+        return QFCA_ERR_ARG;
+    }
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int launch_plane_mean(const float* x, int64_t planes, int64_t plane_len, double* mean,
+                      cudaStream_t st) {
+    if (planes <= 0 || plane_len <= 0) return QFCA_ERR_ARG;
+    k_plane_mean<<<(unsigned)planes, 256, 0, st>>>(x, plane_len, mean);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+}  // namespace qfca

@@ -1,0 +1,173 @@
+"""Feature maps and PCA-residual preprocessing on the GPU.
+
+Mirrors qfca.features (reference features.py:26-41, 49-77, 150-193): same
+names, same dataclasses, same validation and error types.  The covariance is
+an fp32 tensor-core-free GEMM split into K-chunks whose partial products are
+summed in fp64; the eigensolver is fp64; the residual kernel is ours
+(csrc/pca.cu).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._dev import empty, is_torch, to_dev, to_host
+
+__all__ = ["FeatureMap", "PcaModel", "pca_fit", "pca_residual", "pca_fit_batch",
+           "pca_residual_batch", "gaussian_blur", "FormatError"]
+
+
+class FormatError(Exception):
+    """External feature file does not match the expected layout."""
+
+
+@dataclass(frozen=True)
+class FeatureMap:
+    """(C, H, W) float32 features + downsampling scale (features.py:26-41).
+
+    ``values`` may be a NumPy array or a torch CUDA tensor.
+    """
+
+    values: object
+    scale: int = 1
+
+    def __post_init__(self):
+        v = self.values
+        if v.ndim != 3:
+            raise ValueError("feature values must be (C, H, W)")
+        if self.scale < 1:
+            raise ValueError("scale must be >= 1")
+        if is_torch(v):
+            finite = bool(torch.isfinite(v).all())
+        else:
+            finite = bool(np.all(np.isfinite(v)))
+        if not finite:
+            raise ValueError("feature values must be finite")
+
+    @property
+    def n_channels(self) -> int:
+        return self.values.shape[0]
+
+
+@dataclass(frozen=True)
+class PcaModel:
+    mean: object        # (C,) fp64
+    components: object  # (k, C) fp64, orthonormal rows
+    eigenvalues: object  # (k,) fp64, non-increasing
+
+
+def _gauss_kernel(sigma: float) -> np.ndarray:
+    """features.py:49-53."""
+    radius = int(np.ceil(3 * sigma))
+    x = np.arange(-radius, radius + 1, dtype=np.float64)
+    k = np.exp(-0.5 * (x / sigma) ** 2)
+    return k / k.sum()
+
+
+def sep_convolve_dev(planes: torch.Tensor, kernel: np.ndarray, pad: str) -> torch.Tensor:
+    """_sep_convolve (features.py:56-69) on a (B, H, W) fp64 device stack."""
+    b, h, w = planes.shape
+    k = np.ascontiguousarray(kernel, dtype=np.float64)
+    tmp = empty((b, h, w), torch.float64)
+    out = empty((b, h, w), torch.float64)
+    s = N.stream()
+    kp = k.ctypes.data_as(N._P)
+    N.call("qfca_sep_conv", planes.data_ptr(), b, h, w, 0, kp, k.size, N.PAD_CODES[pad],
+           tmp.data_ptr(), s)
+    N.call("qfca_sep_conv", tmp.data_ptr(), b, h, w, 1, kp, k.size, N.PAD_CODES[pad],
+           out.data_ptr(), s)
+    return out
+
+
+def gaussian_blur(plane, sigma: float, pad: str = "reflect"):
+    """features.py:72-77 on the GPU; returns the input's kind (NumPy / torch)."""
+    if sigma <= 0:
+        return plane.to(torch.float64) if is_torch(plane) else np.asarray(plane, np.float64)
+    x = to_dev(plane, torch.float64)
+    out = sep_convolve_dev(x.reshape((1,) + tuple(x.shape)), _gauss_kernel(sigma), pad)[0]
+    return to_host(out, is_torch(plane))
+
+
+def covariance_dev(xc: torch.Tensor, chunk: int = 1024) -> torch.Tensor:
+    """(B, C, HW) centred fp32 -> (B, C, C) fp64 population covariance.
+
+    fp32 GEMMs over K-chunks (IEEE fp32, TF32 off) summed in fp64, / HW.
+    """
+    b, c, hw = xc.shape
+    nk = (hw + chunk - 1) // chunk
+    if nk * chunk != hw:
+        xc = torch.nn.functional.pad(xc, (0, nk * chunk - hw))
+    blocks = xc.reshape(b, c, nk, chunk).permute(0, 2, 1, 3).reshape(b * nk, c, chunk)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        part = torch.bmm(blocks, blocks.transpose(1, 2))
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    cov = part.reshape(b, nk, c, c).sum(dim=1, dtype=torch.float64)
+    return cov / float(hw)
+
+
+def pca_fit_batch(x: torch.Tensor, k: int):
+    """Batched pca_fit on (B, C, H, W) device features -> (mean, comps, evals)."""
+    b, c, h, w = x.shape
+    hw = h * w
+    s = N.stream()
+    mean = empty((b, c), torch.float64)
+    N.call("qfca_plane_mean", x.data_ptr(), b * c, hw, mean.data_ptr(), s)
+    xc = empty((b, c, hw), torch.float32)
+    N.call("qfca_center", x.data_ptr(), b * c, hw, mean.data_ptr(), xc.data_ptr(), s)
+    cov = covariance_dev(xc)
+    del xc
+    evals, evecs = torch.linalg.eigh(cov)  # ascending, fp64
+    # np.argsort(evals, kind="stable")[::-1][:k]: eigh output is sorted already,
+    # so the stable descending order is the reversed index range
+    idx = torch.arange(c - 1, c - 1 - k, -1, device=x.device)
+    ev = evals[:, idx].clamp(min=0.0)
+    comps = evecs[:, :, idx].transpose(1, 2).contiguous()  # (B, k, C)
+    arg = comps.abs().argmax(dim=2, keepdim=True)
+    sign = torch.where(torch.gather(comps, 2, arg) < 0, -1.0, 1.0).to(comps.dtype)
+    comps = comps * sign
+    return mean, comps, ev
+
+
+def pca_residual_batch(x: torch.Tensor, mean: torch.Tensor, comps: torch.Tensor,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
+    """Batched pca_residual (per-image model) on (B, C, H, W) device features."""
+    b, c, h, w = x.shape
+    k = comps.shape[-2]
+    if out is None:
+        out = empty((b, c, h, w), torch.float32)
+    per_image = 1 if mean.dim() == 2 else 0
+    N.call("qfca_pca_residual", x.data_ptr(), b, c, h * w,
+           mean.contiguous().data_ptr(), comps.contiguous().data_ptr(), k, per_image,
+           out.data_ptr(), N.stream())
+    return out
+
+
+def pca_fit(f: FeatureMap, k: int) -> PcaModel:
+    """features.py:157-180: top-k principal components of the pixel vectors."""
+    c = f.n_channels
+    if not (1 <= k <= c):
+        raise ValueError(f"k must be in [1, {c}], got {k}")
+    x = to_dev(f.values)
+    mean, comps, ev = pca_fit_batch(x[None], k)
+    t = is_torch(f.values)
+    return PcaModel(mean=to_host(mean[0], t), components=to_host(comps[0], t),
+                    eigenvalues=to_host(ev[0], t))
+
+
+def pca_residual(f: FeatureMap, m: PcaModel) -> FeatureMap:
+    """features.py:183-193: r = (x - mean) - V^T V (x - mean), float32."""
+    c = f.n_channels
+    if m.mean.shape[0] != c:
+        raise ValueError(f"model has {m.mean.shape[0]} channels, features have {c}")
+    x = to_dev(f.values)
+    mean = to_dev(m.mean, torch.float64)
+    comps = to_dev(m.components, torch.float64)
+    r = pca_residual_batch(x[None], mean, comps)[0]
+    return FeatureMap(values=to_host(r, is_torch(f.values)), scale=f.scale)

@@ -1,0 +1,258 @@
+"""Per-channel quantization, window histograms and reference selection (GPU).
+
+Mirrors qfca.quantize (reference quantize.py:1-200): same names, dataclasses,
+validation and error messages.  fit_quantizer / bin_indices run K1/K2
+(csrc/quantize.cu), patch_histograms the window-count kernels
+(csrc/generic.cu), select_reference the sort-free order-statistic kernel K3
+(csrc/reference.cu) -- bit-exact against the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._dev import empty, is_torch, to_dev, to_host, zeros
+
+REFERENCE_MODES = ("median-quan", "mean-quan", "quan-median", "quan-mean")
+
+__all__ = ["Quantizer", "BinIndexMap", "HistogramField", "ReferenceHistogram",
+           "REFERENCE_MODES", "fit_quantizer", "bin_indices", "patch_histograms",
+           "select_reference", "sample_stride", "bins_dtype"]
+
+
+@dataclass(frozen=True)
+class Quantizer:
+    """Equally-spaced bins per channel over [lo, hi] (quantize.py:16-38)."""
+
+    lo: object  # (C,) fp64
+    hi: object  # (C,) fp64
+    n_bins: int
+    degenerate: object  # (C,) bool
+
+    @property
+    def n_channels(self) -> int:
+        return self.lo.shape[0]
+
+    def centers(self, c: int) -> np.ndarray:
+        lo, hi = float(self.lo[c]), float(self.hi[c])
+        width = (hi - lo) / self.n_bins if hi > lo else 1.0
+        return lo + (np.arange(self.n_bins) + 0.5) * width
+
+
+@dataclass(frozen=True)
+class BinIndexMap:
+    indices: object  # (C, H, W) int32 in [0, N)
+    n_bins: int
+
+
+@dataclass(frozen=True)
+class HistogramField:
+    counts: object  # (C, N, H, W) float32
+    patch_size: int
+
+
+@dataclass(frozen=True)
+class ReferenceHistogram:
+    weights: object  # (C, N) fp64, mass T^2 per channel
+    patch_size: int
+
+
+def bins_dtype(n_bins: int):
+    """Compact on-device bin storage: uint8 up to 256 bins, else int16 bits."""
+    return (torch.uint8, 1) if n_bins <= 256 else (torch.int16, 2)
+
+
+def sample_stride(h: int, w: int, budget: int) -> int:
+    """quantize.py:109-116."""
+    return int(N.lib().qfca_sample_stride(h, w, budget))
+
+
+# ---------------------------------------------------------------- device ops
+def minmax_dev(x: torch.Tensor, planes: int, plane_len: int):
+    lo = empty((planes,), torch.float32)
+    hi = empty((planes,), torch.float32)
+    flag = zeros((1,), torch.int32)
+    N.call("qfca_fit_quantizer", x.data_ptr(), planes, plane_len, lo.data_ptr(), hi.data_ptr(),
+           flag.data_ptr(), N.stream())
+    return lo, hi, flag
+
+
+def bins_dev(x: torch.Tensor, lo: torch.Tensor, hi: torch.Tensor, planes: int, plane_len: int,
+             n_bins: int, dtype=None) -> torch.Tensor:
+    if dtype is None:
+        dtype, nb = bins_dtype(n_bins)
+    else:
+        nb = {torch.uint8: 1, torch.int16: 2, torch.int32: 4}[dtype]
+    out = empty((planes * plane_len,), dtype)
+    N.call("qfca_bin_indices", x.data_ptr(), planes, plane_len, lo.data_ptr(), hi.data_ptr(),
+           n_bins, out.data_ptr(), nb, N.stream())
+    return out
+
+
+def reference_stats_dev(bins: torch.Tensor, lo: torch.Tensor, hi: torch.Tensor, planes: int,
+                        h: int, w: int, n_bins: int, t: int, pad: str, budget: int,
+                        mode: str) -> torch.Tensor:
+    stats = empty((planes, n_bins), torch.int32)
+    nb = bins.element_size()
+    N.call("qfca_select_reference", bins.data_ptr(), nb, lo.data_ptr(), hi.data_ptr(), planes,
+           h, w, n_bins, t, N.PAD_CODES[pad], budget, N.REF_MODE_CODES[mode],
+           stats.data_ptr(), N.stream())
+    return stats
+
+
+def window_counts_dev(bins: torch.Tensor, planes: int, h: int, w: int, n_bins: int, t: int,
+                      pad: str, kind=torch.float32) -> torch.Tensor:
+    scratch = empty((planes * n_bins * h * w,), torch.int16)
+    out = empty((planes, n_bins, h, w), kind)
+    N.call("qfca_window_counts", bins.data_ptr(), bins.element_size(), planes, h, w, n_bins, t,
+           N.PAD_CODES[pad], scratch.data_ptr(), out.data_ptr(),
+           0 if kind == torch.float32 else 1, N.stream())
+    return out
+
+
+def _qtensors(q: Quantizer):
+    lo = to_dev(q.lo, torch.float64).to(torch.float32)
+    hi = to_dev(q.hi, torch.float64).to(torch.float32)
+    return lo, hi
+
+
+# ---------------------------------------------------------------- public API
+def fit_quantizer(values, n_bins: int) -> Quantizer:
+    """quantize.py:61-68 -- per-channel min/max range."""
+    if n_bins < 1:
+        raise ValueError(f"n_bins must be >= 1, got {n_bins}")
+    x = to_dev(values)
+    c = x.shape[0]
+    lo, hi, _ = minmax_dev(x, c, x.numel() // c)
+    lo64, hi64 = lo.to(torch.float64), hi.to(torch.float64)
+    t = is_torch(values)
+    return Quantizer(lo=to_host(lo64, t), hi=to_host(hi64, t), n_bins=n_bins,
+                     degenerate=to_host(hi64 <= lo64, t))
+
+
+def bin_indices(values, q: Quantizer) -> BinIndexMap:
+    """quantize.py:71-82 -- clamp(floor((v - lo) * N / (hi - lo)), 0, N - 1)."""
+    x = to_dev(values)
+    if x.shape[0] != q.n_channels:
+        raise ValueError("channel count mismatch with quantizer")
+    # the kernel evaluates the rule from the float32 range; a Quantizer built
+    # elsewhere must hold float32-representable bounds (fit_quantizer's do)
+    lo, hi = _qtensors(q)
+    c = x.shape[0]
+    b = bins_dev(x, lo, hi, c, x.numel() // c, q.n_bins, torch.int32).reshape(x.shape)
+    return BinIndexMap(indices=to_host(b, is_torch(values)), n_bins=q.n_bins)
+
+
+def patch_histograms(b: BinIndexMap, patch_size: int, pad: str = "reflect") -> HistogramField:
+    """quantize.py:92-106 -- window counts of every location (float32)."""
+    if patch_size % 2 == 0:
+        raise ValueError(f"patch size must be odd, got {patch_size}")
+    if pad not in N.PAD_CODES:
+        raise ValueError(f"unknown pad mode {pad!r}")
+    idx = to_dev(b.indices, torch.int32)
+    c, h, w = idx.shape
+    counts = window_counts_dev(idx, c, h, w, b.n_bins, patch_size, pad)
+    return HistogramField(counts=to_host(counts, is_torch(b.indices)), patch_size=patch_size)
+
+
+def _weights_from_stats(stats: np.ndarray, degen: np.ndarray, mode: str, t2: int,
+                        n_samples: int) -> np.ndarray:
+    """Reference weights from the kernel's integer statistics (quantize.py:168-199)."""
+    c, n = stats.shape
+    if mode == "median-quan":
+        v = stats.astype(np.int64)
+        return np.diff(np.concatenate([np.zeros((c, 1), np.int64), v], 1), axis=1).astype(
+            np.float64)
+    weights = np.zeros((c, n), np.float64)
+    for ch in range(c):
+        if degen[ch]:
+            weights[ch, 0] = t2
+            continue
+        if mode == "quan-median":
+            wv = stats[ch].astype(np.float64)
+        else:  # quan-mean: hists.mean(axis=0) of integer counts
+            wv = stats[ch].astype(np.float64) / n_samples
+        total = wv.sum()
+        weights[ch] = wv * (t2 / total) if total > 0 else 0.0
+        if total <= 0:
+            weights[ch, 0] = t2
+    return weights
+
+
+def _mean_quan_dev(x: torch.Tensor, lo64, hi64, degen, t: int, budget: int, pad: str):
+    """mean-quan (quantize.py:174-183): per-rank mean of the sorted sampled
+    patches, then binned.  Sorting on the GPU (torch.sort), fp64 mean."""
+    c, h, w = x.shape
+    r = t // 2
+    s = sample_stride(h, w, budget)
+    ys = torch.arange(0, h, s, device=x.device)
+    xs = torch.arange(0, w, s, device=x.device)
+    edge = pad == "reflect" and not (h > 1 and w > 1)
+
+    def idx(n, lim):
+        i = torch.arange(-r, n + r, device=x.device)
+        if pad == "wrap":
+            return torch.remainder(i, n), None
+        if pad == "zero":
+            return i.clamp(0, n - 1), (i >= 0) & (i < n)
+        if edge or n == 1:
+            return i.clamp(0, n - 1), None
+        while bool(((i < 0) | (i >= n)).any()):
+            i = torch.where(i < 0, -i, i)
+            i = torch.where(i >= n, 2 * n - 2 - i, i)
+        return i, None
+
+    yi, ym = idx(h, h)
+    xi, xm = idx(w, w)
+    padded = x[:, yi][:, :, xi]
+    if pad == "zero":
+        mask = ym[:, None] & xm[None, :]
+        padded = padded * mask.to(padded.dtype)
+    win = padded.unfold(1, t, 1).unfold(2, t, 1)  # (C, h, w, t, t)
+    pts = win[:, ys][:, :, xs].reshape(c, -1, t * t)
+    ranked = torch.sort(pts, dim=2).values
+    return ranked.to(torch.float64).mean(dim=1)  # (C, T^2)
+
+
+def select_reference(values, q: Quantizer, patch_size: int, mode: str = "median-quan",
+                     sample_budget: int = 4096, pad: str = "reflect") -> ReferenceHistogram:
+    """quantize.py:150-200 -- global per-channel reference histogram."""
+    if mode not in REFERENCE_MODES:
+        raise ValueError(f"unknown reference mode {mode!r}")
+    if sample_budget < 1:
+        raise ValueError("sample_budget must be >= 1")
+    if patch_size % 2 == 0 or patch_size < 1:
+        raise ValueError(f"patch size must be odd, got {patch_size}")
+    if pad not in N.PAD_CODES:
+        raise ValueError(f"unknown pad mode {pad!r}")
+    x = to_dev(values)
+    c, h, w = x.shape
+    t2 = patch_size * patch_size
+    lo, hi = _qtensors(q)
+    degen = np.asarray(q.degenerate.cpu() if is_torch(q.degenerate) else q.degenerate, bool)
+    if mode == "mean-quan":
+        ref = _mean_quan_dev(x, lo, hi, degen, patch_size, sample_budget, pad).cpu().numpy()
+        weights = np.zeros((c, q.n_bins), np.float64)
+        lo_h = np.asarray(q.lo.cpu() if is_torch(q.lo) else q.lo, np.float64)
+        hi_h = np.asarray(q.hi.cpu() if is_torch(q.hi) else q.hi, np.float64)
+        for ch in range(c):
+            if degen[ch]:
+                weights[ch, 0] = t2
+                continue
+            span = hi_h[ch] - lo_h[ch] if hi_h[ch] > lo_h[ch] else 1.0
+            idx = np.clip(np.floor((ref[ch] - lo_h[ch]) * q.n_bins / span), 0, q.n_bins - 1)
+            weights[ch] = np.bincount(idx.astype(np.int64), minlength=q.n_bins)
+    else:
+        b = bins_dev(x, lo, hi, c, h * w, q.n_bins)
+        stats = reference_stats_dev(b, lo, hi, c, h, w, q.n_bins, patch_size, pad,
+                                    sample_budget, mode).cpu().numpy()
+        s = sample_stride(h, w, sample_budget)
+        n_samples = ((h + s - 1) // s) * ((w + s - 1) // s)
+        weights = _weights_from_stats(stats, degen, mode, t2, n_samples)
+    if is_torch(values):
+        weights = torch.from_numpy(weights).to(x.device)
+    return ReferenceHistogram(weights=weights, patch_size=patch_size)

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path vs the reference golden vectors and the CPU oracle.
+
+Bar: lo/hi, bins, window counts and median-quan reference weights bit-exact;
+anomaly maps within max-abs <= 1e-4 x max|ref| (north star tolerance).
+"""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import cfg_of, golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # max-abs relative to max |reference map| (BASELINE.json north star)
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = max(np.abs(b).max(), 1e-30)
+    return float(np.abs(a - b).max() / den)
+
+
+@pytest.fixture(scope="module")
+def Q():
+    import paper_2510_15602_b200 as q
+    return q
+
+
+CASES = [n for n in golden_names() if n not in ("transport_random", "wrn256_qfca_plus")]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_stages_and_map(Q, name):
+    d = load_golden(name)
+    cfg = Q.PipelineConfig(**cfg_of(d))
+    v = d["values"]
+    q = Q.fit_quantizer(v, cfg.n_bins)
+    np.testing.assert_array_equal(q.lo, d["lo"])
+    np.testing.assert_array_equal(q.hi, d["hi"])
+    np.testing.assert_array_equal(q.degenerate, d["degenerate"])
+    b = Q.bin_indices(v, q)
+    np.testing.assert_array_equal(b.indices, d["bins"])
+    ref = Q.select_reference(v, q, cfg.patch_size, mode=cfg.reference_mode,
+                             sample_budget=cfg.sample_budget, pad=cfg.pad)
+    if cfg.reference_mode == "mean-quan":
+        np.testing.assert_allclose(ref.weights, d["ref_weights"], atol=1e-9)
+    else:
+        np.testing.assert_array_equal(ref.weights, d["ref_weights"])
+    if "counts" in d:
+        hf = Q.patch_histograms(b, cfg.patch_size, pad=cfg.pad)
+        np.testing.assert_array_equal(hf.counts, d["counts"])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        am = Q.detect(Q.FeatureMap(values=v, scale=1), cfg)
+    assert am.degenerate == bool(d["detect_degenerate"])
+    if np.abs(d["scores"]).max() == 0:
+        assert np.abs(am.scores).max() <= 1e-12
+    else:
+        assert rel_err(am.scores, d["scores"]) <= TOL
+        assert abs(am.image_score - float(d["image_score"])) <= TOL * np.abs(d["scores"]).max()
+
+
+def test_wrn256_config1(Q):
+    """Config 1: 256x256 texture with a planted defect, random-init WRN50-2
+    block-2 features (512 x 32 x 32), default bins / patch size."""
+    d = load_golden("wrn256_qfca")
+    v = d["values"]
+    q = Q.fit_quantizer(v, 16)
+    b = Q.bin_indices(v, q)
+    np.testing.assert_array_equal(b.indices, d["bins"])
+    ref = Q.select_reference(v, q, 9)
+    np.testing.assert_array_equal(ref.weights, d["ref_weights"])
+    am = Q.detect(Q.FeatureMap(values=v, scale=8))
+    e = rel_err(am.scores, d["scores"])
+    print(f"config1 map rel max-abs err {e:.3e}")
+    assert e <= TOL
+    up = Q.upsample_scores(am.scores, 256, 256)
+    assert rel_err(up, d["upsampled"]) <= TOL
+    # upsampling itself is bit-exact on identical input
+    up_ref_in = Q.upsample_scores(d["scores"], 256, 256)
+    np.testing.assert_array_equal(up_ref_in.astype(np.float32), d["upsampled"])
+    # identical AUROC on the planted mask (ranking parity)
+    from oracle_metrics import auroc
+    a_gpu = auroc(up, d["mask"])
+    a_ref = auroc(d["upsampled"], d["mask"])
+    assert abs(a_gpu - a_ref) < 1e-4
+
+
+def test_wrn256_qfca_plus_on_reference_residual(Q):
+    """QFCA+ scoring fed the reference's own pca_residual: bins bit-exact,
+    map within tolerance (SURVEY 8c protocol (3))."""
+    p = load_golden("wrn256_qfca_plus")
+    res = p["residual"]
+    from oracle import qfca_oracle as O
+    lo, hi, dg = O.fit_quantizer(res, 16)
+    q = Q.fit_quantizer(res, 16)
+    np.testing.assert_array_equal(q.lo, lo)
+    np.testing.assert_array_equal(Q.bin_indices(res, q).indices, O.bin_indices(res, lo, hi, dg, 16))
+    am = Q.detect(Q.FeatureMap(values=res, scale=8))
+    assert rel_err(am.scores, p["scores"]) <= TOL
+
+
+def test_wrn256_qfca_plus_end_to_end(Q):
+    """QFCA+ with the GPU PCA (covariance, fp64 eigh, residual kernel)."""
+    d = load_golden("wrn256_qfca")
+    p = load_golden("wrn256_qfca_plus")
+    f = Q.FeatureMap(values=d["values"], scale=8)
+    m = Q.pca_fit(f, 10)
+    np.testing.assert_allclose(m.eigenvalues, p["pca_eigenvalues"], rtol=1e-5)
+    np.testing.assert_allclose(m.mean, p["pca_mean"], rtol=1e-9, atol=1e-12)
+    proj = m.components.T @ m.components
+    proj_ref = p["pca_components"].T @ p["pca_components"]
+    assert np.abs(proj - proj_ref).max() < 1e-4
+    r = Q.pca_residual(f, m).values
+    assert np.abs(r - p["residual"]).max() < 1e-4 * np.abs(p["residual"]).max()
+    am = Q.detect(f, Q.PipelineConfig(pca_components=10))
+    e = rel_err(am.scores, p["scores"])
+    print(f"QFCA+ end-to-end map rel max-abs err {e:.3e}")
+    assert e <= 1e-3
+
+
+@pytest.mark.parametrize("n,t,pad", [(16, 9, "reflect"), (16, 3, "wrap"), (64, 9, "reflect"),
+                                     (8, 17, "reflect"), (16, 9, "wrap"), (256, 5, "reflect")])
+def test_batch_vs_oracle(Q, n, t, pad):
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(n * 100 + t)
+    x = np.maximum(rng.standard_normal((2, 24, 40, 36)), 0).astype(np.float32)
+    x[0, 3] = 0.0  # a degenerate channel
+    cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
+    res = Q.detect_batch(torch.from_numpy(x).cuda(), cfg)
+    torch.cuda.synchronize()
+    for i in range(2):
+        s_ref, img_ref, _ = O.detect(x[i], n_bins=n, patch_size=t, pad=pad)
+        assert rel_err(res.scores[i].cpu().numpy(), s_ref) <= TOL
+        assert abs(float(res.image_scores[i]) - img_ref) <= TOL * np.abs(s_ref).max()
+    assert int(res.used[0]) == 23 and int(res.used[1]) == 24
+
+
+def test_capi_detect_matches_detect(Q):
+    d = load_golden("smooth_square_48")
+    cfg = Q.PipelineConfig(**cfg_of(d))
+    x = torch.from_numpy(d["values"][None]).cuda()
+    r = Q.detect_batch(x, cfg)
+    assert rel_err(r.scores[0].cpu().numpy(), d["scores"]) <= TOL
+
+
+def test_all_degenerate_warns_and_zero(Q):
+    v = np.full((3, 10, 10), 2.0, np.float32)
+    with pytest.warns(UserWarning):
+        am = Q.detect(Q.FeatureMap(values=v))
+    assert am.degenerate
+    assert np.abs(am.scores).max() == 0
+
+
+def test_affine_rescale_doubles_scores(Q):
+    d = load_golden("smooth_square_48")
+    v = d["values"]
+    cfg = Q.PipelineConfig(patch_size=5, sample_budget=48 * 48)
+    a = Q.detect(Q.FeatureMap(values=v), cfg).scores
+    b = Q.detect(Q.FeatureMap(values=(v * 2.0 + 1.0).astype(np.float32)), cfg).scores
+    np.testing.assert_allclose(b, 2.0 * a, rtol=1e-5, atol=1e-7 * np.abs(a).max())
+
+
+def test_toroidal_shift_equivariance(Q):
+    rng = np.random.default_rng(7)
+    v = rng.random((3, 24, 24)).astype(np.float32)
+    cfg = Q.PipelineConfig(patch_size=5, pad="wrap", sample_budget=24 * 24)
+    a = Q.detect(Q.FeatureMap(values=v), cfg).scores
+    b = Q.detect(Q.FeatureMap(values=np.roll(v, (7, 11), axis=(1, 2))), cfg).scores
+    np.testing.assert_allclose(np.roll(a, (7, 11), axis=(0, 1)), b, atol=1e-9)
+
+
+def test_transport_api(Q):
+    np.testing.assert_allclose(Q.quantized_mismatch([2, 1], [1, 2], [0, 1]), [0.5, 0.0])
+    np.testing.assert_allclose(Q.quantized_mismatch([3, 0], [0, 3], [0, 2]), [2.0, 0.0])
+    with pytest.raises(Q.MassError):
+        Q.quantized_mismatch([1, 1], [1, 2], [0, 1])
+    d = load_golden("transport_random")
+    for p, r, q, e in zip(d["P"], d["R"], d["Q"], d["E"]):
+        np.testing.assert_allclose(Q.quantized_mismatch(p, r, q), e, rtol=1e-9, atol=1e-12)
+    out = np.empty_like(d["P"])
+    r = d["R"][0]
+    Q.mismatch_batch(d["P"], r, d["Q"][0], out)
+    from oracle import qfca_oracle as O
+    np.testing.assert_array_equal(out, O.mismatch_batch(d["P"], r, d["Q"][0]))
+
+
+def test_step_apis_vs_reference_route(Q):
+    """bin_error_maps -> associate_errors -> aggregate -> smooth reproduces
+    detect (the reference's unfused route, scoring.py:87-166)."""
+    d = load_golden("small_rand_n16_t9_reflect")
+    v = d["values"]
+    cfg = Q.PipelineConfig(n_bins=16, patch_size=9)
+    q = Q.fit_quantizer(v, 16)
+    b = Q.bin_indices(v, q)
+    hf = Q.patch_histograms(b, 9)
+    ref = Q.select_reference(v, q, 9)
+    err = Q.bin_error_maps(hf, ref, q)
+    sc = Q.associate_errors(err, b, cfg)
+    agg, dg = Q.aggregate_channels(sc, skip=q.degenerate)
+    fin = Q.smooth_scores(agg, 1.0)
+    assert rel_err(fin, d["scores"]) <= 1e-12
+    assert Q.image_score_of(fin, 4) == pytest.approx(float(d["image_score"]), rel=1e-12)
+
+
+def test_large_plane_properties(Q):
+    """Full-size feature planes (128 x 128, config 3/4 geometry) on a channel
+    subset: bins and reference bit-exact vs the oracle, map within tolerance."""
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(11)
+    x = np.maximum(rng.standard_normal((6, 128, 128)) + 0.3, 0).astype(np.float32)
+    q = Q.fit_quantizer(x, 16)
+    lo, hi, dg = O.fit_quantizer(x, 16)
+    bins = O.bin_indices(x, lo, hi, dg, 16)
+    np.testing.assert_array_equal(Q.bin_indices(x, q).indices, bins)
+    np.testing.assert_array_equal(Q.select_reference(x, q, 9).weights,
+                                  O.select_reference(x, lo, hi, dg, 16, 9))
+    s_ref, _, _ = O.detect(x)
+    am = Q.detect(Q.FeatureMap(values=x))
+    assert rel_err(am.scores, s_ref) <= TOL
