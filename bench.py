@@ -212,6 +212,10 @@ def main():
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    for a, z in sev:  # torch creates the cudaEvent handle lazily, on first record
+        a.record()
+        z.record()
+    torch.cuda.synchronize()
     launches0 = _native.launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
