@@ -110,6 +110,11 @@ int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t ch
 int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, int32_t channels,
                       int64_t images, int32_t groups_hint);
 
+/* select the fused scoring kernel: 0 = auto (v2 -- compile-time patch size
+ * T <= 15, uint8 bins, 4 * G * w <= 512 -- where it applies, else v1),
+ * 1 = force v1 (score.cu), 2 = force v2 (score2.cu).  Process-global. */
+int qfca_set_score_kernel(int32_t version);
+
 /* THE HOT PATH: _channel_score_kernel + channel accumulation
  * (scoring.py:205-260, 286-309) fused, for uniform sigma_p, median-quan and
  * reflect / wrap padding.  ref_cum = qfca_select_reference mode-0 stats.

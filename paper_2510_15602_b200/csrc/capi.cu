@@ -38,6 +38,37 @@ int launch_upsample(const double*, int64_t, int, int, int, int, float*, cudaStre
 int launch_pca_residual(const float*, int64_t, int, int64_t, const double*, const double*, int,
                         int, float*, cudaStream_t);
 int launch_center(const float*, int64_t, int64_t, const double*, float*, cudaStream_t);
+int score2_groups(int, int, int, int, int, int64_t, int);
+int launch_score2(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
+                  int, int, int, int, int, float*, cudaStream_t);
+
+// fused-kernel selection: 0 = auto (v2 where it applies, else v1), 1 / 2 = force
+static int g_score_kernel = 0;
+
+static bool use_v2(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                   int bins_bytes) {
+    if (g_score_kernel == 1 || bins_bytes != 1) return false;
+    return score2_groups(h, w, n_bins, t, C, images, groups_hint) > 0;
+}
+
+static int score_groups_any(int h, int w, int n_bins, int t, int C, int64_t images,
+                            int groups_hint, int bins_bytes) {
+    if (use_v2(h, w, n_bins, t, C, images, groups_hint, bins_bytes))
+        return score2_groups(h, w, n_bins, t, C, images, groups_hint);
+    if (g_score_kernel == 2) return -1;
+    return score_groups(h, w, n_bins, t, C, images, groups_hint);
+}
+
+static int launch_score_any(const void* bins, int bins_bytes, const float* lo, const float* hi,
+                            const int32_t* V, int64_t images, int C, int h, int w, int n_bins,
+                            int t, int pad, int groups, float* partial, cudaStream_t st) {
+    if (use_v2(h, w, n_bins, t, C, images, groups, bins_bytes))
+        return launch_score2(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, groups,
+                             partial, st);
+    if (g_score_kernel == 2) return QFCA_ERR_UNSUPPORTED;
+    return launch_score(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, groups,
+                        partial, st);
+}
 }  // namespace qfca
 
 using namespace qfca;
@@ -137,15 +168,22 @@ int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t ch
 
 int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, int32_t channels,
                       int64_t images, int32_t groups_hint) {
-    return score_groups(h, w, n_bins, patch_size, channels, images, groups_hint);
+    return score_groups_any(h, w, n_bins, patch_size, channels, images, groups_hint,
+                            n_bins <= 256 ? 1 : 2);
+}
+
+int qfca_set_score_kernel(int32_t version) {
+    if (version < 0 || version > 2) return QFCA_ERR_ARG;
+    g_score_kernel = version;
+    return QFCA_OK;
 }
 
 int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
                const int32_t* ref_cum, int64_t images, int32_t channels, int32_t h, int32_t w,
                int32_t n_bins, int32_t patch_size, int32_t pad, int32_t groups, float* partial,
                void* stream) {
-    return counted(launch_score(bins, bins_bytes, lo, hi, ref_cum, images, channels, h, w, n_bins,
-                        patch_size, pad, groups, partial, S(stream)), 1);
+    return counted(launch_score_any(bins, bins_bytes, lo, hi, ref_cum, images, channels, h, w,
+                                    n_bins, patch_size, pad, groups, partial, S(stream)), 1);
 }
 
 int qfca_reduce_partials(const float* partial, int64_t images, int32_t groups, int64_t hw,
@@ -208,7 +246,8 @@ static int detect_layout(int64_t images, int32_t C, int32_t h, int32_t w, const 
     if (cfg->pad != QFCA_PAD_REFLECT && cfg->pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
     const int64_t planes = images * C, hw = (int64_t)h * w;
     L->bins_bytes = cfg->n_bins <= 256 ? 1 : 2;
-    L->groups = score_groups(h, w, cfg->n_bins, cfg->patch_size, C, images, cfg->groups);
+    L->groups = score_groups_any(h, w, cfg->n_bins, cfg->patch_size, C, images, cfg->groups,
+                                 L->bins_bytes);
     if (L->groups <= 0) return QFCA_ERR_UNSUPPORTED;
     size_t off = 0;
     L->lo = off; off = align256(off + planes * 4);
@@ -281,7 +320,7 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
     if (stage_events && stage_events[0] &&
         cudaEventRecord((cudaEvent_t)stage_events[0], st) != cudaSuccess)
         return QFCA_ERR_CUDA;
-    if ((rc = counted(launch_score(bins, L.bins_bytes, lo, hi, V, images, C, h, w, cfg->n_bins,
+    if ((rc = counted(launch_score_any(bins, L.bins_bytes, lo, hi, V, images, C, h, w, cfg->n_bins,
                            cfg->patch_size, cfg->pad, L.groups, partial, st), 1)))
         return rc;
     if (stage_events && stage_events[1] &&

@@ -236,3 +236,28 @@ def test_large_plane_properties(Q):
     s_ref, _, _ = O.detect(x)
     am = Q.detect(Q.FeatureMap(values=x))
     assert rel_err(am.scores, s_ref) <= TOL
+
+
+@pytest.mark.parametrize("shape,n,t,pad", [((3, 37, 64, 64), 16, 9, "reflect"),
+                                           ((2, 40, 128, 128), 16, 9, "reflect"),
+                                           ((2, 20, 32, 32), 16, 3, "wrap"),
+                                           ((2, 24, 48, 40), 8, 15, "reflect"),
+                                           ((1, 16, 20, 24), 32, 5, "reflect"),
+                                           ((2, 12, 9, 16), 16, 7, "wrap")])
+def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
+    """v1 (score.cu) and v2 (score2.cu) fused kernels both match the oracle."""
+    from paper_2510_15602_b200 import _native
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(sum(shape) + n + t)
+    x = np.maximum(rng.standard_normal(shape) + 0.2, 0).astype(np.float32)
+    cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
+    refs = [O.detect(x[i], n_bins=n, patch_size=t, pad=pad)[0] for i in range(shape[0])]
+    try:
+        for ver in (1, 2):
+            _native.call("qfca_set_score_kernel", ver)
+            res = Q.detect_batch(torch.from_numpy(x).cuda(), cfg)
+            for i in range(shape[0]):
+                e = rel_err(res.scores[i].cpu().numpy(), refs[i])
+                assert e <= TOL, (ver, i, e)
+    finally:
+        _native.call("qfca_set_score_kernel", 0)
