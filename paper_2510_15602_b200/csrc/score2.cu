@@ -1,5 +1,5 @@
 // score2.cu -- K4 v2: the fused scoring kernel, specialised for the default
-// family (uint8 bins, T <= 15 compile-time, a whole row of bins per CTA pass).
+// family (uint8 bins, compile-time T <= 15, all bins of a row in one pass).
 //
 // Same mathematics as score.cu (see its header) -- exact integer window
 // counts, closed-form Alg. 1, exact sliding box sums -- with a thread mapping
@@ -9,105 +9,106 @@
 //   of one channel; CPB channels ("slots") of one image share the CTA.
 //
 //   H1  vertical window counts as *thermometer* words: 8-bit lane j holds
-//       #{rows of the column window with bin <= 4g+j}; one column tracker per
-//       thread slides down the row stream (2 thermometer updates per row).
-//   H2  horizontal window: a (row, slot, group, 8-column segment) task slides
-//       the padded row of column words -> A_{4g+j}(y,x) directly (cumulative
-//       counts, no cross-word prefix; A_{4g-1} is lane 3 of group g-1).
+//       #{rows of the column window with bin <= 4g+j} (table lookup per bin);
+//       one column tracker per thread slides down the row stream.
+//   H2  horizontal window: a (row, slot, group, segment) task slides the padded
+//       row of column words -> A_{4g+j}(y,x) directly (cumulative counts; no
+//       cross-word prefix; A_{4g-1} is lane 3 of group g-1).
 //   E   per thread, per row, 4 bins: E_i = (G_i(A_i) - G_i(A_{i-1})) / P_i in
-//       fp32 from exact small integers; the vertical box sum keeps a T-row
-//       ring of E in REGISTERS (row loop unrolled by T, static slots),
-//       re-anchored every T rows (no drift).
-//   A   own-bin horizontal box from the per-row V planes, all slots of the
-//       CTA summed in fixed order, one RMW of the group partial per pixel.
+//       fp32 from exact small integers (byte -> float by PRMT magic, one
+//       MUFU.RCP); the vertical box keeps a T-row ring of E in REGISTERS (row
+//       loop unrolled by T, static slots), re-anchored every T rows.
+//   A   own-bin horizontal box from the per-row V planes, slots summed in
+//       fixed order, one RMW of the group partial per pixel; runs in the same
+//       phase as the next chunk's H1 (no dependency between them).
 //
-// Shared rows are skewed (one pad word per 8) so the 8-column segment tasks
-// of a warp hit distinct banks.
+// Shared-memory offsets are computed on the host and passed as kernel
+// parameters (no runtime layout arithmetic, no local-memory arrays).
+#include <string.h>
+
 #include "common.cuh"
 
 namespace qfca {
 
 constexpr int S2_THREADS = 512;
-constexpr int S2_SEG = 8;  // columns per H2 task
 
 struct Score2Geom {
     int h, w, n_bins, pad, C, groups, cpg;
-    int G;      // bin groups of 4 (ceil(N / 4))
-    int CPB;    // channels per CTA pass
-    int WP;     // padded row length (w + 2r), skewed storage length WPS
-    int WPS;
-    int S;      // stream rows h + 2r
+    int G;     // bin groups of 4 (ceil(N / 4))
+    int CPB;   // channels per CTA pass
+    int WP;    // padded row length w + 2r
+    int WPS;   // skewed storage length of a padded row
+    int S;     // stream rows h + 2r
+    int seg;   // H2 segment length
+    int nseg;  // H2 segments per row
+    // shared-memory byte offsets
+    int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, total;
 };
 
 __device__ __forceinline__ int skew(int p) { return p + (p >> 3); }
 
-__device__ __forceinline__ uint32_t thermo(int b, int g4) {
-    // lane j = [b <= g4 + j]
-    const int d = b - g4;
-    return d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 template <int T>
-struct S2Smem {
-    static constexpr int R = T / 2;
-};
-
-template <int T>
-__host__ __device__ inline size_t score2_smem(const Score2Geom& g, size_t* offs) {
-    size_t off = 0;
-    int k = 0;
-    auto take = [&](size_t bytes) {
-        if (offs) offs[k] = off;
-        ++k;
-        off = (off + bytes + 15) & ~(size_t)15;
+static void score2_layout(Score2Geom& g) {
+    int off = 0;
+    auto take = [&](long long bytes) {
+        const int o = off;
+        off = (int)((off + bytes + 15) & ~15LL);
+        return o;
     };
     const int np = g.G * 4;
-    take((size_t)g.CPB * g.h * g.w);                       // 0 bins planes (u8)
-    take((size_t)g.CPB * (T * T + 1) * 4);                 // 1 PJ tables (float)
-    take((size_t)g.CPB * np * 2 * 4);                      // 2 Vm / D per bin (float)
-    take((size_t)g.S * 4 * 4);                             // 3 stream table (int4)
-    take((size_t)T * g.CPB * g.G * g.WPS * 4);             // 4 CHp
-    take((size_t)T * g.CPB * g.G * g.w * 4);               // 5 WH
-    take((size_t)T * g.CPB * np * g.w * 4);                // 6 Vb
-    take((size_t)g.WP * 4);                                // 7 padded-x -> x map
-    take((size_t)g.CPB * 4);                               // 8 slot flags
-    return off;
+    g.o_bins = take((long long)g.CPB * g.h * g.w);
+    g.o_pj = take((long long)g.CPB * (T * T + 1) * 4);
+    g.o_vd = take((long long)g.CPB * np * 2 * 4);
+    g.o_stab = take((long long)g.S * 16);
+    g.o_chp = take((long long)T * g.CPB * g.G * g.WPS * 4);
+    g.o_wh = take((long long)T * g.CPB * g.G * g.w * 4);
+    g.o_vb = take((long long)T * g.CPB * np * g.w * 4);
+    g.o_xmap = take((long long)g.WP * 4);
+    g.o_scale = take((long long)g.CPB * 4);
+    g.o_th = take((long long)256 * g.G * 4);
+    g.total = off;
 }
 
 template <int T>
 __global__ void __launch_bounds__(S2_THREADS, 1)
 k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
-         const float* __restrict__ hi, const int32_t* __restrict__ Vref, Score2Geom g,
+         const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score2Geom g,
          float* __restrict__ partial) {
     constexpr int R = T / 2;
     constexpr int T2 = T * T;
     extern __shared__ __align__(16) uint8_t sm[];
-    size_t offs[9];
-    score2_smem<T>(g, offs);
-    uint8_t* sb = sm + offs[0];
-    float* sPJ = reinterpret_cast<float*>(sm + offs[1]);
-    float* sVD = reinterpret_cast<float*>(sm + offs[2]);
-    int4* stab = reinterpret_cast<int4*>(sm + offs[3]);
-    uint32_t* CHp = reinterpret_cast<uint32_t*>(sm + offs[4]);
-    uint32_t* WH = reinterpret_cast<uint32_t*>(sm + offs[5]);
-    float* Vb = reinterpret_cast<float*>(sm + offs[6]);
-    int* xmap = reinterpret_cast<int*>(sm + offs[7]);
-    float* sscale = reinterpret_cast<float*>(sm + offs[8]);
+    uint8_t* const sb = sm + g.o_bins;
+    float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
+    float* const sVD = reinterpret_cast<float*>(sm + g.o_vd);
+    int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);
+    uint32_t* const CHp = reinterpret_cast<uint32_t*>(sm + g.o_chp);
+    uint32_t* const WH = reinterpret_cast<uint32_t*>(sm + g.o_wh);
+    float* const Vb = reinterpret_cast<float*>(sm + g.o_vb);
+    int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
+    float* const sscale = reinterpret_cast<float*>(sm + g.o_scale);
+    uint32_t* const TH = reinterpret_cast<uint32_t*>(sm + g.o_th);
 
     const int tid = threadIdx.x;
     const int w = g.w, h = g.h, G = g.G, NP = G * 4;
     const int per_slot = G * w;
     const int cs = tid / per_slot;
     const int gx = tid - cs * per_slot;
-    const int grp4 = (gx / w) * 4;  // first bin of this thread's group
-    const int x = gx % w;
+    const int grp = gx / w;
+    const int grp4 = grp * 4;
+    const int x = gx - grp * w;
     const bool active = cs < g.CPB;
     const int img = blockIdx.x / g.groups, cg = blockIdx.x % g.groups;
     const int c_begin = cg * g.cpg, c_end = min(g.C, c_begin + g.cpg);
-    const int64_t hw = (int64_t)h * w;
-    float* part = partial + ((int64_t)img * g.groups + cg) * hw;
+    const int hw = h * w;
+    float* const part = partial + ((int64_t)img * g.groups + cg) * hw;
 
-    // ---- per-CTA geometry tables: stream rows and padded-x map
+    // ---- per-CTA tables: stream rows, padded-x map, thermometer words
     for (int s = tid; s < g.S; s += S2_THREADS) {
         const int e = s - R;
         const int ye = map_coord(e, h, g.pad);
@@ -115,23 +116,39 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         if (s > 0) {
             const int yp = map_coord(e - 1, h, g.pad);
             if (ye == yp + 1) { mode = 1; add = map_coord(ye + R, h, g.pad); rem = map_coord(yp - R, h, g.pad); }
-            else if (ye == yp - 1) { mode = 2; add = map_coord(ye - R, h, g.pad); rem = map_coord(yp + R, h, g.pad); }
-            else if (ye == yp) { mode = 3; }
+            else if (ye == yp - 1) { mode = 1; add = map_coord(ye - R, h, g.pad); rem = map_coord(yp + R, h, g.pad); }
+            else if (ye == yp) { mode = 2; }
         }
-        stab[s] = make_int4(ye, mode, add, rem);
+        stab[s] = make_int4(ye, mode, add * w, rem * w);
     }
     for (int p = tid; p < g.WP; p += S2_THREADS) xmap[p] = map_coord(p - R, w, g.pad);
+    for (int idx = tid; idx < 256 * G; idx += S2_THREADS) {
+        const int b = idx / G, q = idx % G, d = b - 4 * q;  // lane j = [b <= 4q + j]
+        TH[idx] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+    }
     __syncthreads();
-    // halo positions this thread's column feeds (padded p with xmap[p] == x, p outside [R, R+w))
-    uint32_t halo_mask = 0;
+    // padded positions (outside [R, R + w)) that this thread's column feeds
+    int halo0 = -1, halo1 = -1;
     if (active) {
         for (int j = 0; j < 2 * R; ++j) {
             const int p = j < R ? j : w + j;
-            if (xmap[p] == x) halo_mask |= 1u << j;
+            if (xmap[p] == x) {
+                if (halo0 < 0) halo0 = skew(p);
+                else if (halo1 < 0) halo1 = skew(p);
+            }
         }
     }
+    // a padded column can feed > 2 halo slots only for planes narrower than R
+    const bool many_halo = w <= R;
 
     const int n_chunks = (g.S + T - 1) / T;
+    const int cs_ = active ? cs : 0;
+    const uint8_t* const mb = sb + cs_ * hw;
+    const float* const pj = sPJ + cs_ * (T2 + 1);
+    uint32_t* const chp = CHp + (cs_ * G + grp) * g.WPS;
+    const int a_rows = S2_THREADS / w;  // A-phase rows per pass
+    const int a_x = tid % w, a_r0 = tid / w;
+
     for (int cb = c_begin; cb < c_end; cb += g.CPB) {
         // ---- load the slot channels: bins planes, reference tables
         __syncthreads();
@@ -139,55 +156,53 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             const int c = cb + k;
             const int64_t plane = (int64_t)img * g.C + c;
             if (tid == 0) {
-                // per-slot score scale w_c / T^2; 0 marks an empty or degenerate slot
-                float sc = 0.f;
+                float sc = 0.f;  // w_c / T^2; 0 marks an empty or degenerate slot
                 if (c < c_end && hi[plane] > lo[plane])
                     sc = (float)(((double)hi[plane] - (double)lo[plane]) / (double)g.n_bins /
                                  (double)T2);
                 sscale[k] = sc;
             }
-            uint8_t* dst = sb + (size_t)k * hw;
+            uint8_t* dst = sb + k * hw;
             if (c < c_end) {
                 const uint8_t* src = bins + plane * hw;
                 if ((hw & 15) == 0) {
                     const uint4* s4 = reinterpret_cast<const uint4*>(src);
                     uint4* d4 = reinterpret_cast<uint4*>(dst);
-                    for (int64_t i = tid; i < hw / 16; i += S2_THREADS) d4[i] = __ldg(s4 + i);
+                    for (int i = tid; i < hw / 16; i += S2_THREADS) d4[i] = __ldg(s4 + i);
                 } else {
-                    for (int64_t i = tid; i < hw; i += S2_THREADS) dst[i] = src[i];
+                    for (int i = tid; i < hw; i += S2_THREADS) dst[i] = src[i];
                 }
-                // PJ[x] = sum_{k<x} J_k, J_k = min{i : V_i > k}
                 const int32_t* V = Vref + plane * g.n_bins;
-                float* pj = sPJ + (size_t)k * (T2 + 1);
-                for (int q = tid; q < T2; q += S2_THREADS) {
+                float* pjk = sPJ + k * (T2 + 1);
+                for (int q = tid; q < T2; q += S2_THREADS) {  // J_q = min{i : V_i > q}
                     int a = 0, b = g.n_bins - 1;
                     while (a < b) {
                         const int mid = (a + b) >> 1;
                         if (__ldg(V + mid) > q) b = mid; else a = mid + 1;
                     }
-                    pj[q + 1] = (float)a;
+                    pjk[q + 1] = (float)a;
                 }
             } else {
-                for (int64_t i = tid; i < hw; i += S2_THREADS) dst[i] = 0;
-                for (int q = tid; q < T2; q += S2_THREADS) sPJ[(size_t)k * (T2 + 1) + q + 1] = 0.f;
+                for (int i = tid; i < hw; i += S2_THREADS) dst[i] = 0;
+                for (int q = tid; q < T2; q += S2_THREADS) sPJ[k * (T2 + 1) + q + 1] = 0.f;
             }
         }
         __syncthreads();
-        if (tid < 32 * g.CPB) {  // one warp per slot: inclusive scan of PJ[1..T2]
+        if (tid < 32 * g.CPB) {  // one warp per slot: PJ = inclusive prefix of J
             const int k = tid >> 5, lane = tid & 31;
-            float* pj = sPJ + (size_t)k * (T2 + 1);
+            float* pjk = sPJ + k * (T2 + 1);
             float carry = 0.f;
-            if (lane == 0) pj[0] = 0.f;
+            if (lane == 0) pjk[0] = 0.f;
             for (int base = 1; base <= T2; base += 32) {
                 const int q = base + lane;
-                float v = q <= T2 ? pj[q] : 0.f;
+                float v = q <= T2 ? pjk[q] : 0.f;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float u = __shfl_up_sync(0xffffffffu, v, o);
                     if (lane >= o) v += u;
                 }
                 v += carry;
-                if (q <= T2) pj[q] = v;
+                if (q <= T2) pjk[q] = v;
                 carry = __shfl_sync(0xffffffffu, v, 31);
             }
         }
@@ -200,21 +215,18 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 const int32_t* V = Vref + ((int64_t)img * g.C + c) * g.n_bins;
                 const int vmi = i > 0 ? V[i - 1] : 0;
                 vm = (float)vmi;
-                d = 2.f * ((float)i * vm - sPJ[(size_t)k * (T2 + 1) + vmi]);
+                d = 2.f * ((float)i * vm - sPJ[k * (T2 + 1) + vmi]);
             }
-            sVD[(size_t)(k * NP + i) * 2] = vm;
-            sVD[(size_t)(k * NP + i) * 2 + 1] = d;
+            sVD[(k * NP + i) * 2] = vm;
+            sVD[(k * NP + i) * 2 + 1] = d;
         }
         __syncthreads();
 
-        const int cs_ = active ? cs : 0;
-        const uint8_t* mb = sb + (size_t)cs_ * hw;
-        const float* pj = sPJ + (size_t)cs_ * (T2 + 1);
         float Vm[4], Dv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            Vm[j] = sVD[(size_t)(cs_ * NP + grp4 + j) * 2];
-            Dv[j] = sVD[(size_t)(cs_ * NP + grp4 + j) * 2 + 1];
+            Vm[j] = sVD[(cs_ * NP + grp4 + j) * 2];
+            Dv[j] = sVD[(cs_ * NP + grp4 + j) * 2 + 1];
         }
         uint32_t cst = 0;  // column tracker (thermometer word)
         float ring[T][4];
@@ -226,142 +238,154 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             for (int q = 0; q < T; ++q) ring[q][j] = 0.f;
         }
 
-        for (int ch = 0; ch < n_chunks; ++ch) {
+        for (int ch = 0; ch <= n_chunks; ++ch) {
             const int s0 = ch * T;
-            const int nrow = min(T, g.S - s0);
-            // ---- H1: vertical thermometer window counts for the chunk rows
-            if (active) {
-                uint32_t* chp = CHp + ((size_t)cs * G + grp4 / 4) * g.WPS;
+            // ---- phase 1: H1 of chunk ch  +  A of chunk ch-1
+            if (ch < n_chunks && active) {
+                const int nrow = min(T, g.S - s0);
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
                     if (rho < nrow) {
                         const int4 st = stab[s0 + rho];
-                        if (st.y == 0) {
+                        if (st.y == 1) {
+                            cst += TH[mb[st.z + x] * G + grp] - TH[mb[st.w + x] * G + grp];
+                        } else if (st.y == 0) {
                             cst = 0;
 #pragma unroll 1
                             for (int dy = -R; dy <= R; ++dy)
-                                cst += thermo(mb[map_coord(st.x + dy, h, g.pad) * w + x], grp4);
-                        } else if (st.y != 3) {
-                            cst += thermo(mb[st.z * w + x], grp4) - thermo(mb[st.w * w + x], grp4);
+                                cst += TH[mb[map_coord(st.x + dy, h, g.pad) * w + x] * G + grp];
                         }
-                        uint32_t* row = chp + (size_t)rho * g.CPB * G * g.WPS;
+                        uint32_t* row = chp + rho * g.CPB * G * g.WPS;
                         row[skew(x + R)] = cst;
-                        if (halo_mask) {
-                            for (int j = 0; j < 2 * R; ++j)
-                                if (halo_mask & (1u << j)) row[skew(j < R ? j : w + j)] = cst;
+                        if (halo0 >= 0) row[halo0] = cst;
+                        if (halo1 >= 0) row[halo1] = cst;
+                        if (many_halo) {
+                            for (int j = 0; j < 2 * R; ++j) {
+                                const int p = j < R ? j : w + j;
+                                if (xmap[p] == x) row[skew(p)] = cst;
+                            }
                         }
                     }
                 }
             }
+            if (ch > 0 && tid < a_rows * w) {
+                const int ps0 = s0 - T;
+                const int pnrow = min(T, g.S - ps0);
+                for (int rho = a_r0; rho < pnrow; rho += a_rows) {
+                    const int y = ps0 + rho - 2 * R;
+                    if (y < 0) continue;
+                    float acc = 0.f;
+                    for (int k = 0; k < g.CPB; ++k) {
+                        const float scale = sscale[k];
+                        if (scale == 0.f) continue;
+                        const int b = sb[k * hw + y * w + a_x];
+                        const float* vb = Vb + ((rho * g.CPB + k) * NP + b) * w;
+                        float f = 0.f;
+                        if (a_x >= R && a_x + R < w) {
+#pragma unroll
+                            for (int d = -R; d <= R; ++d) f += vb[a_x + d];
+                        } else {
+#pragma unroll
+                            for (int d = 0; d < T; ++d) f += vb[xmap[a_x + d]];
+                        }
+                        acc = fmaf(f, scale, acc);
+                    }
+                    part[y * w + a_x] += acc;
+                }
+            }
             __syncthreads();
-            // ---- H2: horizontal windows of the column words (segments of 8)
+            if (ch == n_chunks) break;
+            const int nrow = min(T, g.S - s0);
+            // ---- phase 2: H2, horizontal windows of the column words
             {
-                const int nseg = (w + S2_SEG - 1) / S2_SEG;
-                const int rows_tasks = nrow * g.CPB * G;
-                for (int task = tid; task < rows_tasks * nseg; task += S2_THREADS) {
-                    const int seg = task % nseg;
-                    const int rg = task / nseg;  // (rho * CPB + cs) * G + grp
-                    const uint32_t* src = CHp + (size_t)rg * g.WPS;
-                    uint32_t* dst = WH + (size_t)rg * w;
-                    const int x0 = seg * S2_SEG;
+                const int ntask = nrow * g.CPB * G * g.nseg;
+                for (int task = tid; task < ntask; task += S2_THREADS) {
+                    const int sg = task % g.nseg;
+                    const int rg = task / g.nseg;  // (rho * CPB + cs) * G + grp
+                    const uint32_t* src = CHp + rg * g.WPS;
+                    uint32_t* dst = WH + rg * w;
+                    const int x0 = sg * g.seg;
+                    const int x1 = min(w, x0 + g.seg);
                     uint32_t sum = 0;
 #pragma unroll
                     for (int p = 0; p < T; ++p) sum += src[skew(x0 + p)];
                     dst[x0] = sum;
-#pragma unroll
-                    for (int k = 1; k < S2_SEG; ++k) {
-                        const int xx = x0 + k;
-                        if (xx < w) {
-                            sum += src[skew(xx + 2 * R)] - src[skew(xx - 1)];
-                            dst[xx] = sum;
-                        }
+                    for (int xx = x0 + 1; xx < x1; ++xx) {
+                        sum += src[skew(xx + 2 * R)] - src[skew(xx - 1)];
+                        dst[xx] = sum;
                     }
                 }
             }
             __syncthreads();
-            // ---- E: closed-form transport + register ring + vertical box
+            // ---- phase 3: E, closed-form transport + register ring + vertical box
             if (active) {
-                const int grp = grp4 / 4;
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
                     if (rho < nrow) {
-                        const uint32_t* whr = WH + ((size_t)(rho * g.CPB + cs) * G) * w + x;
-                        const uint32_t word = whr[(size_t)grp * w];
-                        int a = grp > 0 ? (int)(whr[(size_t)(grp - 1) * w] >> 24) : 0;
-                        float af = (float)a;
-                        float pja = pj[a];
+                        const uint32_t* whr = WH + ((rho * g.CPB + cs) * G) * w + x;
+                        const uint32_t word = whr[grp * w];
+                        const uint32_t prev = grp > 0 ? whr[(grp - 1) * w] : 0u;
+                        // byte -> float by exponent magic: 0x4B0000bb = 2^23 + b
+                        uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                        float af = __uint_as_float(ma) - 8388608.0f;
+                        float pja = pj[ma - 0x4B000000u];
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
-                            const int b = (word >> (8 * j)) & 0xff;
-                            const float bf = (float)b;
-                            const float pjb = pj[b];
+                            const uint32_t mbits = __byte_perm(word, 0x4B000000u, 0x7650 + j);
+                            const float bf = __uint_as_float(mbits) - 8388608.0f;
+                            const float pjb = pj[mbits - 0x4B000000u];
                             const float fi = (float)(grp4 + j);
-                            const float ua = fmaf(-fi, af, pja);
-                            const float ub = fmaf(-fi, bf, pjb);
-                            const float ga = af < Vm[j] ? -ua : ua + Dv[j];
-                            const float gb = bf < Vm[j] ? -ub : ub + Dv[j];
+                            const float nua = fmaf(fi, af, -pja);  // -u(a)
+                            const float nub = fmaf(fi, bf, -pjb);  // -u(b)
+                            const float ga = af < Vm[j] ? nua : Dv[j] - nua;
+                            const float gb = bf < Vm[j] ? nub : Dv[j] - nub;
                             const float pc = bf - af;
-                            const float E = pc > 0.f ? __fdividef(gb - ga, pc) : 0.f;
+                            // pc == 0 -> gb == ga exactly -> E == 0
+                            const float E = (gb - ga) * rcp_approx(fmaxf(pc, 1.f));
                             vs[j] += E - ring[rho][j];
                             ring[rho][j] = E;
                             af = bf;
                             pja = pjb;
                         }
-                        if (rho == T - 1) {
+                        if (rho == T - 1) {  // re-anchor: exact sum of the ring
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                float s = 0.f;
+                                float s = ring[0][j];
 #pragma unroll
-                                for (int q = 0; q < T; ++q) s += ring[q][j];
+                                for (int q = 1; q < T; ++q) s += ring[q][j];
                                 vs[j] = s;
                             }
                         }
-                        const int y = s0 + rho - 2 * R;
-                        if (y >= 0) {
-                            float* vb = Vb + ((size_t)(rho * g.CPB + cs) * NP + grp4) * w + x;
+                        if (s0 + rho >= 2 * R) {
+                            float* vb = Vb + ((rho * g.CPB + cs) * NP + grp4) * w + x;
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) vb[(size_t)j * w] = vs[j];
+                            for (int j = 0; j < 4; ++j) vb[j * w] = vs[j];
                         }
                     }
                 }
             }
             __syncthreads();
-            // ---- A: own-bin horizontal box, slots summed in order, partial RMW
-            for (int task = tid; task < nrow * w; task += S2_THREADS) {
-                const int rho = task / w, xx = task % w;
-                const int y = s0 + rho - 2 * R;
-                if (y < 0) continue;
-                float acc = 0.f;
-                for (int k = 0; k < g.CPB; ++k) {
-                    const float scale = sscale[k];
-                    if (scale == 0.f) continue;
-                    const int b = sb[(size_t)k * hw + (size_t)y * w + xx];
-                    const float* vb = Vb + ((size_t)(rho * g.CPB + k) * NP + b) * w;
-                    float f = 0.f;
-                    if (xx >= R && xx + R < w) {
-#pragma unroll
-                        for (int d = -R; d <= R; ++d) f += vb[xx + d];
-                    } else {
-#pragma unroll
-                        for (int d = 0; d < T; ++d) f += vb[xmap[xx + d]];
-                    }
-                    acc += f * scale;
-                }
-                part[(size_t)y * w + xx] += acc;
-            }
         }
     }
+}
+
+template <int T>
+static int score2_plan_t(Score2Geom& g) {
+    score2_layout<T>(g);
+    return g.total;
 }
 
 static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
                        Score2Geom* out, size_t* smem_out) {
     if (t < 1 || t > 15 || (t & 1) == 0) return QFCA_ERR_UNSUPPORTED;
     if (n_bins > 256) return QFCA_ERR_UNSUPPORTED;
+    if ((int64_t)h * w > (1 << 24)) return QFCA_ERR_UNSUPPORTED;
     Score2Geom g;
+    memset(&g, 0, sizeof(g));
     g.h = h; g.w = w; g.n_bins = n_bins; g.pad = 0; g.C = C;
     g.G = (n_bins + 3) / 4;
     const int per = g.G * w;
-    if (per > S2_THREADS || w < 8) return QFCA_ERR_UNSUPPORTED;
+    if (per > S2_THREADS || w < 4) return QFCA_ERR_UNSUPPORTED;
     g.CPB = S2_THREADS / per;
     if (g.CPB > 8) g.CPB = 8;
     const int r = t / 2;
@@ -370,8 +394,14 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.S = h + 2 * r;
     size_t bytes = 0;
     for (;;) {
+        // H2 segments: one task per thread where possible
+        const int rows = t * g.CPB * g.G;
+        int nseg = S2_THREADS / rows;
+        nseg = nseg < 1 ? 1 : (nseg > w ? w : nseg);
+        g.seg = (w + nseg - 1) / nseg;
+        g.nseg = (w + g.seg - 1) / g.seg;
         switch (t) {
-#define QFCA_S2_CASE(TT) case TT: bytes = score2_smem<TT>(g, nullptr); break;
+#define QFCA_S2_CASE(TT) case TT: bytes = score2_plan_t<TT>(g); break;
             QFCA_S2_CASE(1) QFCA_S2_CASE(3) QFCA_S2_CASE(5) QFCA_S2_CASE(7)
             QFCA_S2_CASE(9) QFCA_S2_CASE(11) QFCA_S2_CASE(13) QFCA_S2_CASE(15)
 #undef QFCA_S2_CASE
