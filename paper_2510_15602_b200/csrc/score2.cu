@@ -41,6 +41,7 @@ struct Score2Geom {
     int S;     // stream rows h + 2r
     int seg;   // H2 segment length
     int nseg;  // H2 segments per row
+    int fastW; // compile-time-width variant in use (0 = runtime geometry)
     // shared-memory byte offsets
     int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, total;
 };
@@ -65,7 +66,7 @@ static void score2_layout(Score2Geom& g) {
     g.o_bins = take((long long)g.CPB * g.h * g.w);
     g.o_pj = take((long long)g.CPB * (T * T + 1) * 4);
     g.o_vd = take((long long)g.CPB * np * 2 * 4);
-    g.o_stab = take((long long)g.S * 16);
+    g.o_stab = take((long long)((g.S + T - 1) / T) * T * 16);
     g.o_chp = take((long long)T * g.CPB * g.G * g.WPS * 4);
     g.o_wh = take((long long)T * g.CPB * g.G * g.w * 4);
     g.o_vb = take((long long)T * g.CPB * np * g.w * 4);
@@ -75,13 +76,16 @@ static void score2_layout(Score2Geom& g) {
     g.total = off;
 }
 
-template <int T>
+// W > 0: compile-time plane width (32 / 64 / 128) with 4 bin groups (N <= 16),
+// so all index arithmetic folds to shifts; W == 0: runtime geometry.
+template <int T, int W>
 __global__ void __launch_bounds__(S2_THREADS, 1)
 k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
          const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score2Geom g,
          float* __restrict__ partial) {
     constexpr int R = T / 2;
     constexpr int T2 = T * T;
+    static_assert(W == 0 || (S2_THREADS % (4 * W)) == 0, "W must divide the CTA");
     extern __shared__ __align__(16) uint8_t sm[];
     uint8_t* const sb = sm + g.o_bins;
     float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
@@ -95,21 +99,29 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     uint32_t* const TH = reinterpret_cast<uint32_t*>(sm + g.o_th);
 
     const int tid = threadIdx.x;
-    const int w = g.w, h = g.h, G = g.G, NP = G * 4;
+    const int w = W ? W : g.w;
+    const int G = W ? 4 : g.G;
+    const int CPB = W ? S2_THREADS / (4 * W) : g.CPB;
+    const int h = g.h, NP = G * 4;
     const int per_slot = G * w;
     const int cs = tid / per_slot;
     const int gx = tid - cs * per_slot;
     const int grp = gx / w;
     const int grp4 = grp * 4;
     const int x = gx - grp * w;
-    const bool active = cs < g.CPB;
+    const bool active = cs < CPB;
     const int img = blockIdx.x / g.groups, cg = blockIdx.x % g.groups;
     const int c_begin = cg * g.cpg, c_end = min(g.C, c_begin + g.cpg);
     const int hw = h * w;
     float* const part = partial + ((int64_t)img * g.groups + cg) * hw;
 
     // ---- per-CTA tables: stream rows, padded-x map, thermometer words
-    for (int s = tid; s < g.S; s += S2_THREADS) {
+    const int n_chunks = (g.S + T - 1) / T;
+    for (int s = tid; s < n_chunks * T; s += S2_THREADS) {
+        if (s >= g.S) {  // padding rows of the last chunk: tracker stays put
+            stab[s] = make_int4(0, 2, 0, 0);
+            continue;
+        }
         const int e = s - R;
         const int ye = map_coord(e, h, g.pad);
         int mode = 0, add = 0, rem = 0;
@@ -141,7 +153,6 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     // a padded column can feed > 2 halo slots only for planes narrower than R
     const bool many_halo = w <= R;
 
-    const int n_chunks = (g.S + T - 1) / T;
     const int cs_ = active ? cs : 0;
     const uint8_t* const mb = sb + cs_ * hw;
     const float* const pj = sPJ + cs_ * (T2 + 1);
@@ -149,10 +160,10 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int a_rows = S2_THREADS / w;  // A-phase rows per pass
     const int a_x = tid % w, a_r0 = tid / w;
 
-    for (int cb = c_begin; cb < c_end; cb += g.CPB) {
+    for (int cb = c_begin; cb < c_end; cb += CPB) {
         // ---- load the slot channels: bins planes, reference tables
         __syncthreads();
-        for (int k = 0; k < g.CPB; ++k) {
+        for (int k = 0; k < CPB; ++k) {
             const int c = cb + k;
             const int64_t plane = (int64_t)img * g.C + c;
             if (tid == 0) {
@@ -188,7 +199,7 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
         __syncthreads();
-        if (tid < 32 * g.CPB) {  // one warp per slot: PJ = inclusive prefix of J
+        if (tid < 32 * CPB) {  // one warp per slot: PJ = inclusive prefix of J
             const int k = tid >> 5, lane = tid & 31;
             float* pjk = sPJ + k * (T2 + 1);
             float carry = 0.f;
@@ -207,7 +218,7 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
         __syncthreads();
-        for (int idx = tid; idx < g.CPB * NP; idx += S2_THREADS) {
+        for (int idx = tid; idx < CPB * NP; idx += S2_THREADS) {
             const int k = idx / NP, i = idx % NP;
             const int c = cb + k;
             float vm = 0.f, d = 0.f;
@@ -238,48 +249,45 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             for (int q = 0; q < T; ++q) ring[q][j] = 0.f;
         }
 
+        // the stream is padded to whole chunks of T rows (stab mode 2 = no move)
         for (int ch = 0; ch <= n_chunks; ++ch) {
             const int s0 = ch * T;
             // ---- phase 1: H1 of chunk ch  +  A of chunk ch-1
             if (ch < n_chunks && active) {
-                const int nrow = min(T, g.S - s0);
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
-                    if (rho < nrow) {
-                        const int4 st = stab[s0 + rho];
-                        if (st.y == 1) {
-                            cst += TH[mb[st.z + x] * G + grp] - TH[mb[st.w + x] * G + grp];
-                        } else if (st.y == 0) {
-                            cst = 0;
+                    const int4 st = stab[s0 + rho];
+                    if (st.y == 1) {
+                        cst += TH[mb[st.z + x] * G + grp] - TH[mb[st.w + x] * G + grp];
+                    } else if (st.y == 0) {
+                        cst = 0;
 #pragma unroll 1
-                            for (int dy = -R; dy <= R; ++dy)
-                                cst += TH[mb[map_coord(st.x + dy, h, g.pad) * w + x] * G + grp];
-                        }
-                        uint32_t* row = chp + rho * g.CPB * G * g.WPS;
-                        row[skew(x + R)] = cst;
-                        if (halo0 >= 0) row[halo0] = cst;
-                        if (halo1 >= 0) row[halo1] = cst;
-                        if (many_halo) {
-                            for (int j = 0; j < 2 * R; ++j) {
-                                const int p = j < R ? j : w + j;
-                                if (xmap[p] == x) row[skew(p)] = cst;
-                            }
+                        for (int dy = -R; dy <= R; ++dy)
+                            cst += TH[mb[map_coord(st.x + dy, h, g.pad) * w + x] * G + grp];
+                    }
+                    uint32_t* row = chp + rho * CPB * G * g.WPS;
+                    row[skew(x + R)] = cst;
+                    if (halo0 >= 0) row[halo0] = cst;
+                    if (halo1 >= 0) row[halo1] = cst;
+                    if (many_halo) {
+                        for (int j = 0; j < 2 * R; ++j) {
+                            const int p = j < R ? j : w + j;
+                            if (xmap[p] == x) row[skew(p)] = cst;
                         }
                     }
                 }
             }
             if (ch > 0 && tid < a_rows * w) {
                 const int ps0 = s0 - T;
-                const int pnrow = min(T, g.S - ps0);
-                for (int rho = a_r0; rho < pnrow; rho += a_rows) {
+                for (int rho = a_r0; rho < T; rho += a_rows) {
                     const int y = ps0 + rho - 2 * R;
-                    if (y < 0) continue;
+                    if (y < 0 || y >= h) continue;
                     float acc = 0.f;
-                    for (int k = 0; k < g.CPB; ++k) {
+                    for (int k = 0; k < CPB; ++k) {
                         const float scale = sscale[k];
                         if (scale == 0.f) continue;
                         const int b = sb[k * hw + y * w + a_x];
-                        const float* vb = Vb + ((rho * g.CPB + k) * NP + b) * w;
+                        const float* vb = Vb + ((rho * CPB + k) * NP + b) * w;
                         float f = 0.f;
                         if (a_x >= R && a_x + R < w) {
 #pragma unroll
@@ -295,10 +303,9 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
             __syncthreads();
             if (ch == n_chunks) break;
-            const int nrow = min(T, g.S - s0);
             // ---- phase 2: H2, horizontal windows of the column words
             {
-                const int ntask = nrow * g.CPB * G * g.nseg;
+                const int ntask = T * CPB * G * g.nseg;
                 for (int task = tid; task < ntask; task += S2_THREADS) {
                     const int sg = task % g.nseg;
                     const int rg = task / g.nseg;  // (rho * CPB + cs) * G + grp
@@ -321,12 +328,15 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             if (active) {
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
-                    if (rho < nrow) {
-                        const uint32_t* whr = WH + ((rho * g.CPB + cs) * G) * w + x;
-                        const uint32_t word = whr[grp * w];
-                        const uint32_t prev = grp > 0 ? whr[(grp - 1) * w] : 0u;
+                    const uint32_t* whr = WH + ((rho * CPB + cs) * G) * w + x;
+                    const uint32_t word = whr[grp * w];
+                    const uint32_t prev = grp > 0 ? whr[(grp - 1) * w] : 0u;
+                    // the group has mass in this window iff A_{4g+3} > A_{4g-1};
+                    // groups empty across the whole warp contribute E = 0
+                    const bool mass = (word >> 24) != (prev >> 24);
+                    if (__any_sync(__activemask(), mass)) {
                         // byte -> float by exponent magic: 0x4B0000bb = 2^23 + b
-                        uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                        const uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
                         float af = __uint_as_float(ma) - 8388608.0f;
                         float pja = pj[ma - 0x4B000000u];
 #pragma unroll
@@ -347,20 +357,26 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             af = bf;
                             pja = pjb;
                         }
-                        if (rho == T - 1) {  // re-anchor: exact sum of the ring
+                    } else {
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                float s = ring[0][j];
-#pragma unroll
-                                for (int q = 1; q < T; ++q) s += ring[q][j];
-                                vs[j] = s;
-                            }
+                        for (int j = 0; j < 4; ++j) {
+                            vs[j] -= ring[rho][j];
+                            ring[rho][j] = 0.f;
                         }
-                        if (s0 + rho >= 2 * R) {
-                            float* vb = Vb + ((rho * g.CPB + cs) * NP + grp4) * w + x;
+                    }
+                    if (rho == T - 1) {  // re-anchor: exact sum of the ring
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) vb[j * w] = vs[j];
+                        for (int j = 0; j < 4; ++j) {
+                            float s = ring[0][j];
+#pragma unroll
+                            for (int q = 1; q < T; ++q) s += ring[q][j];
+                            vs[j] = s;
                         }
+                    }
+                    if (s0 + rho >= 2 * R) {
+                        float* vb = Vb + ((rho * CPB + cs) * NP + grp4) * w + x;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) vb[j * w] = vs[j];
                     }
                 }
             }
@@ -383,7 +399,10 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     Score2Geom g;
     memset(&g, 0, sizeof(g));
     g.h = h; g.w = w; g.n_bins = n_bins; g.pad = 0; g.C = C;
-    g.G = (n_bins + 3) / 4;
+    // compile-time-width variant: w in {32, 64, 128}, 4 groups (N <= 16)
+    const bool fast = n_bins <= 16 && (w == 32 || w == 64 || w == 128);
+    g.fastW = fast ? w : 0;
+    g.G = fast ? 4 : (n_bins + 3) / 4;
     const int per = g.G * w;
     if (per > S2_THREADS || w < 4) return QFCA_ERR_UNSUPPORTED;
     g.CPB = S2_THREADS / per;
@@ -407,6 +426,13 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
 #undef QFCA_S2_CASE
         }
         if (bytes <= 225 * 1024) break;
+        if (g.fastW) {  // the fixed-width variant needs its full slot count
+            g.fastW = 0;
+            g.G = (n_bins + 3) / 4;
+            g.CPB = S2_THREADS / (g.G * w);
+            if (g.CPB > 8) g.CPB = 8;
+            continue;
+        }
         if (g.CPB > 1) { g.CPB--; continue; }
         return QFCA_ERR_UNSUPPORTED;
     }
@@ -446,21 +472,24 @@ int launch_score2(const void* bins, int bins_bytes, const float* lo, const float
     if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
     g.pad = pad;
     const int64_t grid = images * g.groups;
-    cudaError_t e = cudaSuccess;
-    switch (t) {
-#define QFCA_S2_LAUNCH(TT)                                                                   \
-    case TT:                                                                                 \
-        e = cudaFuncSetAttribute(k_score2<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                 (int)smem);                                                 \
-        if (e != cudaSuccess) return QFCA_ERR_CUDA;                                          \
-        k_score2<TT><<<(unsigned)grid, S2_THREADS, smem, st>>>((const uint8_t*)bins, lo, hi, \
-                                                               V, g, partial);               \
+    void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score2Geom,
+                 float*) = nullptr;
+#define QFCA_S2_PICK(TT)                                                       \
+    case TT:                                                                   \
+        kern = g.fastW == 128 ? k_score2<TT, 128>                              \
+             : g.fastW == 64  ? k_score2<TT, 64>                               \
+             : g.fastW == 32  ? k_score2<TT, 32> : k_score2<TT, 0>;            \
         break;
-        QFCA_S2_LAUNCH(1) QFCA_S2_LAUNCH(3) QFCA_S2_LAUNCH(5) QFCA_S2_LAUNCH(7)
-        QFCA_S2_LAUNCH(9) QFCA_S2_LAUNCH(11) QFCA_S2_LAUNCH(13) QFCA_S2_LAUNCH(15)
-#undef QFCA_S2_LAUNCH
+    switch (t) {
+        QFCA_S2_PICK(1) QFCA_S2_PICK(3) QFCA_S2_PICK(5) QFCA_S2_PICK(7)
+        QFCA_S2_PICK(9) QFCA_S2_PICK(11) QFCA_S2_PICK(13) QFCA_S2_PICK(15)
         default: return QFCA_ERR_UNSUPPORTED;
     }
+#undef QFCA_S2_PICK
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    kern<<<(unsigned)grid, S2_THREADS, smem, st>>>((const uint8_t*)bins, lo, hi, V, g, partial);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
