@@ -106,9 +106,12 @@ int qfca_channel_sum(const double* score, int64_t images, int32_t channels, int6
 int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t channels,
                     int32_t* used, void* stream);
 
-/* channel groups qfca_score will use (host-only) for groups_hint (<= 0: auto) */
+/* channel groups qfca_score will use (host-only) for groups_hint (<= 0: auto);
+ * with_reference = 0 asks for the in-kernel reference selection (returns -1
+ * where that is not available). */
 int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, int32_t channels,
-                      int64_t images, int32_t groups_hint);
+                      int64_t images, int32_t groups_hint, int32_t pad, int32_t sample_budget,
+                      int32_t with_reference);
 
 /* select the fused scoring kernel: 0 = auto (v2 -- compile-time patch size
  * T <= 15, uint8 bins, 4 * G * w <= 512 -- where it applies, else v1),
@@ -117,13 +120,15 @@ int qfca_set_score_kernel(int32_t version);
 
 /* THE HOT PATH: _channel_score_kernel + channel accumulation
  * (scoring.py:205-260, 286-309) fused, for uniform sigma_p, median-quan and
- * reflect / wrap padding.  ref_cum = qfca_select_reference mode-0 stats.
+ * reflect / wrap padding.  ref_cum = qfca_select_reference mode-0 stats, or
+ * NULL to select the reference inside the kernel (select_reference,
+ * quantize.py:150-200, from the same window counts; sample_budget applies).
  * partial: (images, groups, h, w) float32, must be zeroed by the caller; each
  * group adds its channels' scores in fixed channel order. */
 int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
                const int32_t* ref_cum, int64_t images, int32_t channels, int32_t h, int32_t w,
-               int32_t n_bins, int32_t patch_size, int32_t pad, int32_t groups, float* partial,
-               void* stream);
+               int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
+               int32_t groups, float* partial, void* stream);
 
 /* agg = (sum over groups, fixed order, fp64) / used   (scoring.py:311-317) */
 int qfca_reduce_partials(const float* partial, int64_t images, int32_t groups, int64_t hw,

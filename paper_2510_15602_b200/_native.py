@@ -47,9 +47,9 @@ _SIGNATURES = {
     "qfca_channel_sum": ([_P, _I64, _I32, _I64, _P, _I32, _P, _P, _P], _I32),
     "qfca_count_used": ([_P, _P, _I64, _I32, _P, _P], _I32),
     "qfca_set_score_kernel": ([_I32], _I32),
-    "qfca_score_groups": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32], _I32),
-    "qfca_score": ([_P, _I32, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P,
-                    _P], _I32),
+    "qfca_score_groups": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32], _I32),
+    "qfca_score": ([_P, _I32, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                    _P, _P], _I32),
     "qfca_reduce_partials": ([_P, _I64, _I32, _I64, _P, _P, _P], _I32),
     "qfca_divide_used": ([_P, _I64, _I64, _P, _P, _P], _I32),
     "qfca_sep_conv": ([_P, _I64, _I32, _I32, _I32, _P, _I32, _I32, _P, _P], _I32),

@@ -38,35 +38,50 @@ int launch_upsample(const double*, int64_t, int, int, int, int, float*, cudaStre
 int launch_pca_residual(const float*, int64_t, int, int64_t, const double*, const double*, int,
                         int, float*, cudaStream_t);
 int launch_center(const float*, int64_t, int64_t, const double*, float*, cudaStream_t);
-int score2_groups(int, int, int, int, int, int64_t, int);
+int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int launch_score2(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
-                  int, int, int, int, int, float*, cudaStream_t);
+                  int, int, int, int, int, int, float*, cudaStream_t);
 
 // fused-kernel selection: 0 = auto (v2 where it applies, else v1), 1 / 2 = force
 static int g_score_kernel = 0;
 
-static bool use_v2(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
-                   int bins_bytes) {
-    if (g_score_kernel == 1 || bins_bytes != 1) return false;
-    return score2_groups(h, w, n_bins, t, C, images, groups_hint) > 0;
+struct ScoreChoice {
+    int groups;  // channel groups (partial maps per image); <= 0: unsupported
+    int v2;      // 1: score2.cu, 0: score.cu
+    int fref;    // 1: the reference is selected inside the kernel
+};
+
+// want_fref: the caller has no reference (V) and wants the kernel to select it
+static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t images,
+                                int groups_hint, int bins_bytes, int pad, int budget,
+                                int want_fref) {
+    ScoreChoice ch{-1, 0, 0};
+    if (g_score_kernel != 1 && bins_bytes == 1) {
+        int fr = 0;
+        const int gg = score2_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
+                                    want_fref, &fr);
+        if (gg > 0) {
+            ch.groups = gg;
+            ch.v2 = 1;
+            ch.fref = fr;
+            return ch;
+        }
+    }
+    if (g_score_kernel == 2) return ch;
+    ch.groups = score_groups(h, w, n_bins, t, C, images, groups_hint);
+    return ch;
 }
 
-static int score_groups_any(int h, int w, int n_bins, int t, int C, int64_t images,
-                            int groups_hint, int bins_bytes) {
-    if (use_v2(h, w, n_bins, t, C, images, groups_hint, bins_bytes))
-        return score2_groups(h, w, n_bins, t, C, images, groups_hint);
-    if (g_score_kernel == 2) return -1;
-    return score_groups(h, w, n_bins, t, C, images, groups_hint);
-}
-
-static int launch_score_any(const void* bins, int bins_bytes, const float* lo, const float* hi,
-                            const int32_t* V, int64_t images, int C, int h, int w, int n_bins,
-                            int t, int pad, int groups, float* partial, cudaStream_t st) {
-    if (use_v2(h, w, n_bins, t, C, images, groups, bins_bytes))
-        return launch_score2(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, groups,
-                             partial, st);
-    if (g_score_kernel == 2) return QFCA_ERR_UNSUPPORTED;
-    return launch_score(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, groups,
+static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_bytes,
+                            const float* lo, const float* hi, const int32_t* V, int64_t images,
+                            int C, int h, int w, int n_bins, int t, int pad, int budget,
+                            float* partial, cudaStream_t st) {
+    if (ch.groups <= 0) return QFCA_ERR_UNSUPPORTED;
+    if (ch.v2)
+        return launch_score2(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
+                             n_bins, t, pad, budget, ch.groups, partial, st);
+    if (!V) return QFCA_ERR_UNSUPPORTED;
+    return launch_score(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, ch.groups,
                         partial, st);
 }
 }  // namespace qfca
@@ -167,9 +182,13 @@ int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t ch
 }
 
 int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, int32_t channels,
-                      int64_t images, int32_t groups_hint) {
-    return score_groups_any(h, w, n_bins, patch_size, channels, images, groups_hint,
-                            n_bins <= 256 ? 1 : 2);
+                      int64_t images, int32_t groups_hint, int32_t pad, int32_t sample_budget,
+                      int32_t with_reference) {
+    const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, groups_hint,
+                                        n_bins <= 256 ? 1 : 2, pad, sample_budget,
+                                        with_reference ? 0 : 1);
+    if (!with_reference && !ch.fref) return -1;
+    return ch.groups;
 }
 
 int qfca_set_score_kernel(int32_t version) {
@@ -180,10 +199,15 @@ int qfca_set_score_kernel(int32_t version) {
 
 int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
                const int32_t* ref_cum, int64_t images, int32_t channels, int32_t h, int32_t w,
-               int32_t n_bins, int32_t patch_size, int32_t pad, int32_t groups, float* partial,
-               void* stream) {
-    return counted(launch_score_any(bins, bins_bytes, lo, hi, ref_cum, images, channels, h, w,
-                                    n_bins, patch_size, pad, groups, partial, S(stream)), 1);
+               int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
+               int32_t groups, float* partial, void* stream) {
+    const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, groups,
+                                        bins_bytes, pad, sample_budget, ref_cum ? 0 : 1);
+    if (groups > 0 && ch.groups != groups) return QFCA_ERR_ARG;
+    if (!ref_cum && !ch.fref) return QFCA_ERR_UNSUPPORTED;
+    return counted(launch_score_any(ch, bins, bins_bytes, lo, hi, ref_cum, images, channels, h,
+                                    w, n_bins, patch_size, pad, sample_budget, partial, S(stream)),
+                   1);
 }
 
 int qfca_reduce_partials(const float* partial, int64_t images, int32_t groups, int64_t hw,
@@ -233,6 +257,7 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
 struct DetectLayout {
     size_t lo, hi, bins, V, partial, used_scratch, agg, tmp, total;
     int groups, bins_bytes;
+    ScoreChoice choice;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -246,8 +271,9 @@ static int detect_layout(int64_t images, int32_t C, int32_t h, int32_t w, const 
     if (cfg->pad != QFCA_PAD_REFLECT && cfg->pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
     const int64_t planes = images * C, hw = (int64_t)h * w;
     L->bins_bytes = cfg->n_bins <= 256 ? 1 : 2;
-    L->groups = score_groups_any(h, w, cfg->n_bins, cfg->patch_size, C, images, cfg->groups,
-                                 L->bins_bytes);
+    L->choice = score_choose(h, w, cfg->n_bins, cfg->patch_size, C, images, cfg->groups,
+                             L->bins_bytes, cfg->pad, cfg->sample_budget, 1);
+    L->groups = L->choice.groups;
     if (L->groups <= 0) return QFCA_ERR_UNSUPPORTED;
     size_t off = 0;
     L->lo = off; off = align256(off + planes * 4);
@@ -311,8 +337,10 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
     if ((rc = counted(launch_minmax(features, planes, hw, lo, hi, nonfinite, st), 1))) return rc;
     if ((rc = counted(launch_bin(features, planes, hw, lo, hi, cfg->n_bins, bins, L.bins_bytes, st), 1)))
         return rc;
-    if ((rc = counted(launch_reference(bins, L.bins_bytes, lo, hi, planes, h, w, cfg->n_bins,
-                               cfg->patch_size, cfg->pad, cfg->sample_budget, 0, V, st), 1)))
+    if (!L.choice.fref &&  // else the scoring kernel selects the reference itself
+        (rc = counted(launch_reference(bins, L.bins_bytes, lo, hi, planes, h, w, cfg->n_bins,
+                                       cfg->patch_size, cfg->pad, cfg->sample_budget, 0, V, st),
+                      1)))
         return rc;
     if ((rc = counted(launch_count_used(lo, hi, images, C, used, st), 1))) return rc;
     if (cudaMemsetAsync(partial, 0, images * (int64_t)L.groups * hw * 4, st) != cudaSuccess)
@@ -320,8 +348,10 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
     if (stage_events && stage_events[0] &&
         cudaEventRecord((cudaEvent_t)stage_events[0], st) != cudaSuccess)
         return QFCA_ERR_CUDA;
-    if ((rc = counted(launch_score_any(bins, L.bins_bytes, lo, hi, V, images, C, h, w, cfg->n_bins,
-                           cfg->patch_size, cfg->pad, L.groups, partial, st), 1)))
+    if ((rc = counted(launch_score_any(L.choice, bins, L.bins_bytes, lo, hi, V, images, C, h, w,
+                                       cfg->n_bins, cfg->patch_size, cfg->pad,
+                                       cfg->sample_budget, partial, st),
+                      1)))
         return rc;
     if (stage_events && stage_events[1] &&
         cudaEventRecord((cudaEvent_t)stage_events[1], st) != cudaSuccess)

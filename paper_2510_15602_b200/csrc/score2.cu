@@ -42,8 +42,10 @@ struct Score2Geom {
     int seg;   // H2 segment length
     int nseg;  // H2 segments per row
     int fastW; // compile-time-width variant in use (0 = runtime geometry)
+    // fused reference selection (pass 0): sample grid of quantize.py:109-116
+    int fref, stride, nsx, nsamp, sp;  // sp = nsamp rounded up to 4
     // shared-memory byte offsets
-    int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, total;
+    int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, o_sv, o_sa, total;
 };
 
 __device__ __forceinline__ int skew(int p) { return p + (p >> 3); }
@@ -73,6 +75,8 @@ static void score2_layout(Score2Geom& g) {
     g.o_xmap = take((long long)g.WP * 4);
     g.o_scale = take((long long)g.CPB * 4);
     g.o_th = take((long long)256 * g.G * 4);
+    g.o_sv = take((long long)g.CPB * np * 4);
+    g.o_sa = take(g.fref ? (long long)g.CPB * np * g.sp : 0);
     g.total = off;
 }
 
@@ -97,6 +101,8 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
     float* const sscale = reinterpret_cast<float*>(sm + g.o_scale);
     uint32_t* const TH = reinterpret_cast<uint32_t*>(sm + g.o_th);
+    int* const sV = reinterpret_cast<int*>(sm + g.o_sv);
+    uint8_t* const SA = sm + g.o_sa;
 
     const int tid = threadIdx.x;
     const int w = W ? W : g.w;
@@ -160,6 +166,57 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int a_rows = S2_THREADS / w;  // A-phase rows per pass
     const int a_x = tid % w, a_r0 = tid / w;
 
+    // H1 for the T stream rows of chunk starting at s0 (column trackers)
+    uint32_t cst = 0;  // column tracker (thermometer word)
+    auto h1_chunk = [&](int s0) {
+#pragma unroll
+        for (int rho = 0; rho < T; ++rho) {
+            const int4 st = stab[s0 + rho];
+            if (st.y == 1) {
+                cst += TH[mb[st.z + x] * G + grp] - TH[mb[st.w + x] * G + grp];
+            } else if (st.y == 0) {
+                cst = 0;
+#pragma unroll 1
+                for (int dy = -R; dy <= R; ++dy)
+                    cst += TH[mb[map_coord(st.x + dy, h, g.pad) * w + x] * G + grp];
+            }
+            uint32_t* row = chp + rho * CPB * G * g.WPS;
+            row[skew(x + R)] = cst;
+            if (halo0 >= 0) row[halo0] = cst;
+            if (halo1 >= 0) row[halo1] = cst;
+            if (many_halo) {
+                for (int j = 0; j < 2 * R; ++j) {
+                    const int p = j < R ? j : w + j;
+                    if (xmap[p] == x) row[skew(p)] = cst;
+                }
+            }
+        }
+    };
+    // H2 for the chunk starting at s0; only_samples: just the sample rows
+    auto h2_chunk = [&](int s0, bool only_samples) {
+        const int ntask = T * CPB * G * g.nseg;
+        for (int task = tid; task < ntask; task += S2_THREADS) {
+            const int sg = task % g.nseg;
+            const int rg = task / g.nseg;  // (rho * CPB + cs) * G + grp
+            if (only_samples) {
+                const int e = s0 + rg / (CPB * G) - R;
+                if (e < 0 || e >= h || e % g.stride) continue;
+            }
+            const uint32_t* src = CHp + rg * g.WPS;
+            uint32_t* dst = WH + rg * w;
+            const int x0 = sg * g.seg;
+            const int x1 = min(w, x0 + g.seg);
+            uint32_t sum = 0;
+#pragma unroll
+            for (int p = 0; p < T; ++p) sum += src[skew(x0 + p)];
+            dst[x0] = sum;
+            for (int xx = x0 + 1; xx < x1; ++xx) {
+                sum += src[skew(xx + 2 * R)] - src[skew(xx - 1)];
+                dst[xx] = sum;
+            }
+        }
+    };
+
     for (int cb = c_begin; cb < c_end; cb += CPB) {
         // ---- load the slot channels: bins planes, reference tables
         __syncthreads();
@@ -183,19 +240,79 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 } else {
                     for (int i = tid; i < hw; i += S2_THREADS) dst[i] = src[i];
                 }
-                const int32_t* V = Vref + plane * g.n_bins;
-                float* pjk = sPJ + k * (T2 + 1);
-                for (int q = tid; q < T2; q += S2_THREADS) {  // J_q = min{i : V_i > q}
-                    int a = 0, b = g.n_bins - 1;
-                    while (a < b) {
-                        const int mid = (a + b) >> 1;
-                        if (__ldg(V + mid) > q) b = mid; else a = mid + 1;
-                    }
-                    pjk[q + 1] = (float)a;
-                }
+                if (!g.fref)
+                    for (int i = tid; i < NP; i += S2_THREADS)
+                        sV[k * NP + i] = i < g.n_bins ? __ldg(Vref + plane * g.n_bins + i) : T2;
             } else {
                 for (int i = tid; i < hw; i += S2_THREADS) dst[i] = 0;
-                for (int q = tid; q < T2; q += S2_THREADS) sPJ[k * (T2 + 1) + q + 1] = 0.f;
+                for (int i = tid; i < NP; i += S2_THREADS) sV[k * NP + i] = T2;
+            }
+        }
+        __syncthreads();
+        if (g.fref) {
+            // ---- pass 0: the global reference, fused (quantize.py:150-200).  The
+            // window counts at the stride-grid samples come from the same trackers;
+            // V_i = the (S-1-m)-th smallest A_i over the samples (reference.cu).
+            for (int ch = 0; ch < n_chunks; ++ch) {
+                const int s0 = ch * T;
+                if (active) h1_chunk(s0);
+                __syncthreads();
+                h2_chunk(s0, true);
+                __syncthreads();
+                if (active && x % g.stride == 0) {
+                    uint8_t* sa = SA + (cs * NP + grp4) * g.sp + x / g.stride;
+#pragma unroll
+                    for (int rho = 0; rho < T; ++rho) {
+                        const int e = s0 + rho - R;
+                        if (e < 0 || e >= h || e % g.stride) continue;
+                        const uint32_t word = WH[((rho * CPB + cs) * G + grp) * w + x];
+                        const int si = (e / g.stride) * g.nsx;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
+                    }
+                }
+            }
+            // pad each sample row with values above any query (packed compares)
+            for (int idx = tid; idx < CPB * NP * (g.sp - g.nsamp); idx += S2_THREADS) {
+                const int row = idx / (g.sp - g.nsamp), k = idx % (g.sp - g.nsamp);
+                SA[row * g.sp + g.nsamp + k] = 127;
+            }
+            __syncthreads();
+            {  // one warp per (slot, bin): smallest v with #{A <= v} >= S - m
+                const int warp = tid >> 5, lane = tid & 31;
+                const int c0 = g.nsamp - (g.nsamp - 1) / 2;
+                for (int task = warp; task < CPB * NP; task += S2_THREADS / 32) {
+                    const int k = task / NP, i = task % NP;
+                    int res = T2;
+                    if (i < g.n_bins - 1 && sscale[k] != 0.f) {
+                        const uint32_t* row = reinterpret_cast<const uint32_t*>(SA + task * g.sp);
+                        int a = 0, b = T2;
+                        while (a < b) {
+                            const int mid = (a + b) >> 1;
+                            const uint32_t q = 0x80808080u | ((uint32_t)mid * 0x01010101u);
+                            int cnt = 0;
+                            for (int wi = lane; wi < g.sp / 4; wi += 32)
+                                cnt += __popc((q - row[wi]) & 0x80808080u);
+                            cnt = warp_sum_i(cnt);
+                            if (cnt >= c0) b = mid; else a = mid + 1;
+                        }
+                        res = a;
+                    }
+                    if (lane == 0) sV[task] = res;
+                }
+            }
+            __syncthreads();
+        }
+        for (int k = 0; k < CPB; ++k) {
+            float* pjk = sPJ + k * (T2 + 1);
+            const int* V = sV + k * NP;
+            for (int q = tid; q < T2; q += S2_THREADS) {  // J_q = min{i : V_i > q}
+                int a = 0, b = g.n_bins - 1;
+                while (a < b) {
+                    const int mid = (a + b) >> 1;
+                    if (V[mid] > q) b = mid; else a = mid + 1;
+                }
+                pjk[q + 1] = (float)a;
             }
         }
         __syncthreads();
@@ -220,11 +337,9 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         __syncthreads();
         for (int idx = tid; idx < CPB * NP; idx += S2_THREADS) {
             const int k = idx / NP, i = idx % NP;
-            const int c = cb + k;
             float vm = 0.f, d = 0.f;
-            if (c < c_end && i < g.n_bins) {
-                const int32_t* V = Vref + ((int64_t)img * g.C + c) * g.n_bins;
-                const int vmi = i > 0 ? V[i - 1] : 0;
+            if (i < g.n_bins) {
+                const int vmi = i > 0 ? sV[k * NP + i - 1] : 0;
                 vm = (float)vmi;
                 d = 2.f * ((float)i * vm - sPJ[k * (T2 + 1) + vmi]);
             }
@@ -239,7 +354,6 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             Vm[j] = sVD[(cs_ * NP + grp4 + j) * 2];
             Dv[j] = sVD[(cs_ * NP + grp4 + j) * 2 + 1];
         }
-        uint32_t cst = 0;  // column tracker (thermometer word)
         float ring[T][4];
         float vs[4];
 #pragma unroll
@@ -253,30 +367,7 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         for (int ch = 0; ch <= n_chunks; ++ch) {
             const int s0 = ch * T;
             // ---- phase 1: H1 of chunk ch  +  A of chunk ch-1
-            if (ch < n_chunks && active) {
-#pragma unroll
-                for (int rho = 0; rho < T; ++rho) {
-                    const int4 st = stab[s0 + rho];
-                    if (st.y == 1) {
-                        cst += TH[mb[st.z + x] * G + grp] - TH[mb[st.w + x] * G + grp];
-                    } else if (st.y == 0) {
-                        cst = 0;
-#pragma unroll 1
-                        for (int dy = -R; dy <= R; ++dy)
-                            cst += TH[mb[map_coord(st.x + dy, h, g.pad) * w + x] * G + grp];
-                    }
-                    uint32_t* row = chp + rho * CPB * G * g.WPS;
-                    row[skew(x + R)] = cst;
-                    if (halo0 >= 0) row[halo0] = cst;
-                    if (halo1 >= 0) row[halo1] = cst;
-                    if (many_halo) {
-                        for (int j = 0; j < 2 * R; ++j) {
-                            const int p = j < R ? j : w + j;
-                            if (xmap[p] == x) row[skew(p)] = cst;
-                        }
-                    }
-                }
-            }
+            if (ch < n_chunks && active) h1_chunk(s0);
             if (ch > 0 && tid < a_rows * w) {
                 const int ps0 = s0 - T;
                 for (int rho = a_r0; rho < T; rho += a_rows) {
@@ -304,25 +395,7 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             __syncthreads();
             if (ch == n_chunks) break;
             // ---- phase 2: H2, horizontal windows of the column words
-            {
-                const int ntask = T * CPB * G * g.nseg;
-                for (int task = tid; task < ntask; task += S2_THREADS) {
-                    const int sg = task % g.nseg;
-                    const int rg = task / g.nseg;  // (rho * CPB + cs) * G + grp
-                    const uint32_t* src = CHp + rg * g.WPS;
-                    uint32_t* dst = WH + rg * w;
-                    const int x0 = sg * g.seg;
-                    const int x1 = min(w, x0 + g.seg);
-                    uint32_t sum = 0;
-#pragma unroll
-                    for (int p = 0; p < T; ++p) sum += src[skew(x0 + p)];
-                    dst[x0] = sum;
-                    for (int xx = x0 + 1; xx < x1; ++xx) {
-                        sum += src[skew(xx + 2 * R)] - src[skew(xx - 1)];
-                        dst[xx] = sum;
-                    }
-                }
-            }
+            h2_chunk(s0, false);
             __syncthreads();
             // ---- phase 3: E, closed-form transport + register ring + vertical box
             if (active) {
@@ -391,14 +464,28 @@ static int score2_plan_t(Score2Geom& g) {
     return g.total;
 }
 
+int sample_stride(int h, int w, int budget);
+
+// fused_ref: compute the median-quan reference inside the kernel (pass 0) when
+// possible -- T^2 <= 126 (packed u8 compares), reflect with h, w > 1 or wrap
+// (pad_plane's edge fallback for size-1 axes differs from _map_coord), and the
+// sample store fits shared memory.
 static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
-                       Score2Geom* out, size_t* smem_out) {
+                       int pad, int budget, bool fused_ref, Score2Geom* out, size_t* smem_out) {
     if (t < 1 || t > 15 || (t & 1) == 0) return QFCA_ERR_UNSUPPORTED;
     if (n_bins > 256) return QFCA_ERR_UNSUPPORTED;
     if ((int64_t)h * w > (1 << 24)) return QFCA_ERR_UNSUPPORTED;
     Score2Geom g;
     memset(&g, 0, sizeof(g));
-    g.h = h; g.w = w; g.n_bins = n_bins; g.pad = 0; g.C = C;
+    g.h = h; g.w = w; g.n_bins = n_bins; g.pad = pad; g.C = C;
+    g.fref = fused_ref && t * t <= 126 && budget >= 1 &&
+             (pad == QFCA_PAD_WRAP || (h > 1 && w > 1)) ? 1 : 0;
+    if (g.fref) {
+        g.stride = sample_stride(h, w, budget);
+        g.nsx = (w + g.stride - 1) / g.stride;
+        g.nsamp = ((h + g.stride - 1) / g.stride) * g.nsx;
+        g.sp = (g.nsamp + 3) & ~3;
+    }
     // compile-time-width variant: w in {32, 64, 128}, 4 groups (N <= 16)
     const bool fast = n_bins <= 16 && (w == 32 || w == 64 || w == 128);
     g.fastW = fast ? w : 0;
@@ -426,6 +513,10 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
 #undef QFCA_S2_CASE
         }
         if (bytes <= 225 * 1024) break;
+        if (g.fref) {  // keep the fast variant, compute the reference outside
+            g.fref = 0;
+            continue;
+        }
         if (g.fastW) {  // the fixed-width variant needs its full slot count
             g.fastW = 0;
             g.G = (n_bins + 3) / 4;
@@ -453,24 +544,31 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     return QFCA_OK;
 }
 
-int score2_groups(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint) {
+// groups the v2 kernel would use (-1: not applicable); *fref = fused reference
+int score2_query(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                 int pad, int budget, int want_fref, int* fref) {
     Score2Geom g;
     size_t smem;
-    if (score2_plan(h, w, n_bins, t, C, images, groups_hint, &g, &smem) != QFCA_OK) return -1;
+    if (score2_plan(h, w, n_bins, t, C, images, groups_hint, pad, budget, want_fref != 0, &g,
+                    &smem) != QFCA_OK)
+        return -1;
+    if (fref) *fref = g.fref;
     return g.groups;
 }
 
+// V == nullptr: the reference is selected inside the kernel (needs fref).
 int launch_score2(const void* bins, int bins_bytes, const float* lo, const float* hi,
                   const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
-                  int pad, int groups, float* partial, cudaStream_t st) {
+                  int pad, int budget, int groups, float* partial, cudaStream_t st) {
     if (bins_bytes != 1) return QFCA_ERR_UNSUPPORTED;
     if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
     Score2Geom g;
     size_t smem;
-    int rc = score2_plan(h, w, n_bins, t, C, images, groups, &g, &smem);
+    int rc = score2_plan(h, w, n_bins, t, C, images, groups, pad, budget, V == nullptr, &g,
+                         &smem);
     if (rc != QFCA_OK) return rc;
     if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
-    g.pad = pad;
+    if (V == nullptr && !g.fref) return QFCA_ERR_UNSUPPORTED;
     const int64_t grid = images * g.groups;
     void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score2Geom,
                  float*) = nullptr;

@@ -45,7 +45,7 @@ def test_host_only_entry_points():
     from oracle import qfca_oracle as O
     for h, w, b in [(13, 17, 30), (32, 32, 4096), (7, 1000, 100), (1, 1, 1)]:
         assert L.qfca_sample_stride(h, w, b) == O.sample_stride(h, w, b)
-    g = L.qfca_score_groups(128, 128, 16, 9, 512, 64, 0)
+    g = L.qfca_score_groups(128, 128, 16, 9, 512, 64, 0, 1, 4096, 0)
     assert 1 <= g <= 512
     import ctypes
     cfg = N.QfcaConfig(16, 9, 1, 4096, 4, 0, 1.0)
