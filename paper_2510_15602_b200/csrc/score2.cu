@@ -48,7 +48,17 @@ struct Score2Geom {
     int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, o_sv, o_sa, total;
 };
 
-__device__ __forceinline__ int skew(int p) { return p + (p >> 3); }
+constexpr int S2_MAXSEG = 33;  // longest H2 segment the unrolled loop covers
+
+// H2 segment length: as few segments per (row, slot, group) as keep every
+// thread busy, rounded up to odd (distinct banks across a warp's segments)
+__host__ __device__ constexpr int s2_seg_rows(int rows, int w) {
+    return ((w + ((S2_THREADS / rows) > 0 ? (S2_THREADS / rows) : 1) - 1) /
+            ((S2_THREADS / rows) > 0 ? (S2_THREADS / rows) : 1)) | 1;
+}
+__host__ __device__ constexpr int s2_seg(int t, int w) {  // fixed-width: CPB*G = 512/w
+    return s2_seg_rows(t * (S2_THREADS / w), w);
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -122,22 +132,27 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     float* const part = partial + ((int64_t)img * g.groups + cg) * hw;
 
     // ---- per-CTA tables: stream rows, padded-x map, thermometer words
+    // stab[s] = {row offset entering the column window, row offset leaving it,
+    //            -1 (slide) or the E row to recount from scratch,
+    //            sample-row base index (fused reference) or -1}
     const int n_chunks = (g.S + T - 1) / T;
     for (int s = tid; s < n_chunks * T; s += S2_THREADS) {
         if (s >= g.S) {  // padding rows of the last chunk: tracker stays put
-            stab[s] = make_int4(0, 2, 0, 0);
+            stab[s] = make_int4(0, 0, -1, -1);
             continue;
         }
         const int e = s - R;
         const int ye = map_coord(e, h, g.pad);
-        int mode = 0, add = 0, rem = 0;
+        int add = 0, rem = 0, recount = ye;
         if (s > 0) {
             const int yp = map_coord(e - 1, h, g.pad);
-            if (ye == yp + 1) { mode = 1; add = map_coord(ye + R, h, g.pad); rem = map_coord(yp - R, h, g.pad); }
-            else if (ye == yp - 1) { mode = 1; add = map_coord(ye - R, h, g.pad); rem = map_coord(yp + R, h, g.pad); }
-            else if (ye == yp) { mode = 2; }
+            if (ye == yp + 1) { recount = -1; add = map_coord(ye + R, h, g.pad); rem = map_coord(yp - R, h, g.pad); }
+            else if (ye == yp - 1) { recount = -1; add = map_coord(ye - R, h, g.pad); rem = map_coord(yp + R, h, g.pad); }
+            else if (ye == yp) { recount = -1; }
         }
-        stab[s] = make_int4(ye, mode, add * w, rem * w);
+        const int samp = (g.fref && e >= 0 && e < h && e % g.stride == 0)
+                             ? (e / g.stride) * g.nsx : -1;
+        stab[s] = make_int4(add * w, rem * w, recount, samp);
     }
     for (int p = tid; p < g.WP; p += S2_THREADS) xmap[p] = map_coord(p - R, w, g.pad);
     for (int idx = tid; idx < 256 * G; idx += S2_THREADS) {
@@ -151,20 +166,27 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         for (int j = 0; j < 2 * R; ++j) {
             const int p = j < R ? j : w + j;
             if (xmap[p] == x) {
-                if (halo0 < 0) halo0 = skew(p);
-                else if (halo1 < 0) halo1 = skew(p);
+                if (halo0 < 0) halo0 = p;
+                else if (halo1 < 0) halo1 = p;
             }
         }
     }
     // a padded column can feed > 2 halo slots only for planes narrower than R
     const bool many_halo = w <= R;
+    // sample column of this thread's x (fused reference), -1 if not on the grid
+    const int xsamp = (g.fref && x % g.stride == 0) ? x / g.stride : -1;
 
     const int cs_ = active ? cs : 0;
-    const uint8_t* const mb = sb + cs_ * hw;
+    const uint8_t* const mbx = sb + cs_ * hw + x;
+    const uint32_t* const thg = TH + grp;
     const float* const pj = sPJ + cs_ * (T2 + 1);
     uint32_t* const chp = CHp + (cs_ * G + grp) * g.WPS;
     const int a_rows = S2_THREADS / w;  // A-phase rows per pass
     const int a_x = tid % w, a_r0 = tid / w;
+    // H2 task geometry: odd segment length keeps the lanes of a warp on
+    // distinct banks without padding the rows
+    const int seg = W ? s2_seg(T, W) : g.seg;
+    const int nseg = (w + seg - 1) / seg;
 
     // H1 for the T stream rows of chunk starting at s0 (column trackers)
     uint32_t cst = 0;  // column tracker (thermometer word)
@@ -172,47 +194,52 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll
         for (int rho = 0; rho < T; ++rho) {
             const int4 st = stab[s0 + rho];
-            if (st.y == 1) {
-                cst += TH[mb[st.z + x] * G + grp] - TH[mb[st.w + x] * G + grp];
-            } else if (st.y == 0) {
+            if (st.z < 0) {
+                cst += thg[mbx[st.x] * G] - thg[mbx[st.y] * G];
+            } else {
                 cst = 0;
 #pragma unroll 1
                 for (int dy = -R; dy <= R; ++dy)
-                    cst += TH[mb[map_coord(st.x + dy, h, g.pad) * w + x] * G + grp];
+                    cst += thg[mbx[map_coord(st.z + dy, h, g.pad) * w] * G];
             }
             uint32_t* row = chp + rho * CPB * G * g.WPS;
-            row[skew(x + R)] = cst;
+            row[x + R] = cst;
             if (halo0 >= 0) row[halo0] = cst;
             if (halo1 >= 0) row[halo1] = cst;
             if (many_halo) {
                 for (int j = 0; j < 2 * R; ++j) {
                     const int p = j < R ? j : w + j;
-                    if (xmap[p] == x) row[skew(p)] = cst;
+                    if (xmap[p] == x) row[p] = cst;
                 }
             }
         }
     };
     // H2 for the chunk starting at s0; only_samples: just the sample rows
     auto h2_chunk = [&](int s0, bool only_samples) {
-        const int ntask = T * CPB * G * g.nseg;
+        const int ntask = T * CPB * G * nseg;
         for (int task = tid; task < ntask; task += S2_THREADS) {
-            const int sg = task % g.nseg;
-            const int rg = task / g.nseg;  // (rho * CPB + cs) * G + grp
-            if (only_samples) {
-                const int e = s0 + rg / (CPB * G) - R;
-                if (e < 0 || e >= h || e % g.stride) continue;
-            }
-            const uint32_t* src = CHp + rg * g.WPS;
-            uint32_t* dst = WH + rg * w;
-            const int x0 = sg * g.seg;
-            const int x1 = min(w, x0 + g.seg);
+            const int rg = task / nseg;  // (rho * CPB + cs) * G + grp
+            const int x0 = (task - rg * nseg) * seg;
+            if (only_samples && stab[s0 + rg / (CPB * G)].w < 0) continue;
+            const uint32_t* src = CHp + rg * g.WPS + x0;
+            uint32_t* dst = WH + rg * w + x0;
             uint32_t sum = 0;
 #pragma unroll
-            for (int p = 0; p < T; ++p) sum += src[skew(x0 + p)];
-            dst[x0] = sum;
-            for (int xx = x0 + 1; xx < x1; ++xx) {
-                sum += src[skew(xx + 2 * R)] - src[skew(xx - 1)];
-                dst[xx] = sum;
+            for (int p = 0; p < T; ++p) sum += src[p];
+            dst[0] = sum;
+            if (x0 + seg <= w && seg <= S2_MAXSEG) {
+#pragma unroll
+                for (int k = 1; k < S2_MAXSEG; ++k) {
+                    if (k < seg) {
+                        sum += src[k + 2 * R] - src[k - 1];
+                        dst[k] = sum;
+                    }
+                }
+            } else {
+                for (int k = 1; k < w - x0; ++k) {
+                    sum += src[k + 2 * R] - src[k - 1];
+                    dst[k] = sum;
+                }
             }
         }
     };
@@ -259,14 +286,13 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 __syncthreads();
                 h2_chunk(s0, true);
                 __syncthreads();
-                if (active && x % g.stride == 0) {
-                    uint8_t* sa = SA + (cs * NP + grp4) * g.sp + x / g.stride;
+                if (active && xsamp >= 0) {
+                    uint8_t* sa = SA + (cs * NP + grp4) * g.sp + xsamp;
 #pragma unroll
                     for (int rho = 0; rho < T; ++rho) {
-                        const int e = s0 + rho - R;
-                        if (e < 0 || e >= h || e % g.stride) continue;
+                        const int si = stab[s0 + rho].w;
+                        if (si < 0) continue;
                         const uint32_t word = WH[((rho * CPB + cs) * G + grp) * w + x];
-                        const int si = (e / g.stride) * g.nsx;
 #pragma unroll
                         for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
                     }
@@ -496,15 +522,14 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     if (g.CPB > 8) g.CPB = 8;
     const int r = t / 2;
     g.WP = w + 2 * r;
-    g.WPS = g.WP + g.WP / 8 + 1;
+    g.WPS = g.WP | 1;  // odd row stride
     g.S = h + 2 * r;
     size_t bytes = 0;
     for (;;) {
-        // H2 segments: one task per thread where possible
-        const int rows = t * g.CPB * g.G;
-        int nseg = S2_THREADS / rows;
-        nseg = nseg < 1 ? 1 : (nseg > w ? w : nseg);
-        g.seg = (w + nseg - 1) / nseg;
+        // H2 segments: one task per thread where possible (kernel recomputes
+        // the same value at compile time for the fixed-width variants)
+        g.seg = g.fastW ? s2_seg(t, w) : s2_seg_rows(t * g.CPB * g.G, w);
+        if (g.seg > w) g.seg = w;
         g.nseg = (w + g.seg - 1) / g.seg;
         switch (t) {
 #define QFCA_S2_CASE(TT) case TT: bytes = score2_plan_t<TT>(g); break;
