@@ -79,7 +79,7 @@ static void score2_layout(Score2Geom& g) {
     g.o_pj = take((long long)g.CPB * (T * T + 1) * 4);
     g.o_vd = take((long long)g.CPB * np * 2 * 4);
     g.o_stab = take((long long)((g.S + T - 1) / T) * T * 16);
-    g.o_chp = take((long long)T * g.CPB * g.G * g.WPS * 4);
+    g.o_chp = take((long long)T * g.CPB * g.G * g.WP * 4);
     g.o_wh = take((long long)T * g.CPB * g.G * g.w * 4);
     g.o_vb = take((long long)T * g.CPB * np * g.w * 4);
     g.o_xmap = take((long long)g.WP * 4);
@@ -116,7 +116,8 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 
     const int tid = threadIdx.x;
     const int w = W ? W : g.w;
-    const int G = W ? 4 : g.G;
+    const int G = W ? 4 : g.G;  // a multiple of 4: GQ quads of groups
+    const int GQ = G / 4;
     const int CPB = W ? S2_THREADS / (4 * W) : g.CPB;
     const int h = g.h, NP = G * 4;
     const int per_slot = G * w;
@@ -160,12 +161,17 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         TH[idx] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
     }
     __syncthreads();
-    // padded positions (outside [R, R + w)) that this thread's column feeds
+
+    // ---- H1 role: thread (slot hcs, quad hq, column hx) tracks 4 group words
+    const int h1_threads = CPB * GQ * w;
+    const bool h1_act = tid < h1_threads;
+    const int hx = tid % w, hq = (tid / w) % GQ, hcs = h1_act ? tid / (w * GQ) : 0;
+    // padded positions (outside [R, R + w)) that column hx feeds
     int halo0 = -1, halo1 = -1;
-    if (active) {
+    if (h1_act) {
         for (int j = 0; j < 2 * R; ++j) {
             const int p = j < R ? j : w + j;
-            if (xmap[p] == x) {
+            if (xmap[p] == hx) {
                 if (halo0 < 0) halo0 = p;
                 else if (halo1 < 0) halo1 = p;
             }
@@ -173,75 +179,117 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     }
     // a padded column can feed > 2 halo slots only for planes narrower than R
     const bool many_halo = w <= R;
-    // sample column of this thread's x (fused reference), -1 if not on the grid
-    const int xsamp = (g.fref && x % g.stride == 0) ? x / g.stride : -1;
+    const uint8_t* const hbx = sb + hcs * hw + hx;
+    const uint4* const th4 = reinterpret_cast<const uint4*>(TH) + hq;
+    uint4* const chq = reinterpret_cast<uint4*>(CHp) + hcs * g.WP * GQ + hq;
+    // ---- A role: the threads without an H1 column share the A phase
+    const int a_threads = S2_THREADS - h1_threads;
+    const int a_rows = a_threads / w;
+    const int a_t = tid - h1_threads;
+    const int a_x = a_t % w, a_r0 = a_t / w;
+    const bool a_act = a_t >= 0 && a_t < a_rows * w;
 
+    // ---- E role: thread (slot cs, group grp, column x)
+    // sample column of x (fused reference), -1 if not on the grid
+    const int xsamp = (g.fref && x % g.stride == 0) ? x / g.stride : -1;
     const int cs_ = active ? cs : 0;
-    const uint8_t* const mbx = sb + cs_ * hw + x;
-    const uint32_t* const thg = TH + grp;
     const float* const pj = sPJ + cs_ * (T2 + 1);
-    uint32_t* const chp = CHp + (cs_ * G + grp) * g.WPS;
-    const int a_rows = S2_THREADS / w;  // A-phase rows per pass
-    const int a_x = tid % w, a_r0 = tid / w;
     // H2 task geometry: odd segment length keeps the lanes of a warp on
-    // distinct banks without padding the rows
+    // distinct banks
     const int seg = W ? s2_seg(T, W) : g.seg;
     const int nseg = (w + seg - 1) / seg;
 
     // H1 for the T stream rows of chunk starting at s0 (column trackers)
-    uint32_t cst = 0;  // column tracker (thermometer word)
+    uint4 cst = make_uint4(0, 0, 0, 0);  // 4 thermometer words
     auto h1_chunk = [&](int s0) {
 #pragma unroll
         for (int rho = 0; rho < T; ++rho) {
             const int4 st = stab[s0 + rho];
             if (st.z < 0) {
-                cst += thg[mbx[st.x] * G] - thg[mbx[st.y] * G];
+                const uint4 a = th4[hbx[st.x] * GQ], r = th4[hbx[st.y] * GQ];
+                cst.x += a.x - r.x;
+                cst.y += a.y - r.y;
+                cst.z += a.z - r.z;
+                cst.w += a.w - r.w;
             } else {
-                cst = 0;
+                cst = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
-                for (int dy = -R; dy <= R; ++dy)
-                    cst += thg[mbx[map_coord(st.z + dy, h, g.pad) * w] * G];
+                for (int dy = -R; dy <= R; ++dy) {
+                    const uint4 a = th4[hbx[map_coord(st.z + dy, h, g.pad) * w] * GQ];
+                    cst.x += a.x;
+                    cst.y += a.y;
+                    cst.z += a.z;
+                    cst.w += a.w;
+                }
             }
-            uint32_t* row = chp + rho * CPB * G * g.WPS;
-            row[x + R] = cst;
-            if (halo0 >= 0) row[halo0] = cst;
-            if (halo1 >= 0) row[halo1] = cst;
+            uint4* row = chq + rho * CPB * g.WP * GQ;
+            row[(hx + R) * GQ] = cst;
+            if (halo0 >= 0) row[halo0 * GQ] = cst;
+            if (halo1 >= 0) row[halo1 * GQ] = cst;
             if (many_halo) {
                 for (int j = 0; j < 2 * R; ++j) {
                     const int p = j < R ? j : w + j;
-                    if (xmap[p] == x) row[p] = cst;
+                    if (xmap[p] == hx) row[p * GQ] = cst;
                 }
             }
         }
     };
-    // H2 for the chunk starting at s0; only_samples: just the sample rows
+    // H2 for the chunk starting at s0; only_samples: just the sample rows.
+    // Task = (row, slot, quad, segment): uint4 sliding window along the row.
     auto h2_chunk = [&](int s0, bool only_samples) {
-        const int ntask = T * CPB * G * nseg;
+        const int ntask = T * CPB * GQ * nseg;
         for (int task = tid; task < ntask; task += S2_THREADS) {
-            const int rg = task / nseg;  // (rho * CPB + cs) * G + grp
-            const int x0 = (task - rg * nseg) * seg;
-            if (only_samples && stab[s0 + rg / (CPB * G)].w < 0) continue;
-            const uint32_t* src = CHp + rg * g.WPS + x0;
-            uint32_t* dst = WH + rg * w + x0;
-            uint32_t sum = 0;
+            const int rq = task / nseg;  // (rho * CPB + cs) * GQ + q
+            const int x0 = (task - rq * nseg) * seg;
+            const int rc = rq / GQ, q = rq - rc * GQ;
+            if (only_samples && stab[s0 + rc / CPB].w < 0) continue;
+            const uint4* src = reinterpret_cast<const uint4*>(CHp) + (rc * g.WP + x0) * GQ + q;
+            uint4* dst = reinterpret_cast<uint4*>(WH) + (rc * w + x0) * GQ + q;
+            uint4 sum = make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int p = 0; p < T; ++p) sum += src[p];
+            for (int p = 0; p < T; ++p) {
+                const uint4 v = src[p * GQ];
+                sum.x += v.x;
+                sum.y += v.y;
+                sum.z += v.z;
+                sum.w += v.w;
+            }
             dst[0] = sum;
-            if (x0 + seg <= w && seg <= S2_MAXSEG) {
+            const int kend = min(seg, w - x0);
+            if (kend == seg && seg <= S2_MAXSEG) {
 #pragma unroll
                 for (int k = 1; k < S2_MAXSEG; ++k) {
                     if (k < seg) {
-                        sum += src[k + 2 * R] - src[k - 1];
-                        dst[k] = sum;
+                        const uint4 a = src[(k + 2 * R) * GQ], r = src[(k - 1) * GQ];
+                        sum.x += a.x - r.x;
+                        sum.y += a.y - r.y;
+                        sum.z += a.z - r.z;
+                        sum.w += a.w - r.w;
+                        dst[k * GQ] = sum;
                     }
                 }
             } else {
-                for (int k = 1; k < w - x0; ++k) {
-                    sum += src[k + 2 * R] - src[k - 1];
-                    dst[k] = sum;
+                for (int k = 1; k < kend; ++k) {
+                    const uint4 a = src[(k + 2 * R) * GQ], r = src[(k - 1) * GQ];
+                    sum.x += a.x - r.x;
+                    sum.y += a.y - r.y;
+                    sum.z += a.z - r.z;
+                    sum.w += a.w - r.w;
+                    dst[k * GQ] = sum;
                 }
             }
         }
+    };
+    // group words of (stream row rho, slot cs, column x): this group and the previous one
+    auto wh_words = [&](int rho, uint32_t& word, uint32_t& prev) {
+        const uint4 v = reinterpret_cast<const uint4*>(WH)[((rho * CPB + cs) * w + x) * GQ +
+                                                           (grp >> 2)];
+        const int gl = grp & 3;
+        word = gl == 0 ? v.x : gl == 1 ? v.y : gl == 2 ? v.z : v.w;
+        prev = gl == 1 ? v.x : gl == 2 ? v.y : gl == 3 ? v.z : 0u;
+        if (gl == 0 && grp > 0)
+            prev = reinterpret_cast<const uint4*>(WH)[((rho * CPB + cs) * w + x) * GQ +
+                                                     (grp >> 2) - 1].w;
     };
 
     for (int cb = c_begin; cb < c_end; cb += CPB) {
@@ -282,7 +330,7 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             // V_i = the (S-1-m)-th smallest A_i over the samples (reference.cu).
             for (int ch = 0; ch < n_chunks; ++ch) {
                 const int s0 = ch * T;
-                if (active) h1_chunk(s0);
+                if (h1_act) h1_chunk(s0);
                 __syncthreads();
                 h2_chunk(s0, true);
                 __syncthreads();
@@ -292,7 +340,8 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     for (int rho = 0; rho < T; ++rho) {
                         const int si = stab[s0 + rho].w;
                         if (si < 0) continue;
-                        const uint32_t word = WH[((rho * CPB + cs) * G + grp) * w + x];
+                        uint32_t word, prev;
+                        wh_words(rho, word, prev);
 #pragma unroll
                         for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
                     }
@@ -393,8 +442,8 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         for (int ch = 0; ch <= n_chunks; ++ch) {
             const int s0 = ch * T;
             // ---- phase 1: H1 of chunk ch  +  A of chunk ch-1
-            if (ch < n_chunks && active) h1_chunk(s0);
-            if (ch > 0 && tid < a_rows * w) {
+            if (ch < n_chunks && h1_act) h1_chunk(s0);
+            if (ch > 0 && a_act) {
                 const int ps0 = s0 - T;
                 for (int rho = a_r0; rho < T; rho += a_rows) {
                     const int y = ps0 + rho - 2 * R;
@@ -427,9 +476,8 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             if (active) {
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
-                    const uint32_t* whr = WH + ((rho * CPB + cs) * G) * w + x;
-                    const uint32_t word = whr[grp * w];
-                    const uint32_t prev = grp > 0 ? whr[(grp - 1) * w] : 0u;
+                    uint32_t word, prev;
+                    wh_words(rho, word, prev);
                     // the group has mass in this window iff A_{4g+3} > A_{4g-1};
                     // groups empty across the whole warp contribute E = 0
                     const bool mass = (word >> 24) != (prev >> 24);
@@ -515,7 +563,7 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     // compile-time-width variant: w in {32, 64, 128}, 4 groups (N <= 16)
     const bool fast = n_bins <= 16 && (w == 32 || w == 64 || w == 128);
     g.fastW = fast ? w : 0;
-    g.G = fast ? 4 : (n_bins + 3) / 4;
+    g.G = fast ? 4 : ((n_bins + 15) / 16) * 4;  // whole quads of 4-bin groups
     const int per = g.G * w;
     if (per > S2_THREADS || w < 4) return QFCA_ERR_UNSUPPORTED;
     g.CPB = S2_THREADS / per;
@@ -544,7 +592,7 @@ static int score2_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
         }
         if (g.fastW) {  // the fixed-width variant needs its full slot count
             g.fastW = 0;
-            g.G = (n_bins + 3) / 4;
+            g.G = ((n_bins + 15) / 16) * 4;
             g.CPB = S2_THREADS / (g.G * w);
             if (g.CPB > 8) g.CPB = 8;
             continue;
