@@ -1,51 +1,97 @@
 // pca.cu -- K7: PCA residual r = (x - mu) - V^T V (x - mu)   (features.py:183-193)
 //
-// One thread per pixel: z = V (x - mu) accumulates the k projections in fp64
-// (the reference computes in fp64, then casts the residual to float32), the
-// second channel sweep writes the float32 residual.  mu and V (k x C, fp64)
-// are staged in shared memory and broadcast.  The feature read is coalesced
-// along pixels; the second read hits L2.
+// z = V (x - mu) accumulates the k projections in fp64 (the reference computes
+// in fp64, then casts the residual to float32); a second channel sweep writes
+// the float32 residual.  Each thread owns PX consecutive pixels, so every
+// broadcast of V[j][c] from shared memory feeds PX fused multiply-adds; the
+// feature reads are float4-vectorised and coalesced along pixels (the second
+// sweep hits L2).
 #include "common.cuh"
 
 namespace qfca {
 
-constexpr int PCA_MAXK = 32;
+constexpr int PCA_MAXK = 16;
 constexpr int PCA_THREADS = 128;
+constexpr int PCA_PX = 4;
 
+template <int K>
 __global__ void __launch_bounds__(PCA_THREADS)
-k_pca_residual(const float* __restrict__ x, int64_t images, int C, int64_t hw,
-               const double* __restrict__ mean, const double* __restrict__ comps, int k,
+k_pca_residual(const float* __restrict__ x, int C, int64_t hw,
+               const double* __restrict__ mean, const double* __restrict__ comps,
                int64_t blocks_per_image, int per_image_model, float* __restrict__ out) {
     extern __shared__ __align__(16) double sm[];
-    double* smu = sm;          // [C]
-    double* sV = sm + C;       // [k][C]
+    double* smu = sm;      // [C]
+    double* sV = sm + C;   // [C][K]  (transposed: the K values of a channel are adjacent)
     const int64_t img = blockIdx.x / blocks_per_image;
     const int64_t blk = blockIdx.x % blocks_per_image;
     const double* mu = mean + (per_image_model ? img * C : 0);
-    const double* V = comps + (per_image_model ? img * (int64_t)k * C : 0);
+    const double* V = comps + (per_image_model ? img * (int64_t)K * C : 0);
     for (int i = threadIdx.x; i < C; i += PCA_THREADS) smu[i] = mu[i];
-    for (int i = threadIdx.x; i < k * C; i += PCA_THREADS) sV[i] = V[i];
+    for (int i = threadIdx.x; i < K * C; i += PCA_THREADS) {
+        const int j = i / C, c = i % C;
+        sV[c * K + j] = V[i];
+    }
     __syncthreads();
-    const int64_t px = blk * PCA_THREADS + threadIdx.x;
-    if (px >= hw) return;
-    const float* xp = x + img * C * hw + px;
-    float* op = out + img * C * hw + px;
-    double z[PCA_MAXK];
+    const int64_t p0 = (blk * PCA_THREADS + threadIdx.x) * PCA_PX;
+    if (p0 >= hw) return;
+    const float* xp = x + img * C * hw + p0;
+    float* op = out + img * C * hw + p0;
+    const bool full = p0 + PCA_PX <= hw && (hw % 4) == 0;
+    double z[PCA_PX][K];
 #pragma unroll
-    for (int j = 0; j < PCA_MAXK; ++j) z[j] = 0.0;
+    for (int q = 0; q < PCA_PX; ++q)
+#pragma unroll
+        for (int j = 0; j < K; ++j) z[q][j] = 0.0;
+    auto load = [&](int c, double (&v)[PCA_PX]) {
+        const float* src = xp + (int64_t)c * hw;
+        if (full) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(src));
+            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < PCA_PX; ++q) v[q] = p0 + q < hw ? (double)__ldg(src + q) : 0.0;
+        }
+        const double m = smu[c];
+#pragma unroll
+        for (int q = 0; q < PCA_PX; ++q) v[q] -= m;
+    };
     for (int c = 0; c < C; ++c) {
-        const double xc = (double)__ldg(xp + (int64_t)c * hw) - smu[c];
+        double xc[PCA_PX];
+        load(c, xc);
+        const double* vc = sV + c * K;
 #pragma unroll
-        for (int j = 0; j < PCA_MAXK; ++j)
-            if (j < k) z[j] = fma(sV[j * C + c], xc, z[j]);
+        for (int j = 0; j < K; ++j) {
+            const double vj = vc[j];
+#pragma unroll
+            for (int q = 0; q < PCA_PX; ++q) z[q][j] = fma(vj, xc[q], z[q][j]);
+        }
     }
     for (int c = 0; c < C; ++c) {
-        const double xc = (double)__ldg(xp + (int64_t)c * hw) - smu[c];
-        double proj = 0.0;
+        double xc[PCA_PX];
+        load(c, xc);
+        const double* vc = sV + c * K;
+        double proj[PCA_PX];
 #pragma unroll
-        for (int j = 0; j < PCA_MAXK; ++j)
-            if (j < k) proj = fma(sV[j * C + c], z[j], proj);
-        op[(int64_t)c * hw] = (float)(xc - proj);
+        for (int q = 0; q < PCA_PX; ++q) proj[q] = 0.0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const double vj = vc[j];
+#pragma unroll
+            for (int q = 0; q < PCA_PX; ++q) proj[q] = fma(vj, z[q][j], proj[q]);
+        }
+        float* dst = op + (int64_t)c * hw;
+        if (full) {
+            float4 f;
+            f.x = (float)(xc[0] - proj[0]);
+            f.y = (float)(xc[1] - proj[1]);
+            f.z = (float)(xc[2] - proj[2]);
+            f.w = (float)(xc[3] - proj[3]);
+            *reinterpret_cast<float4*>(dst) = f;
+        } else {
+#pragma unroll
+            for (int q = 0; q < PCA_PX; ++q)
+                if (p0 + q < hw) dst[q] = (float)(xc[q] - proj[q]);
+        }
     }
 }
 
@@ -57,19 +103,34 @@ __global__ void k_center(const float* __restrict__ x, int64_t planes, int64_t hw
     out[gid] = (float)((double)x[gid] - mean[gid / hw]);
 }
 
+template <int K>
+static int launch_res_k(const float* x, int64_t images, int C, int64_t hw, const double* mean,
+                        const double* comps, int per_image_model, float* out, cudaStream_t st) {
+    const size_t smem = (size_t)(C + (size_t)K * C) * sizeof(double);
+    if (smem > 200 * 1024) return QFCA_ERR_UNSUPPORTED;
+    if (cudaFuncSetAttribute(k_pca_residual<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return QFCA_ERR_CUDA;
+    const int64_t per_block = (int64_t)PCA_THREADS * PCA_PX;
+    const int64_t bpi = (hw + per_block - 1) / per_block;
+    k_pca_residual<K><<<(unsigned)(bpi * images), PCA_THREADS, smem, st>>>(
+        x, C, hw, mean, comps, bpi, per_image_model, out);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
 int launch_pca_residual(const float* x, int64_t images, int C, int64_t hw, const double* mean,
                         const double* comps, int k, int per_image_model, float* out,
                         cudaStream_t st) {
     if (images <= 0 || C <= 0 || hw <= 0 || k < 1 || k > PCA_MAXK) return QFCA_ERR_ARG;
-    const size_t smem = (size_t)(C + (size_t)k * C) * sizeof(double);
-    if (smem > 200 * 1024) return QFCA_ERR_UNSUPPORTED;
-    if (cudaFuncSetAttribute(k_pca_residual, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return QFCA_ERR_CUDA;
-    const int64_t bpi = (hw + PCA_THREADS - 1) / PCA_THREADS;
-    k_pca_residual<<<(unsigned)(bpi * images), PCA_THREADS, smem, st>>>(
-        x, images, C, hw, mean, comps, k, bpi, per_image_model, out);
-    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+    switch (k) {
+#define QFCA_RES_K(KK) \
+    case KK: return launch_res_k<KK>(x, images, C, hw, mean, comps, per_image_model, out, st);
+        QFCA_RES_K(1) QFCA_RES_K(2) QFCA_RES_K(3) QFCA_RES_K(4) QFCA_RES_K(5) QFCA_RES_K(6)
+        QFCA_RES_K(7) QFCA_RES_K(8) QFCA_RES_K(9) QFCA_RES_K(10) QFCA_RES_K(11) QFCA_RES_K(12)
+        QFCA_RES_K(13) QFCA_RES_K(14) QFCA_RES_K(15) QFCA_RES_K(16)
+#undef QFCA_RES_K
+    }
+    return QFCA_ERR_ARG;
 }
 
 int launch_center(const float* x, int64_t planes, int64_t hw, const double* mean, float* out,

@@ -81,12 +81,15 @@ static void score2_layout(Score2Geom& g) {
     g.o_stab = take((long long)((g.S + T - 1) / T) * T * 16);
     g.o_chp = take((long long)T * g.CPB * g.G * g.WP * 4);
     g.o_wh = take((long long)T * g.CPB * g.G * g.w * 4);
-    g.o_vb = take((long long)T * g.CPB * np * g.w * 4);
+    // the sample store (pass 0 only) and the V rows (pass 1 only) share space
+    const long long vb_bytes = (long long)T * g.CPB * np * g.w * 4;
+    const long long sa_bytes = g.fref ? (long long)g.CPB * np * g.sp : 0;
+    g.o_vb = take(vb_bytes > sa_bytes ? vb_bytes : sa_bytes);
+    g.o_sa = g.o_vb;
     g.o_xmap = take((long long)g.WP * 4);
     g.o_scale = take((long long)g.CPB * 4);
     g.o_th = take((long long)256 * g.G * 4);
     g.o_sv = take((long long)g.CPB * np * 4);
-    g.o_sa = take(g.fref ? (long long)g.CPB * np * g.sp : 0);
     g.total = off;
 }
 
@@ -328,17 +331,16 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             // ---- pass 0: the global reference, fused (quantize.py:150-200).  The
             // window counts at the stride-grid samples come from the same trackers;
             // V_i = the (S-1-m)-th smallest A_i over the samples (reference.cu).
-            for (int ch = 0; ch < n_chunks; ++ch) {
+            // phases: [H1(ch) + gather(ch-1)] | H2(ch, sample rows only)
+            for (int ch = 0; ch <= n_chunks; ++ch) {
                 const int s0 = ch * T;
-                if (h1_act) h1_chunk(s0);
-                __syncthreads();
-                h2_chunk(s0, true);
-                __syncthreads();
-                if (active && xsamp >= 0) {
+                if (ch < n_chunks && h1_act) h1_chunk(s0);
+                if (ch > 0 && active && xsamp >= 0) {
+                    const int ps0 = s0 - T;
                     uint8_t* sa = SA + (cs * NP + grp4) * g.sp + xsamp;
 #pragma unroll
                     for (int rho = 0; rho < T; ++rho) {
-                        const int si = stab[s0 + rho].w;
+                        const int si = stab[ps0 + rho].w;
                         if (si < 0) continue;
                         uint32_t word, prev;
                         wh_words(rho, word, prev);
@@ -346,6 +348,10 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
                     }
                 }
+                __syncthreads();
+                if (ch == n_chunks) break;
+                h2_chunk(s0, true);
+                __syncthreads();
             }
             // pad each sample row with values above any query (packed compares)
             for (int idx = tid; idx < CPB * NP * (g.sp - g.nsamp); idx += S2_THREADS) {

@@ -92,10 +92,21 @@ def gaussian_blur(plane, sigma: float, pad: str = "reflect"):
     return to_host(out, is_torch(plane))
 
 
-def covariance_dev(xc: torch.Tensor, chunk: int = 1024) -> torch.Tensor:
+def _tf32_split(x: torch.Tensor):
+    """x = hi + lo with hi exactly representable in TF32 (10-bit mantissa)."""
+    hi_ = (x.view(torch.int32) & -8192).view(torch.float32)
+    return hi_, x - hi_
+
+
+def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "3xtf32"
+                   ) -> torch.Tensor:
     """(B, C, HW) centred fp32 -> (B, C, C) fp64 population covariance.
 
-    fp32 GEMMs over K-chunks (IEEE fp32, TF32 off) summed in fp64, / HW.
+    Tensor-core GEMMs over K-chunks summed in fp64, / HW.  "3xtf32" splits
+    the operand into a TF32 head and an fp32 tail and keeps the three
+    significant products (hi hi' + hi lo' + lo hi'), fp32-faithful at TF32
+    tensor-core speed (a single TF32 pass moves the QFCA+ map by ~4e-4,
+    SURVEY H4); "fp32" uses IEEE fp32 GEMMs.
     """
     b, c, hw = xc.shape
     nk = (hw + chunk - 1) // chunk
@@ -103,9 +114,17 @@ def covariance_dev(xc: torch.Tensor, chunk: int = 1024) -> torch.Tensor:
         xc = torch.nn.functional.pad(xc, (0, nk * chunk - hw))
     blocks = xc.reshape(b, c, nk, chunk).permute(0, 2, 1, 3).reshape(b * nk, c, chunk)
     prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
     try:
-        part = torch.bmm(blocks, blocks.transpose(1, 2))
+        if precise == "3xtf32":
+            torch.backends.cuda.matmul.allow_tf32 = True
+            hi_, lo_ = _tf32_split(blocks)
+            part = torch.bmm(hi_, hi_.transpose(1, 2))
+            cross = torch.bmm(hi_, lo_.transpose(1, 2))
+            part += cross
+            part += cross.transpose(1, 2)
+        else:
+            torch.backends.cuda.matmul.allow_tf32 = False
+            part = torch.bmm(blocks, blocks.transpose(1, 2))
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
     cov = part.reshape(b, nk, c, c).sum(dim=1, dtype=torch.float64)
