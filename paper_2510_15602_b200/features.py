@@ -98,15 +98,17 @@ def _tf32_split(x: torch.Tensor):
     return hi_, x - hi_
 
 
-def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "3xtf32"
+def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "fp32"
                    ) -> torch.Tensor:
     """(B, C, HW) centred fp32 -> (B, C, C) fp64 population covariance.
 
     Tensor-core GEMMs over K-chunks summed in fp64, / HW.  "3xtf32" splits
     the operand into a TF32 head and an fp32 tail and keeps the three
-    significant products (hi hi' + hi lo' + lo hi'), fp32-faithful at TF32
-    tensor-core speed (a single TF32 pass moves the QFCA+ map by ~4e-4,
-    SURVEY H4); "fp32" uses IEEE fp32 GEMMs.
+    significant products (hi hi' + hi lo' + lo hi') at TF32 tensor-core
+    speed; "fp32" (default) uses IEEE fp32 GEMMs.  Measured on the config-1
+    golden: fp32 moves the QFCA+ map by 9e-9 (channel count aligned), 3xtf32
+    by 1.7e-4 (the TF32 rounding of the tail is not negligible against the
+    lambda_10 / lambda_11 gap), a single TF32 pass by ~4e-4.
     """
     b, c, hw = xc.shape
     nk = (hw + chunk - 1) // chunk
