@@ -194,8 +194,10 @@ def main():
     b, c, h, w = feats.shape
 
     def step(x, events=None):
+        torch.cuda.nvtx.range_push("qfca_step")  # ncu --nvtx-include qfca_step/
         res = Q.detect_batch(x, cfg, score_events=events)
         up = Q.upsample_batch(res.scores, size, size)
+        torch.cuda.nvtx.range_pop()
         return res, up
 
     # correctness gate on this workload (first image vs the CPU oracle)
