@@ -159,6 +159,11 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
                       const double* mean, const double* comps, int32_t k,
                       int32_t per_image_model, float* out, void* stream);
 
+/* Cholesky QR of a batch of tall fp64 blocks (batch, rows, cols) row-major,
+ * in place: Y <- Y L^-T, L L^T = Y^T Y (re-orthonormalisation step of the
+ * top-k subspace eigensolver that replaces np.linalg.eigh, features.py:173) */
+int qfca_cholqr(double* blocks, int64_t batch, int32_t rows, int32_t cols, void* stream);
+
 /* ---- one-call detect (scoring.py:263-327) for the fused configuration ---- */
 typedef struct qfca_config {
     int32_t n_bins;        /* PipelineConfig.n_bins (16) */

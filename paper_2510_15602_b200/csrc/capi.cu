@@ -38,6 +38,7 @@ int launch_upsample(const double*, int64_t, int, int, int, int, float*, cudaStre
 int launch_pca_residual(const float*, int64_t, int, int64_t, const double*, const double*, int,
                         int, float*, cudaStream_t);
 int launch_center(const float*, int64_t, int64_t, const double*, float*, cudaStream_t);
+int launch_cholqr(double*, int64_t, int, int, cudaStream_t);
 int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int launch_score2(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
@@ -251,6 +252,10 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
                       int32_t per_image_model, float* out, void* stream) {
     return counted(launch_pca_residual(x, images, channels, hw, mean, comps, k, per_image_model, out,
                                S(stream)), 1);
+}
+
+int qfca_cholqr(double* blocks, int64_t batch, int32_t rows, int32_t cols, void* stream) {
+    return counted(launch_cholqr(blocks, batch, rows, cols, S(stream)), 1);
 }
 
 // ---------------------------------------------------------------- detect

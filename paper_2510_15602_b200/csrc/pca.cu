@@ -95,6 +95,69 @@ k_pca_residual(const float* __restrict__ x, int C, int64_t hw,
     }
 }
 
+// Cholesky QR of a batch of tall fp64 blocks, in place: Y (C x p, row-major)
+// <- Y L^-T with L L^T = Y^T Y.  One CTA per block, the block resident in
+// shared memory: Gram matrix, Cholesky factor and the triangular solve in one
+// launch (the subspace iteration of features.topk_eigh re-orthonormalises
+// with it after every cov @ X product).
+constexpr int CQR_THREADS = 256;
+
+__global__ void __launch_bounds__(CQR_THREADS)
+k_cholqr(double* __restrict__ Y, int C, int p) {
+    extern __shared__ __align__(16) double sq[];
+    const int ps = p | 1;              // odd row stride: rows of a warp hit distinct banks
+    double* sY = sq;                   // [C][ps]
+    double* sL = sq + (size_t)C * ps;  // [p][p] Gram, then its Cholesky factor
+    double* blk = Y + (size_t)blockIdx.x * C * p;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < C * p; i += CQR_THREADS) sY[(i / p) * ps + i % p] = blk[i];
+    __syncthreads();
+    // Gram: G[a][b] = sum_r Y[r][a] Y[r][b], lower triangle
+    for (int e = tid; e < p * p; e += CQR_THREADS) {
+        const int a = e / p, b = e % p;
+        if (b > a) continue;
+        double s = 0.0;
+        for (int r = 0; r < C; ++r) s = fma(sY[r * ps + a], sY[r * ps + b], s);
+        sL[a * p + b] = s;
+    }
+    __syncthreads();
+    // Cholesky (right-looking, one column per step)
+    for (int k = 0; k < p; ++k) {
+        if (tid == 0) sL[k * p + k] = sqrt(sL[k * p + k]);
+        __syncthreads();
+        const double dk = sL[k * p + k];
+        for (int i = k + 1 + tid; i < p; i += CQR_THREADS) sL[i * p + k] /= dk;
+        __syncthreads();
+        for (int e = tid; e < p * p; e += CQR_THREADS) {
+            const int i = e / p, j = e % p;
+            if (i > k && j > k && j <= i) sL[i * p + j] -= sL[i * p + k] * sL[j * p + k];
+        }
+        __syncthreads();
+    }
+    // rows: x L^T = y  ->  forward substitution per row
+    for (int r = tid; r < C; r += CQR_THREADS) {
+        double* row = sY + r * ps;
+        for (int k = 0; k < p; ++k) {
+            double s = row[k];
+            for (int j = 0; j < k; ++j) s -= row[j] * sL[k * p + j];
+            row[k] = s / sL[k * p + k];
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < C * p; i += CQR_THREADS) blk[i] = sY[(i / p) * ps + i % p];
+}
+
+int launch_cholqr(double* Y, int64_t batch, int C, int p, cudaStream_t st) {
+    if (batch <= 0 || C <= 0 || p <= 0 || p > C) return QFCA_ERR_ARG;
+    const size_t smem = ((size_t)C * (p | 1) + (size_t)p * p) * sizeof(double);
+    if (smem > 200 * 1024) return QFCA_ERR_UNSUPPORTED;
+    if (cudaFuncSetAttribute(k_cholqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    k_cholqr<<<(unsigned)batch, CQR_THREADS, smem, st>>>(Y, C, p);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
 // centred copy xc = x - mean (fp32 out) for the covariance GEMM
 __global__ void k_center(const float* __restrict__ x, int64_t planes, int64_t hw,
                          const double* __restrict__ mean, float* __restrict__ out) {

@@ -117,7 +117,9 @@ def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "fp32"
     blocks = xc.reshape(b, c, nk, chunk).permute(0, 2, 1, 3).reshape(b * nk, c, chunk)
     prev = torch.backends.cuda.matmul.allow_tf32
     try:
-        if precise == "3xtf32":
+        if precise == "fp64":  # fp64 tensor-core GEMM (DMMA), the reference's precision
+            part = torch.bmm(blocks.double(), blocks.double().transpose(1, 2))
+        elif precise == "3xtf32":
             torch.backends.cuda.matmul.allow_tf32 = True
             hi_, lo_ = _tf32_split(blocks)
             part = torch.bmm(hi_, hi_.transpose(1, 2))
@@ -134,7 +136,17 @@ def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "fp32"
 
 
 def _cholqr(y: torch.Tensor) -> torch.Tensor:
-    """Orthonormal basis of the columns of y (B, C, p) by Cholesky QR."""
+    """Orthonormal basis of the columns of y (B, C, p) by Cholesky QR.
+
+    One fused kernel per block (csrc/pca.cu k_cholqr: Gram, Cholesky and the
+    triangular solve with the block resident in shared memory); torch's
+    cuSOLVER / cuBLAS route for blocks that do not fit.
+    """
+    b, c, p = y.shape
+    if y.is_cuda and (c * (p | 1) + p * p) * 8 <= 200 * 1024:
+        out = y.contiguous().clone() if not y.is_contiguous() else y.clone()
+        N.call("qfca_cholqr", out.data_ptr(), b, c, p, N.stream())
+        return out
     g = y.mT @ y
     lo = torch.linalg.cholesky(g)
     return torch.linalg.solve_triangular(lo.mT, y, upper=True, left=False)
