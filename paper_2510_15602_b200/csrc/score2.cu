@@ -283,6 +283,17 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
     };
+    // group words of (stream row rho, slot cs, column x): this group and the previous one
+    auto wh_words = [&](int rho, uint32_t& word, uint32_t& prev) {
+        const uint4 v = reinterpret_cast<const uint4*>(WH)[((rho * CPB + cs) * w + x) * GQ +
+                                                           (grp >> 2)];
+        const int gl = grp & 3;
+        word = gl == 0 ? v.x : gl == 1 ? v.y : gl == 2 ? v.z : v.w;
+        prev = gl == 1 ? v.x : gl == 2 ? v.y : gl == 3 ? v.z : 0u;
+        if (gl == 0 && grp > 0)
+            prev = reinterpret_cast<const uint4*>(WH)[((rho * CPB + cs) * w + x) * GQ +
+                                                     (grp >> 2) - 1].w;
+    };
 
     for (int cb = c_begin; cb < c_end; cb += CPB) {
         // ---- load the slot channels: bins planes, reference tables
@@ -326,16 +337,15 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 if (ch < n_chunks && h1_act) h1_chunk(s0);
                 if (ch > 0 && active && xsamp >= 0) {
                     const int ps0 = s0 - T;
-                    // this thread stores bins grp + G m of its sample column
-                    uint8_t* sa = SA + (cs * NP + grp) * g.sp + xsamp;
-                    const uint8_t* recs = reinterpret_cast<const uint8_t*>(WH);
+                    uint8_t* sa = SA + (cs * NP + grp4) * g.sp + xsamp;
 #pragma unroll
                     for (int rho = 0; rho < T; ++rho) {
                         const int si = stab[ps0 + rho].w;
                         if (si < 0) continue;
-                        const uint8_t* rec = recs + ((size_t)((rho * CPB + cs) * w + x)) * NP;
+                        uint32_t word, prev;
+                        wh_words(rho, word, prev);
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) sa[m * G * g.sp + si] = rec[grp + G * m];
+                        for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
                     }
                 }
                 __syncthreads();
@@ -422,8 +432,8 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         float Vm[4], Dv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            Vm[j] = sVD[(cs_ * NP + grp + G * j) * 2];  // bin grp + G j
-            Dv[j] = sVD[(cs_ * NP + grp + G * j) * 2 + 1];
+            Vm[j] = sVD[(cs_ * NP + grp4 + j) * 2];
+            Dv[j] = sVD[(cs_ * NP + grp4 + j) * 2 + 1];
         }
         float ring[T][4];
         float vs[4];
@@ -472,53 +482,39 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             if (active) {
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
-                    // the thread's bins are i_m = grp + G m (interleaved, so every
-                    // warp carries a mix of populated and empty bins); cumulative
-                    // counts b = A_i, a = A_{i-1} as exact floats (exponent magic)
-                    uint32_t cb[4], pb[4];
-                    if (W) {  // one 16-byte record: all 16 cumulative counts
-                        const uint4 v = reinterpret_cast<const uint4*>(WH)[(rho * CPB + cs) * w + x];
-                        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-                        const uint32_t sel_b = 0x7650u + (uint32_t)grp;
-                        const uint32_t sel_a = 0x7650u + (uint32_t)((grp + 3) & 3);
+                    uint32_t word, prev;
+                    wh_words(rho, word, prev);
+                    // the group has mass in this window iff A_{4g+3} > A_{4g-1};
+                    // groups empty across the whole warp contribute E = 0
+                    const bool mass = (word >> 24) != (prev >> 24);
+                    if (__any_sync(__activemask(), mass)) {
+                        // byte -> float by exponent magic: 0x4B0000bb = 2^23 + b
+                        const uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                        float af = __uint_as_float(ma) - 8388608.0f;
+                        float pja = pj[ma - 0x4B000000u];
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            cb[m] = __byte_perm(wd[m], 0x4B000000u, sel_b);
-                            pb[m] = grp > 0 ? __byte_perm(wd[m], 0x4B000000u, sel_a)
-                                            : (m > 0 ? __byte_perm(wd[m - 1], 0x4B000000u, 0x7653)
-                                                     : 0x4B000000u);
-                        }
-                    } else {
-                        const uint8_t* rec = reinterpret_cast<const uint8_t*>(WH) +
-                                             ((size_t)((rho * CPB + cs) * w + x)) * NP;
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const int i = grp + G * m;
-                            cb[m] = 0x4B000000u | rec[i];
-                            pb[m] = i > 0 ? (0x4B000000u | rec[i - 1]) : 0x4B000000u;
-                        }
-                    }
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const float bf = __uint_as_float(cb[m]) - 8388608.0f;
-                        const float af = __uint_as_float(pb[m]) - 8388608.0f;
-                        // bins empty across the whole warp contribute E = 0
-                        if (__any_sync(__activemask(), bf > af)) {
-                            const float pjb = pj[cb[m] - 0x4B000000u];
-                            const float pja = pj[pb[m] - 0x4B000000u];
-                            const float fi = (float)(grp + G * m);
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t mbits = __byte_perm(word, 0x4B000000u, 0x7650 + j);
+                            const float bf = __uint_as_float(mbits) - 8388608.0f;
+                            const float pjb = pj[mbits - 0x4B000000u];
+                            const float fi = (float)(grp4 + j);
                             const float nua = fmaf(fi, af, -pja);  // -u(a)
                             const float nub = fmaf(fi, bf, -pjb);  // -u(b)
-                            const float ga = af < Vm[m] ? nua : Dv[m] - nua;
-                            const float gb = bf < Vm[m] ? nub : Dv[m] - nub;
+                            const float ga = af < Vm[j] ? nua : Dv[j] - nua;
+                            const float gb = bf < Vm[j] ? nub : Dv[j] - nub;
                             const float pc = bf - af;
                             // pc == 0 -> gb == ga exactly -> E == 0
                             const float E = (gb - ga) * rcp_approx(fmaxf(pc, 1.f));
-                            vs[m] += E - ring[rho][m];
-                            ring[rho][m] = E;
-                        } else {
-                            vs[m] -= ring[rho][m];
-                            ring[rho][m] = 0.f;
+                            vs[j] += E - ring[rho][j];
+                            ring[rho][j] = E;
+                            af = bf;
+                            pja = pjb;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            vs[j] -= ring[rho][j];
+                            ring[rho][j] = 0.f;
                         }
                     }
                     if (rho == T - 1) {  // re-anchor: exact sum of the ring
@@ -531,9 +527,9 @@ k_score2(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         }
                     }
                     if (s0 + rho >= 2 * R) {
-                        float* vb = Vb + ((rho * CPB + cs) * NP + grp) * w + x;
+                        float* vb = Vb + ((rho * CPB + cs) * NP + grp4) * w + x;
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) vb[m * G * w] = vs[m];
+                        for (int j = 0; j < 4; ++j) vb[j * w] = vs[j];
                     }
                 }
             }
