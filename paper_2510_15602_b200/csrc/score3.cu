@@ -1,0 +1,602 @@
+// score3.cu -- K4 v3: warp-specialised, pipelined fused scoring kernel.
+//
+// Same mathematics and data layout as score2.cu (see its header); the
+// difference is the execution schedule.  The CTA has 20 warps:
+//
+//   4 producer warps (P)   H1 + H2: column trackers and row windows of the
+//                          thermometer counts for stream chunk c+1, written
+//                          to the double-buffered window store WH[(c+1)&1];
+//   16 consumer warps (C)  E + A: closed-form transport, register E ring,
+//                          vertical box, own-bin horizontal box and the
+//                          partial-map update for chunk c from WH[c&1].
+//
+// Hand-off uses named barriers (bar.arrive / bar.sync), so producers never
+// wait for the association phase and consumers never wait for the histogram
+// phase; the only CTA-wide barriers are once per channel batch.  The fused
+// reference selection (pass 0) runs the producers over the sample rows while
+// the consumers gather the sample counts.  Fixed plane widths 32 / 64 / 128
+// with N <= 16 bins (4 groups of 4) and T <= 15.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace qfca {
+
+constexpr int S3_CWARPS = 16;
+constexpr int S3_PWARPS = 4;
+constexpr int S3_CT = S3_CWARPS * 32;            // consumer threads
+constexpr int S3_PT = S3_PWARPS * 32;            // producer threads
+constexpr int S3_THREADS = S3_CT + S3_PT;        // 640
+constexpr int S3_MAXSEG = 33;
+// named barrier ids (0 is __syncthreads)
+constexpr int BAR_P = 1, BAR_C = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5;
+
+struct Score3Geom {
+    int h, n_bins, pad, C, groups, cpg;
+    int WP;    // padded row length w + 2r
+    int S;     // stream rows h + 2r
+    int fref, stride, nsx, nsamp, sp;
+    int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, o_sv, o_sa, total;
+};
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float rcp_approx3(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// H2 segment: rows * nseg <= S3_PT, odd length (distinct banks per warp)
+__host__ __device__ constexpr int s3_seg(int t, int w) {
+    return ((w + ((S3_PT / (t * (128 / w))) > 0 ? (S3_PT / (t * (128 / w))) : 1) - 1) /
+            ((S3_PT / (t * (128 / w))) > 0 ? (S3_PT / (t * (128 / w))) : 1)) | 1;
+}
+
+template <int T, int W>
+static void score3_layout(Score3Geom& g) {
+    constexpr int CPB = 128 / W;
+    int off = 0;
+    auto take = [&](long long bytes) {
+        const int o = off;
+        off = (int)((off + bytes + 15) & ~15LL);
+        return o;
+    };
+    g.o_bins = take((long long)CPB * g.h * W);
+    g.o_pj = take((long long)CPB * (T * T + 1) * 4);
+    g.o_vd = take((long long)CPB * 16 * 2 * 4);
+    g.o_stab = take((long long)((g.S + T - 1) / T) * T * 16);
+    g.o_chp = take((long long)T * CPB * g.WP * 16);       // uint4 per padded column
+    g.o_wh = take((long long)2 * T * CPB * W * 16);       // double-buffered uint4 windows
+    const long long vb = (long long)T * CPB * 16 * W * 4;
+    const long long sa = g.fref ? (long long)CPB * 16 * g.sp : 0;
+    g.o_vb = take(vb > sa ? vb : sa);
+    g.o_sa = g.o_vb;
+    g.o_xmap = take((long long)g.WP * 4);
+    g.o_scale = take((long long)CPB * 4);
+    g.o_th = take((long long)256 * 16);
+    g.o_sv = take((long long)CPB * 16 * 4);
+    g.total = off;
+}
+
+template <int T, int W>
+__global__ void __launch_bounds__(S3_THREADS, 1)
+k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
+         const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score3Geom g,
+         float* __restrict__ partial) {
+    constexpr int R = T / 2;
+    constexpr int T2 = T * T;
+    constexpr int CPB = 128 / W;  // channel slots: CPB * W = 128 columns per CTA pass
+    constexpr int SEG = s3_seg(T, W);
+    constexpr int NSEG = (W + SEG - 1) / SEG;
+    static_assert(T * CPB * NSEG <= S3_PT, "H2 tasks must fit the producer warps");
+    static_assert(SEG <= S3_MAXSEG, "segment too long");
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint8_t* const sb = sm + g.o_bins;
+    float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
+    float* const sVD = reinterpret_cast<float*>(sm + g.o_vd);
+    int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);
+    uint4* const CHp = reinterpret_cast<uint4*>(sm + g.o_chp);
+    uint4* const WHb = reinterpret_cast<uint4*>(sm + g.o_wh);
+    float* const Vb = reinterpret_cast<float*>(sm + g.o_vb);
+    int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
+    float* const sscale = reinterpret_cast<float*>(sm + g.o_scale);
+    uint4* const TH = reinterpret_cast<uint4*>(sm + g.o_th);
+    int* const sV = reinterpret_cast<int*>(sm + g.o_sv);
+    uint8_t* const SA = sm + g.o_sa;
+
+    const int tid = threadIdx.x;
+    const bool is_p = tid >= S3_CT;
+    const int h = g.h;
+    const int hw = h * W;
+    const int img = blockIdx.x / g.groups, cgi = blockIdx.x % g.groups;
+    const int c_begin = cgi * g.cpg, c_end = min(g.C, c_begin + g.cpg);
+    float* const part = partial + ((int64_t)img * g.groups + cgi) * hw;
+    const int n_chunks = (g.S + T - 1) / T;
+    const int WHSTRIDE = T * CPB * W;  // uint4 per buffer
+
+    // ---- per-CTA tables (see score2.cu): stream rows, padded-x map, thermometer words
+    for (int s = tid; s < n_chunks * T; s += S3_THREADS) {
+        if (s >= g.S) {
+            stab[s] = make_int4(0, 0, -1, -1);
+            continue;
+        }
+        const int e = s - R;
+        const int ye = map_coord(e, h, g.pad);
+        int add = 0, rem = 0, recount = ye;
+        if (s > 0) {
+            const int yp = map_coord(e - 1, h, g.pad);
+            if (ye == yp + 1) { recount = -1; add = map_coord(ye + R, h, g.pad); rem = map_coord(yp - R, h, g.pad); }
+            else if (ye == yp - 1) { recount = -1; add = map_coord(ye - R, h, g.pad); rem = map_coord(yp + R, h, g.pad); }
+            else if (ye == yp) { recount = -1; }
+        }
+        const int samp = (g.fref && e >= 0 && e < h && e % g.stride == 0)
+                             ? (e / g.stride) * g.nsx : -1;
+        stab[s] = make_int4(add * W, rem * W, recount, samp);
+    }
+    for (int p = tid; p < g.WP; p += S3_THREADS) xmap[p] = map_coord(p - R, W, g.pad);
+    for (int b = tid; b < 256; b += S3_THREADS) {
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
+            const int d = b - 4 * q;
+            v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+        }
+        TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+
+    // ---- producer role: thread (slot pcs, column px)
+    const int pt = tid - S3_CT;
+    const int px = pt % W, pcs = is_p ? pt / W : 0;
+    int halo0 = -1, halo1 = -1;
+    if (is_p) {
+        for (int j = 0; j < 2 * R; ++j) {
+            const int p = j < R ? j : W + j;
+            if (xmap[p] == px) {
+                if (halo0 < 0) halo0 = p;
+                else if (halo1 < 0) halo1 = p;
+            }
+        }
+    }
+    const bool many_halo = W <= R;
+    const uint8_t* const pbx = sb + pcs * hw + px;
+    uint4* const pch = CHp + pcs * g.WP;
+
+    // ---- consumer role: thread (slot cs, group grp, column x)
+    const int cs = tid / (4 * W);
+    const int grp = (tid / W) & 3;
+    const int grp4 = grp * 4;
+    const int x = tid % W;
+    const int xsamp = (g.fref && x % g.stride == 0) ? x / g.stride : -1;
+    const int csx = is_p ? 0 : cs;
+    const float* const pj = sPJ + csx * (T2 + 1);
+    constexpr int A_ROWS = S3_CT / W;  // A-phase rows per pass
+    const int a_x = tid % W, a_r0 = tid / W;
+
+    uint4 cst = make_uint4(0, 0, 0, 0);
+    auto h1_chunk = [&](int s0) {
+#pragma unroll
+        for (int rho = 0; rho < T; ++rho) {
+            const int4 st = stab[s0 + rho];
+            if (st.z < 0) {
+                const uint4 a = TH[pbx[st.x]], r = TH[pbx[st.y]];
+                cst.x += a.x - r.x;
+                cst.y += a.y - r.y;
+                cst.z += a.z - r.z;
+                cst.w += a.w - r.w;
+            } else {
+                cst = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+                for (int dy = -R; dy <= R; ++dy) {
+                    const uint4 a = TH[pbx[map_coord(st.z + dy, h, g.pad) * W]];
+                    cst.x += a.x;
+                    cst.y += a.y;
+                    cst.z += a.z;
+                    cst.w += a.w;
+                }
+            }
+            uint4* row = pch + rho * CPB * g.WP;
+            row[px + R] = cst;
+            if (halo0 >= 0) row[halo0] = cst;
+            if (halo1 >= 0) row[halo1] = cst;
+            if (many_halo) {
+                for (int j = 0; j < 2 * R; ++j) {
+                    const int p = j < R ? j : W + j;
+                    if (xmap[p] == px) row[p] = cst;
+                }
+            }
+        }
+    };
+    auto h2_chunk = [&](int s0, uint4* wh, bool only_samples) {
+        const int task = pt;
+        if (task >= T * CPB * NSEG) return;
+        const int rc = task / NSEG;  // rho * CPB + cs
+        const int x0 = (task - rc * NSEG) * SEG;
+        if (only_samples && stab[s0 + rc / CPB].w < 0) return;
+        const uint4* src = CHp + rc * g.WP + x0;
+        uint4* dst = wh + rc * W + x0;
+        uint4 sum = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int p = 0; p < T; ++p) {
+            const uint4 v = src[p];
+            sum.x += v.x;
+            sum.y += v.y;
+            sum.z += v.z;
+            sum.w += v.w;
+        }
+        dst[0] = sum;
+        if (x0 + SEG <= W) {
+#pragma unroll
+            for (int k = 1; k < SEG; ++k) {
+                const uint4 a = src[k + 2 * R], r = src[k - 1];
+                sum.x += a.x - r.x;
+                sum.y += a.y - r.y;
+                sum.z += a.z - r.z;
+                sum.w += a.w - r.w;
+                dst[k] = sum;
+            }
+        } else {
+            for (int k = 1; k < W - x0; ++k) {
+                const uint4 a = src[k + 2 * R], r = src[k - 1];
+                sum.x += a.x - r.x;
+                sum.y += a.y - r.y;
+                sum.z += a.z - r.z;
+                sum.w += a.w - r.w;
+                dst[k] = sum;
+            }
+        }
+    };
+    // producer loop over one pass: chunk c goes to WH buffer c & 1
+    auto produce = [&](bool only_samples) {
+        for (int c = 0; c < n_chunks; ++c) {
+            const int b = c & 1;
+            h1_chunk(c * T);
+            bar_sync(BAR_P, S3_PT);  // CHp complete
+            if (c >= 2) bar_sync(BAR_EMPTY0 + b, S3_THREADS);  // consumers done with buffer b
+            h2_chunk(c * T, WHb + b * WHSTRIDE, only_samples);
+            bar_arrive(BAR_FULL0 + b, S3_THREADS);
+            bar_sync(BAR_P, S3_PT);  // CHp may be overwritten
+        }
+    };
+
+    for (int cb = c_begin; cb < c_end; cb += CPB) {
+        // ---- load the slot channels (all warps)
+        __syncthreads();
+        for (int k = 0; k < CPB; ++k) {
+            const int c = cb + k;
+            const int64_t plane = (int64_t)img * g.C + c;
+            if (tid == 0) {
+                float sc = 0.f;
+                if (c < c_end && hi[plane] > lo[plane])
+                    sc = (float)(((double)hi[plane] - (double)lo[plane]) / (double)g.n_bins /
+                                 (double)T2);
+                sscale[k] = sc;
+            }
+            uint8_t* dst = sb + k * hw;
+            if (c < c_end) {
+                const uint8_t* src = bins + plane * hw;
+                const uint4* s4 = reinterpret_cast<const uint4*>(src);
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+                for (int i = tid; i < hw / 16; i += S3_THREADS) d4[i] = __ldg(s4 + i);
+                if (!g.fref)
+                    for (int i = tid; i < 16; i += S3_THREADS)
+                        sV[k * 16 + i] = i < g.n_bins ? __ldg(Vref + plane * g.n_bins + i) : T2;
+            } else {
+                for (int i = tid; i < hw; i += S3_THREADS) dst[i] = 0;
+                for (int i = tid; i < 16; i += S3_THREADS) sV[k * 16 + i] = T2;
+            }
+        }
+        __syncthreads();
+
+        if (g.fref) {
+            // ---- pass 0: reference selection from the sample-row windows
+            if (is_p) {
+                produce(true);
+            } else {
+                for (int c = 0; c < n_chunks; ++c) {
+                    const int b = c & 1;
+                    bar_sync(BAR_FULL0 + b, S3_THREADS);
+                    if (xsamp >= 0) {
+                        const uint4* wh = WHb + b * WHSTRIDE;
+                        uint8_t* sa = SA + (cs * 16 + grp4) * g.sp + xsamp;
+#pragma unroll
+                        for (int rho = 0; rho < T; ++rho) {
+                            const int si = stab[c * T + rho].w;
+                            if (si < 0) continue;
+                            const uint4 v = wh[(rho * CPB + cs) * W + x];
+                            const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
+                        }
+                    }
+                    if (c + 2 < n_chunks) bar_arrive(BAR_EMPTY0 + b, S3_THREADS);
+                }
+            }
+            __syncthreads();
+            for (int idx = tid; idx < CPB * 16 * (g.sp - g.nsamp); idx += S3_THREADS) {
+                const int row = idx / (g.sp - g.nsamp), k = idx % (g.sp - g.nsamp);
+                SA[row * g.sp + g.nsamp + k] = 127;
+            }
+            __syncthreads();
+            {  // one warp per (slot, bin): smallest v with #{A <= v} >= S - m
+                const int warp = tid >> 5, lane = tid & 31;
+                const int c0 = g.nsamp - (g.nsamp - 1) / 2;
+                for (int task = warp; task < CPB * 16; task += S3_THREADS / 32) {
+                    const int k = task / 16, i = task % 16;
+                    int res = T2;
+                    if (i < g.n_bins - 1 && sscale[k] != 0.f) {
+                        const uint32_t* row = reinterpret_cast<const uint32_t*>(SA + task * g.sp);
+                        int a = 0, bnd = T2;
+                        while (a < bnd) {
+                            const int mid = (a + bnd) >> 1;
+                            const uint32_t q = 0x80808080u | ((uint32_t)mid * 0x01010101u);
+                            int cnt = 0;
+                            for (int wi = lane; wi < g.sp / 4; wi += 32)
+                                cnt += __popc((q - row[wi]) & 0x80808080u);
+                            cnt = warp_sum_i(cnt);
+                            if (cnt >= c0) bnd = mid; else a = mid + 1;
+                        }
+                        res = a;
+                    }
+                    if (lane == 0) sV[task] = res;
+                }
+            }
+            __syncthreads();
+        }
+        // ---- reference tables: PJ = prefix of J, (V_{i-1}, D_i) per bin
+        for (int k = 0; k < CPB; ++k) {
+            float* pjk = sPJ + k * (T2 + 1);
+            const int* V = sV + k * 16;
+            for (int q = tid; q < T2; q += S3_THREADS) {
+                int a = 0, bnd = g.n_bins - 1;
+                while (a < bnd) {
+                    const int mid = (a + bnd) >> 1;
+                    if (V[mid] > q) bnd = mid; else a = mid + 1;
+                }
+                pjk[q + 1] = (float)a;
+            }
+        }
+        __syncthreads();
+        if (tid < 32 * CPB) {
+            const int k = tid >> 5, lane = tid & 31;
+            float* pjk = sPJ + k * (T2 + 1);
+            float carry = 0.f;
+            if (lane == 0) pjk[0] = 0.f;
+            for (int base = 1; base <= T2; base += 32) {
+                const int q = base + lane;
+                float v = q <= T2 ? pjk[q] : 0.f;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float u = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += u;
+                }
+                v += carry;
+                if (q <= T2) pjk[q] = v;
+                carry = __shfl_sync(0xffffffffu, v, 31);
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < CPB * 16; idx += S3_THREADS) {
+            const int k = idx / 16, i = idx % 16;
+            float vm = 0.f, d = 0.f;
+            if (i < g.n_bins) {
+                const int vmi = i > 0 ? sV[k * 16 + i - 1] : 0;
+                vm = (float)vmi;
+                d = 2.f * ((float)i * vm - sPJ[k * (T2 + 1) + vmi]);
+            }
+            sVD[(k * 16 + i) * 2] = vm;
+            sVD[(k * 16 + i) * 2 + 1] = d;
+        }
+        __syncthreads();
+
+        // ---- pass 1: scoring
+        if (is_p) {
+            produce(false);
+        } else {
+            float Vm[4], Dv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                Vm[j] = sVD[(cs * 16 + grp4 + j) * 2];
+                Dv[j] = sVD[(cs * 16 + grp4 + j) * 2 + 1];
+            }
+            float ring[T][4];
+            float vs[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                vs[j] = 0.f;
+#pragma unroll
+                for (int q = 0; q < T; ++q) ring[q][j] = 0.f;
+            }
+            for (int c = 0; c < n_chunks; ++c) {
+                const int b = c & 1;
+                const int s0 = c * T;
+                bar_sync(BAR_FULL0 + b, S3_THREADS);
+                const uint4* wh = WHb + b * WHSTRIDE;
+                // ---- E: closed-form transport, register ring, vertical box
+#pragma unroll
+                for (int rho = 0; rho < T; ++rho) {
+                    const uint4 v = wh[(rho * CPB + cs) * W + x];
+                    const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
+                    const uint32_t prev = grp == 1 ? v.x : grp == 2 ? v.y : grp == 3 ? v.z : 0u;
+                    const bool mass = (word >> 24) != (prev >> 24);
+                    if (__any_sync(0xffffffffu, mass)) {
+                        const uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                        float af = __uint_as_float(ma) - 8388608.0f;
+                        float pja = pj[ma - 0x4B000000u];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t mbits = __byte_perm(word, 0x4B000000u, 0x7650 + j);
+                            const float bf = __uint_as_float(mbits) - 8388608.0f;
+                            const float pjb = pj[mbits - 0x4B000000u];
+                            const float fi = (float)(grp4 + j);
+                            const float nua = fmaf(fi, af, -pja);
+                            const float nub = fmaf(fi, bf, -pjb);
+                            const float ga = af < Vm[j] ? nua : Dv[j] - nua;
+                            const float gb = bf < Vm[j] ? nub : Dv[j] - nub;
+                            const float pc = bf - af;
+                            const float E = (gb - ga) * rcp_approx3(fmaxf(pc, 1.f));
+                            vs[j] += E - ring[rho][j];
+                            ring[rho][j] = E;
+                            af = bf;
+                            pja = pjb;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            vs[j] -= ring[rho][j];
+                            ring[rho][j] = 0.f;
+                        }
+                    }
+                    if (rho == T - 1) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            float s = ring[0][j];
+#pragma unroll
+                            for (int q = 1; q < T; ++q) s += ring[q][j];
+                            vs[j] = s;
+                        }
+                    }
+                    if (s0 + rho >= 2 * R) {
+                        float* vb = Vb + ((rho * CPB + cs) * 16 + grp4) * W + x;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
+                    }
+                }
+                if (c + 2 < n_chunks) bar_arrive(BAR_EMPTY0 + b, S3_THREADS);
+                bar_sync(BAR_C, S3_CT);  // Vb complete
+                // ---- A: own-bin horizontal box, slots in fixed order, partial RMW
+                for (int rho = a_r0; rho < T; rho += A_ROWS) {
+                    const int y = s0 + rho - 2 * R;
+                    if (y < 0 || y >= h) continue;
+                    float acc = 0.f;
+#pragma unroll
+                    for (int k = 0; k < CPB; ++k) {
+                        const float scale = sscale[k];
+                        if (scale == 0.f) continue;
+                        const int bb = sb[k * hw + y * W + a_x];
+                        const float* vb = Vb + ((rho * CPB + k) * 16 + bb) * W;
+                        float f = 0.f;
+                        if (a_x >= R && a_x + R < W) {
+#pragma unroll
+                            for (int d = -R; d <= R; ++d) f += vb[a_x + d];
+                        } else {
+#pragma unroll
+                            for (int d = 0; d < T; ++d) f += vb[xmap[a_x + d]];
+                        }
+                        acc = fmaf(f, scale, acc);
+                    }
+                    part[y * W + a_x] += acc;
+                }
+                bar_sync(BAR_C, S3_CT);  // Vb may be overwritten
+            }
+        }
+    }
+}
+
+int sample_stride(int h, int w, int budget);
+
+template <int T, int W>
+static int s3_total(Score3Geom& g) {
+    score3_layout<T, W>(g);
+    return g.total;
+}
+
+static int score3_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                       int pad, int budget, bool fused_ref, Score3Geom* out, size_t* smem_out) {
+    if (t < 1 || t > 15 || (t & 1) == 0 || n_bins > 16) return QFCA_ERR_UNSUPPORTED;
+    if (w != 32 && w != 64 && w != 128) return QFCA_ERR_UNSUPPORTED;
+    if ((int64_t)h * w > (1 << 24) || ((int64_t)h * w) % 16) return QFCA_ERR_UNSUPPORTED;
+    if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
+    Score3Geom g;
+    memset(&g, 0, sizeof(g));
+    g.h = h; g.n_bins = n_bins; g.pad = pad; g.C = C;
+    g.WP = w + 2 * (t / 2);
+    g.S = h + 2 * (t / 2);
+    g.fref = fused_ref && t * t <= 126 && budget >= 1 && (pad == QFCA_PAD_WRAP || h > 1) ? 1 : 0;
+    if (g.fref) {
+        g.stride = sample_stride(h, w, budget);
+        g.nsx = (w + g.stride - 1) / g.stride;
+        g.nsamp = ((h + g.stride - 1) / g.stride) * g.nsx;
+        g.sp = (g.nsamp + 3) & ~3;
+    }
+    size_t bytes = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        switch (t * 1000 + w) {
+#define S3C(TT, WW) case TT * 1000 + WW: bytes = s3_total<TT, WW>(g); break;
+            S3C(1, 32) S3C(1, 64) S3C(1, 128) S3C(3, 32) S3C(3, 64) S3C(3, 128)
+            S3C(5, 32) S3C(5, 64) S3C(5, 128) S3C(7, 32) S3C(7, 64) S3C(7, 128)
+            S3C(9, 32) S3C(9, 64) S3C(9, 128) S3C(11, 32) S3C(11, 64) S3C(11, 128)
+            S3C(13, 32) S3C(13, 64) S3C(13, 128) S3C(15, 32) S3C(15, 64) S3C(15, 128)
+#undef S3C
+            default: return QFCA_ERR_UNSUPPORTED;
+        }
+        if (bytes <= 225 * 1024) break;
+        if (!g.fref) return QFCA_ERR_UNSUPPORTED;
+        g.fref = 0;
+    }
+    if (bytes > 225 * 1024) return QFCA_ERR_UNSUPPORTED;
+    const int cpb = 128 / w;
+    int groups = groups_hint;
+    if (groups <= 0) {
+        const int64_t want = 4 * 148;
+        int64_t gg = (want + images - 1) / images;
+        gg = gg < 1 ? 1 : gg;
+        const int64_t maxg = (C + cpb - 1) / cpb;
+        gg = gg > maxg ? maxg : gg;
+        groups = (int)gg;
+    }
+    groups = groups < 1 ? 1 : (groups > C ? C : groups);
+    g.cpg = (C + groups - 1) / groups;
+    g.groups = (C + g.cpg - 1) / g.cpg;
+    *out = g;
+    *smem_out = bytes;
+    return QFCA_OK;
+}
+
+int score3_query(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                 int pad, int budget, int want_fref, int* fref) {
+    Score3Geom g;
+    size_t smem;
+    if (score3_plan(h, w, n_bins, t, C, images, groups_hint, pad, budget, want_fref != 0, &g,
+                    &smem) != QFCA_OK)
+        return -1;
+    if (fref) *fref = g.fref;
+    return g.groups;
+}
+
+int launch_score3(const void* bins, int bins_bytes, const float* lo, const float* hi,
+                  const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
+                  int pad, int budget, int groups, float* partial, cudaStream_t st) {
+    if (bins_bytes != 1) return QFCA_ERR_UNSUPPORTED;
+    Score3Geom g;
+    size_t smem;
+    int rc = score3_plan(h, w, n_bins, t, C, images, groups, pad, budget, V == nullptr, &g,
+                         &smem);
+    if (rc != QFCA_OK) return rc;
+    if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
+    if (V == nullptr && !g.fref) return QFCA_ERR_UNSUPPORTED;
+    void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score3Geom,
+                 float*) = nullptr;
+    switch (t * 1000 + w) {
+#define S3K(TT, WW) case TT * 1000 + WW: kern = k_score3<TT, WW>; break;
+        S3K(1, 32) S3K(1, 64) S3K(1, 128) S3K(3, 32) S3K(3, 64) S3K(3, 128)
+        S3K(5, 32) S3K(5, 64) S3K(5, 128) S3K(7, 32) S3K(7, 64) S3K(7, 128)
+        S3K(9, 32) S3K(9, 64) S3K(9, 128) S3K(11, 32) S3K(11, 64) S3K(11, 128)
+        S3K(13, 32) S3K(13, 64) S3K(13, 128) S3K(15, 32) S3K(15, 64) S3K(15, 128)
+#undef S3K
+        default: return QFCA_ERR_UNSUPPORTED;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    const int64_t grid = images * g.groups;
+    kern<<<(unsigned)grid, S3_THREADS, smem, st>>>((const uint8_t*)bins, lo, hi, V, g, partial);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+}  // namespace qfca

@@ -243,9 +243,13 @@ def test_large_plane_properties(Q):
                                            ((2, 20, 32, 32), 16, 3, "wrap"),
                                            ((2, 24, 48, 40), 8, 15, "reflect"),
                                            ((1, 16, 20, 24), 32, 5, "reflect"),
-                                           ((2, 12, 9, 16), 16, 7, "wrap")])
+                                           ((2, 12, 9, 16), 16, 7, "wrap"),
+                                           ((2, 20, 64, 32), 12, 15, "reflect"),
+                                           ((1, 24, 16, 128), 16, 11, "wrap"),
+                                           ((1, 8, 1, 64), 16, 5, "wrap")])
 def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
-    """v1 (score.cu) and v2 (score2.cu) fused kernels both match the oracle."""
+    """v1 (score.cu), v2 (score2.cu) and v3 (score3.cu) fused kernels all match
+    the oracle wherever they apply."""
     from paper_2510_15602_b200 import _native
     from oracle import qfca_oracle as O
     rng = np.random.default_rng(sum(shape) + n + t)
@@ -253,7 +257,13 @@ def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
     cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
     refs = [O.detect(x[i], n_bins=n, patch_size=t, pad=pad)[0] for i in range(shape[0])]
     try:
-        for ver in (1, 2):
+        for ver in (1, 2, 3):
+            _native.call("qfca_set_score_kernel", ver)
+            if ver > 1 and Q.fused_supported(cfg):
+                try:
+                    Q.detect_batch(torch.from_numpy(x[:1]).cuda(), cfg)
+                except NotImplementedError:
+                    continue  # this kernel version does not cover the shape
             _native.call("qfca_set_score_kernel", ver)
             res = Q.detect_batch(torch.from_numpy(x).cuda(), cfg)
             for i in range(shape[0]):
