@@ -3,19 +3,23 @@
 // Same mathematics and data layout as score2.cu (see its header); the
 // difference is the execution schedule.  The CTA has 20 warps:
 //
-//   4 producer warps (P)   H1 + H2: column trackers and row windows of the
-//                          thermometer counts for stream chunk c+1, written
-//                          to the double-buffered window store WH[(c+1)&1];
-//   16 consumer warps (C)  E + A: closed-form transport, register E ring,
-//                          vertical box, own-bin horizontal box and the
-//                          partial-map update for chunk c from WH[c&1].
+//   4 producer warps (P)   H1: one column tracker per thread slides the
+//                          thermometer counts down the row stream and writes
+//                          chunk c+1's column words to the double-buffered
+//                          store CHp[(c+1)&1];
+//   16 consumer warps (C)  H2 (row windows -> cumulative counts), E (closed-
+//                          form transport, register E ring, vertical box) and
+//                          A (own-bin horizontal box, partial-map update) for
+//                          chunk c.
 //
-// Hand-off uses named barriers (bar.arrive / bar.sync), so producers never
-// wait for the association phase and consumers never wait for the histogram
-// phase; the only CTA-wide barriers are once per channel batch.  The fused
-// reference selection (pass 0) runs the producers over the sample rows while
-// the consumers gather the sample counts.  Fixed plane widths 32 / 64 / 128
-// with N <= 16 bins (4 groups of 4) and T <= 15.
+// Hand-off uses named barriers (bar.arrive / bar.sync): FULL[b] (producers ->
+// consumers) and EMPTY[b] (consumers -> producers); the consumers synchronise
+// among themselves on BAR_C; CTA-wide barriers only once per channel batch.
+// The consumer phases are arranged as  E(c) | A(c) + H2(c+1)  so each chunk
+// costs two consumer barriers.  The fused reference selection (pass 0) runs
+// the same producer loop while the consumers window only the sample rows and
+// gather the sample counts.  Fixed plane widths 32 / 64 / 128, N <= 16 bins
+// (4 groups of 4), T <= 15.
 #include <string.h>
 
 #include "common.cuh"
@@ -29,7 +33,7 @@ constexpr int S3_PT = S3_PWARPS * 32;            // producer threads
 constexpr int S3_THREADS = S3_CT + S3_PT;        // 640
 constexpr int S3_MAXSEG = 33;
 // named barrier ids (0 is __syncthreads)
-constexpr int BAR_P = 1, BAR_C = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5;
+constexpr int BAR_C = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5;
 
 struct Score3Geom {
     int h, n_bins, pad, C, groups, cpg;
@@ -51,10 +55,11 @@ __device__ __forceinline__ float rcp_approx3(float x) {
     return y;
 }
 
-// H2 segment: rows * nseg <= S3_PT, odd length (distinct banks per warp)
+// consumer H2 segment: odd (distinct banks across a warp), >= 5 columns,
+// rows * segments <= consumer threads
 __host__ __device__ constexpr int s3_seg(int t, int w) {
-    return ((w + ((S3_PT / (t * (128 / w))) > 0 ? (S3_PT / (t * (128 / w))) : 1) - 1) /
-            ((S3_PT / (t * (128 / w))) > 0 ? (S3_PT / (t * (128 / w))) : 1)) | 1;
+    return ((((w * t * (128 / w) + S3_CT - 1) / S3_CT) > 5
+                 ? ((w * t * (128 / w) + S3_CT - 1) / S3_CT) : 5)) | 1;
 }
 
 template <int T, int W>
@@ -70,8 +75,8 @@ static void score3_layout(Score3Geom& g) {
     g.o_pj = take((long long)CPB * (T * T + 1) * 4);
     g.o_vd = take((long long)CPB * 16 * 2 * 4);
     g.o_stab = take((long long)((g.S + T - 1) / T) * T * 16);
-    g.o_chp = take((long long)T * CPB * g.WP * 16);       // uint4 per padded column
-    g.o_wh = take((long long)2 * T * CPB * W * 16);       // double-buffered uint4 windows
+    g.o_chp = take((long long)2 * T * CPB * g.WP * 16);   // double-buffered column words
+    g.o_wh = take((long long)T * CPB * W * 16);           // row windows (uint4 per pixel)
     const long long vb = (long long)T * CPB * 16 * W * 4;
     const long long sa = g.fref ? (long long)CPB * 16 * g.sp : 0;
     g.o_vb = take(vb > sa ? vb : sa);
@@ -93,7 +98,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     constexpr int CPB = 128 / W;  // channel slots: CPB * W = 128 columns per CTA pass
     constexpr int SEG = s3_seg(T, W);
     constexpr int NSEG = (W + SEG - 1) / SEG;
-    static_assert(T * CPB * NSEG <= S3_PT, "H2 tasks must fit the producer warps");
+    static_assert(T * CPB * NSEG <= S3_CT, "H2 tasks must fit the consumer warps");
     static_assert(SEG <= S3_MAXSEG, "segment too long");
     extern __shared__ __align__(16) uint8_t sm[];
     uint8_t* const sb = sm + g.o_bins;
@@ -101,7 +106,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     float* const sVD = reinterpret_cast<float*>(sm + g.o_vd);
     int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);
     uint4* const CHp = reinterpret_cast<uint4*>(sm + g.o_chp);
-    uint4* const WHb = reinterpret_cast<uint4*>(sm + g.o_wh);
+    uint4* const WH = reinterpret_cast<uint4*>(sm + g.o_wh);
     float* const Vb = reinterpret_cast<float*>(sm + g.o_vb);
     int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
     float* const sscale = reinterpret_cast<float*>(sm + g.o_scale);
@@ -117,7 +122,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int c_begin = cgi * g.cpg, c_end = min(g.C, c_begin + g.cpg);
     float* const part = partial + ((int64_t)img * g.groups + cgi) * hw;
     const int n_chunks = (g.S + T - 1) / T;
-    const int WHSTRIDE = T * CPB * W;  // uint4 per buffer
+    const int CHSTRIDE = T * CPB * g.WP;  // uint4 per CHp buffer
 
     // ---- per-CTA tables (see score2.cu): stream rows, padded-x map, thermometer words
     for (int s = tid; s < n_chunks * T; s += S3_THREADS) {
@@ -165,7 +170,6 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     }
     const bool many_halo = W <= R;
     const uint8_t* const pbx = sb + pcs * hw + px;
-    uint4* const pch = CHp + pcs * g.WP;
 
     // ---- consumer role: thread (slot cs, group grp, column x)
     const int cs = tid / (4 * W);
@@ -178,11 +182,13 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     constexpr int A_ROWS = S3_CT / W;  // A-phase rows per pass
     const int a_x = tid % W, a_r0 = tid / W;
 
+    // H1 (producers) for chunk c into CHp[c & 1]
     uint4 cst = make_uint4(0, 0, 0, 0);
-    auto h1_chunk = [&](int s0) {
+    auto h1_chunk = [&](int c) {
+        uint4* base = CHp + (c & 1) * CHSTRIDE + pcs * g.WP;
 #pragma unroll
         for (int rho = 0; rho < T; ++rho) {
-            const int4 st = stab[s0 + rho];
+            const int4 st = stab[c * T + rho];
             if (st.z < 0) {
                 const uint4 a = TH[pbx[st.x]], r = TH[pbx[st.y]];
                 cst.x += a.x - r.x;
@@ -200,7 +206,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     cst.w += a.w;
                 }
             }
-            uint4* row = pch + rho * CPB * g.WP;
+            uint4* row = base + rho * CPB * g.WP;
             row[px + R] = cst;
             if (halo0 >= 0) row[halo0] = cst;
             if (halo1 >= 0) row[halo1] = cst;
@@ -212,14 +218,23 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
     };
-    auto h2_chunk = [&](int s0, uint4* wh, bool only_samples) {
-        const int task = pt;
+    auto produce = [&]() {
+        for (int c = 0; c < n_chunks; ++c) {
+            const int b = c & 1;
+            if (c >= 2) bar_sync(BAR_EMPTY0 + b, S3_THREADS);  // consumers done with CHp[b]
+            h1_chunk(c);
+            bar_arrive(BAR_FULL0 + b, S3_THREADS);
+        }
+    };
+    // H2 (consumers): CHp[c & 1] -> WH (row windows of chunk c)
+    auto h2_chunk = [&](int c, bool only_samples) {
+        const int task = tid;
         if (task >= T * CPB * NSEG) return;
         const int rc = task / NSEG;  // rho * CPB + cs
         const int x0 = (task - rc * NSEG) * SEG;
-        if (only_samples && stab[s0 + rc / CPB].w < 0) return;
-        const uint4* src = CHp + rc * g.WP + x0;
-        uint4* dst = wh + rc * W + x0;
+        if (only_samples && stab[c * T + rc / CPB].w < 0) return;
+        const uint4* src = CHp + (c & 1) * CHSTRIDE + rc * g.WP + x0;
+        uint4* dst = WH + rc * W + x0;
         uint4 sum = make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int p = 0; p < T; ++p) {
@@ -251,17 +266,11 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
     };
-    // producer loop over one pass: chunk c goes to WH buffer c & 1
-    auto produce = [&](bool only_samples) {
-        for (int c = 0; c < n_chunks; ++c) {
-            const int b = c & 1;
-            h1_chunk(c * T);
-            bar_sync(BAR_P, S3_PT);  // CHp complete
-            if (c >= 2) bar_sync(BAR_EMPTY0 + b, S3_THREADS);  // consumers done with buffer b
-            h2_chunk(c * T, WHb + b * WHSTRIDE, only_samples);
-            bar_arrive(BAR_FULL0 + b, S3_THREADS);
-            bar_sync(BAR_P, S3_PT);  // CHp may be overwritten
-        }
+    // consumer: wait for chunk c's column words, window them, release CHp[c & 1]
+    auto consume_h2 = [&](int c, bool only_samples) {
+        bar_sync(BAR_FULL0 + (c & 1), S3_THREADS);
+        h2_chunk(c, only_samples);
+        if (c + 2 < n_chunks) bar_arrive(BAR_EMPTY0 + (c & 1), S3_THREADS);
     };
 
     for (int cb = c_begin; cb < c_end; cb += CPB) {
@@ -296,25 +305,24 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         if (g.fref) {
             // ---- pass 0: reference selection from the sample-row windows
             if (is_p) {
-                produce(true);
+                produce();
             } else {
                 for (int c = 0; c < n_chunks; ++c) {
-                    const int b = c & 1;
-                    bar_sync(BAR_FULL0 + b, S3_THREADS);
+                    consume_h2(c, true);
+                    bar_sync(BAR_C, S3_CT);  // WH complete
                     if (xsamp >= 0) {
-                        const uint4* wh = WHb + b * WHSTRIDE;
                         uint8_t* sa = SA + (cs * 16 + grp4) * g.sp + xsamp;
 #pragma unroll
                         for (int rho = 0; rho < T; ++rho) {
                             const int si = stab[c * T + rho].w;
                             if (si < 0) continue;
-                            const uint4 v = wh[(rho * CPB + cs) * W + x];
+                            const uint4 v = WH[(rho * CPB + cs) * W + x];
                             const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
 #pragma unroll
                             for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
                         }
                     }
-                    if (c + 2 < n_chunks) bar_arrive(BAR_EMPTY0 + b, S3_THREADS);
+                    bar_sync(BAR_C, S3_CT);  // WH may be overwritten
                 }
             }
             __syncthreads();
@@ -396,7 +404,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 
         // ---- pass 1: scoring
         if (is_p) {
-            produce(false);
+            produce();
         } else {
             float Vm[4], Dv[4];
 #pragma unroll
@@ -412,15 +420,14 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll
                 for (int q = 0; q < T; ++q) ring[q][j] = 0.f;
             }
+            consume_h2(0, false);
+            bar_sync(BAR_C, S3_CT);  // WH(0) complete
             for (int c = 0; c < n_chunks; ++c) {
-                const int b = c & 1;
                 const int s0 = c * T;
-                bar_sync(BAR_FULL0 + b, S3_THREADS);
-                const uint4* wh = WHb + b * WHSTRIDE;
-                // ---- E: closed-form transport, register ring, vertical box
+                // ---- E(c): closed-form transport, register ring, vertical box
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
-                    const uint4 v = wh[(rho * CPB + cs) * W + x];
+                    const uint4 v = WH[(rho * CPB + cs) * W + x];
                     const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
                     const uint32_t prev = grp == 1 ? v.x : grp == 2 ? v.y : grp == 3 ? v.z : 0u;
                     const bool mass = (word >> 24) != (prev >> 24);
@@ -467,9 +474,8 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
                     }
                 }
-                if (c + 2 < n_chunks) bar_arrive(BAR_EMPTY0 + b, S3_THREADS);
-                bar_sync(BAR_C, S3_CT);  // Vb complete
-                // ---- A: own-bin horizontal box, slots in fixed order, partial RMW
+                bar_sync(BAR_C, S3_CT);  // Vb complete, WH free
+                // ---- A(c): own-bin horizontal box, slots in fixed order, partial RMW
                 for (int rho = a_r0; rho < T; rho += A_ROWS) {
                     const int y = s0 + rho - 2 * R;
                     if (y < 0 || y >= h) continue;
@@ -492,7 +498,9 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     }
                     part[y * W + a_x] += acc;
                 }
-                bar_sync(BAR_C, S3_CT);  // Vb may be overwritten
+                // ---- H2(c+1) in the same phase (WH is free, Vb is only read)
+                if (c + 1 < n_chunks) consume_h2(c + 1, false);
+                bar_sync(BAR_C, S3_CT);  // Vb free, WH(c+1) complete
             }
         }
     }
