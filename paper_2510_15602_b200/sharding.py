@@ -1,0 +1,110 @@
+"""Multi-GPU layouts of the scoring path.
+
+* Batches of images: every image is independent -> shard the batch, one
+  process per GPU, no collective (bench.py under torchrun, ``shard_batch``).
+* One very large image (8192^2 -> 512 x 1024^2 features): every stage up to
+  the channel sum is per channel (quantize.py:66-68, 168-199; scoring.py:
+  292-309), so each rank scores a contiguous channel slice and ONE all-reduce
+  (sum) of the (h*w + 1) fp64 partial -- channel-sum map plus the count of
+  used channels -- combines them; every rank then finalises (channel mean,
+  Gaussian, image score) identically.  NCCL over NVLink in production, gloo
+  in the CPU tests.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+from ._dev import empty, zeros
+from .features import _gauss_kernel, sep_convolve_dev
+from .quantize import bins_dev, minmax_dev
+
+__all__ = ["shard_range", "shard_batch", "combine_partials", "channel_partial",
+           "detect_channel_sharded"]
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [start, stop) slice of n items for rank (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world / rank")
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def shard_batch(batch: torch.Tensor, world: int, rank: int) -> torch.Tensor:
+    s, e = shard_range(batch.shape[0], world, rank)
+    return batch[s:e]
+
+
+def combine_partials(acc: torch.Tensor, used: int | torch.Tensor, group=None):
+    """All-reduce(sum) of a rank's channel-sum map and used-channel count.
+
+    One collective on an (h*w + 1) fp64 buffer.  Returns (sum map, total used).
+    """
+    import torch.distributed as dist
+    flat = torch.cat([acc.reshape(-1).to(torch.float64),
+                      torch.as_tensor([float(used)], dtype=torch.float64,
+                                      device=acc.device)])
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat[:-1].reshape(acc.shape), int(round(float(flat[-1])))
+
+
+def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
+    """Channel-sum map (h, w) fp64 and used-channel count for this rank's
+    channel slice (C_local, h, w), fused path (scoring.py:286-309 without the
+    division)."""
+    from .scoring import fused_supported
+    if not fused_supported(cfg):
+        raise NotImplementedError("channel sharding covers the fused configuration")
+    x = values.contiguous()
+    c, h, w = x.shape
+    hw = h * w
+    s = N.stream()
+    lo, hi, flag = minmax_dev(x, c, hw)
+    bins = bins_dev(x, lo, hi, c, hw, cfg.n_bins)
+    L = N.lib()
+    pad = N.PAD_CODES[cfg.pad]
+    groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                 cfg.sample_budget, 0)
+    ref = None
+    if groups <= 0:  # kernel without in-kernel reference selection: run K3 first
+        groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                     cfg.sample_budget, 1)
+        ref = empty((c, cfg.n_bins), torch.int32)
+        N.call("qfca_select_reference", bins.data_ptr(), bins.element_size(), lo.data_ptr(),
+               hi.data_ptr(), c, h, w, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, 0,
+               ref.data_ptr(), s)
+    partial = zeros((groups, hw), torch.float32)
+    N.call("qfca_score", bins.data_ptr(), bins.element_size(), lo.data_ptr(), hi.data_ptr(),
+           None if ref is None else ref.data_ptr(), 1, c, h, w, cfg.n_bins, cfg.patch_size,
+           pad, cfg.sample_budget, groups, partial.data_ptr(), s)
+    used = empty((1,), torch.int32)
+    N.call("qfca_count_used", lo.data_ptr(), hi.data_ptr(), 1, c, used.data_ptr(), s)
+    ones = torch.ones((1,), dtype=torch.int32, device=x.device)
+    acc = empty((1, hw), torch.float64)
+    N.call("qfca_reduce_partials", partial.data_ptr(), 1, groups, hw, ones.data_ptr(),
+           acc.data_ptr(), s)
+    return acc.reshape(h, w), int(used[0])
+
+
+def detect_channel_sharded(values_local: torch.Tensor, cfg=None, group=None):
+    """Score one image whose channels are split across the ranks.
+
+    ``values_local`` is this rank's (C_local, h, w) slice on its GPU.  Returns
+    (scores (h, w) fp64, image_score, degenerate) on every rank.
+    """
+    from .scoring import PipelineConfig
+    cfg = cfg or PipelineConfig()
+    acc, used = channel_partial(values_local, cfg)
+    total, used_all = combine_partials(acc, used, group)
+    h, w = total.shape
+    agg = total / used_all if used_all > 0 else total
+    final = sep_convolve_dev(agg[None].contiguous(), _gauss_kernel(cfg.sigma_s), cfg.pad)[0] \
+        if cfg.sigma_s > 0 else agg
+    img = empty((1,), torch.float64)
+    N.call("qfca_image_score", final.contiguous().data_ptr(), 1, h, w, cfg.border,
+           img.data_ptr(), N.stream())
+    return final, float(img[0]), used_all == 0

@@ -1,0 +1,98 @@
+"""Multi-process (gloo, world size 2, CPU) checks of the sharding logic, and a
+GPU check of the channel-sharded partials.  The per-rank partial on CPU comes
+from the oracle (test-side stand-in for the GPU kernels); the product code
+under test is the channel partition and the single all-reduce."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_range_covers_exactly():
+    from paper_2510_15602_b200.sharding import shard_range
+    for n in (1, 7, 64, 512, 513):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(n, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _worker(rank, world, port, x, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle import qfca_oracle as O
+    from paper_2510_15602_b200.sharding import combine_partials, shard_range
+    s, e = shard_range(x.shape[0], world, rank)
+    _, _, _, st = O.detect(x[s:e], return_stages=True)
+    acc = torch.from_numpy(st["agg"] * max(st["used"], 1) if st["used"] else st["agg"])
+    total, used = combine_partials(acc, st["used"])
+    if rank == 0:
+        out.put((total.numpy(), used))
+    dist.destroy_process_group()
+
+
+def test_channel_sharded_combine_gloo():
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(3)
+    x = np.maximum(rng.standard_normal((10, 20, 24)), 0).astype(np.float32)
+    x[4] = 0.0  # a degenerate channel on rank 0's slice
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, x, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    total, used = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, _, _, st = O.detect(x, return_stages=True)
+    assert used == st["used"] == 9
+    agg = total / used
+    np.testing.assert_allclose(agg, st["agg"], rtol=1e-12, atol=1e-14)
+    final = O.smooth_scores(agg, 1.0)
+    ref, _, _ = O.detect(x)
+    np.testing.assert_allclose(final, ref, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_channel_partials_gpu():
+    """Two channel slices scored separately and summed reproduce detect."""
+    import paper_2510_15602_b200 as Q
+    from paper_2510_15602_b200.sharding import channel_partial, detect_channel_sharded
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(5)
+    x = np.maximum(rng.standard_normal((40, 64, 64)) + 0.1, 0).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    cfg = Q.PipelineConfig()
+    a0, u0 = channel_partial(xt[:17], cfg)
+    a1, u1 = channel_partial(xt[17:], cfg)
+    _, _, _, st = O.detect(x, return_stages=True)
+    assert u0 + u1 == st["used"]
+    agg = ((a0 + a1) / (u0 + u1)).cpu().numpy()
+    assert np.abs(agg - st["agg"]).max() <= 1e-4 * np.abs(st["agg"]).max()
+    final, img, degen = detect_channel_sharded(xt, cfg)  # world size 1
+    ref, img_ref, _ = O.detect(x)
+    assert np.abs(final.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
+    assert not degen
