@@ -113,9 +113,12 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
                       int64_t images, int32_t groups_hint, int32_t pad, int32_t sample_budget,
                       int32_t with_reference);
 
-/* select the fused scoring kernel: 0 = auto (v2 -- compile-time patch size
- * T <= 15, uint8 bins, 4 * G * w <= 512 -- where it applies, else v1),
- * 1 = force v1 (score.cu), 2 = force v2 (score2.cu).  Process-global. */
+/* select the fused scoring kernel: 0 = auto (the first that applies of v4
+ * score4.cu -- plane-resident windows, T <= 11, w in {32, 64, 128}, stride-1
+ * sampling when it selects the reference; v3 score3.cu -- pipelined
+ * warp-specialised, T <= 15; v2 score2.cu; v1 score.cu -- any shape),
+ * 1..4 = force that version (unsupported shapes then return status 3).
+ * Process-global. */
 int qfca_set_score_kernel(int32_t version);
 
 /* THE HOT PATH: _channel_score_kernel + channel accumulation

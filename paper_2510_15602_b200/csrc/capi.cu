@@ -46,14 +46,17 @@ int launch_score2(const void*, int, const float*, const float*, const int32_t*, 
 int score3_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int launch_score3(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
+int score4_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
+int launch_score4(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
+                  int, int, int, int, int, int, float*, cudaStream_t);
 
-// fused-kernel selection: 0 = auto (v3, else v2, else v1 -- the first that
-// applies), 1 / 2 / 3 = force that version
+// fused-kernel selection: 0 = auto (v4, else v3, else v2, else v1 -- the
+// first that applies), 1 / 2 / 3 / 4 = force that version
 static int g_score_kernel = 0;
 
 struct ScoreChoice {
     int groups;  // channel groups (partial maps per image); <= 0: unsupported
-    int ver;     // 3: score3.cu, 2: score2.cu, 1: score.cu
+    int ver;     // 4: score4.cu, 3: score3.cu, 2: score2.cu, 1: score.cu
     int fref;    // 1: the reference is selected inside the kernel
 };
 
@@ -62,6 +65,14 @@ static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t 
                                 int groups_hint, int bins_bytes, int pad, int budget,
                                 int want_fref) {
     ScoreChoice ch{-1, 1, 0};
+    if ((g_score_kernel == 0 || g_score_kernel == 4) && bins_bytes == 1) {
+        int fr = 0;
+        const int gg = score4_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
+                                    want_fref, &fr);
+        // v4 either selects the reference itself or takes the caller's
+        if (gg > 0 && fr == (want_fref ? 1 : 0)) return ScoreChoice{gg, 4, fr};
+    }
+    if (g_score_kernel == 4) return ch;
     if ((g_score_kernel == 0 || g_score_kernel == 3) && bins_bytes == 1) {
         int fr = 0;
         const int gg = score3_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
@@ -85,6 +96,9 @@ static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_by
                             int C, int h, int w, int n_bins, int t, int pad, int budget,
                             float* partial, cudaStream_t st) {
     if (ch.groups <= 0) return QFCA_ERR_UNSUPPORTED;
+    if (ch.ver == 4)
+        return launch_score4(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
+                             n_bins, t, pad, budget, ch.groups, partial, st);
     if (ch.ver == 3)
         return launch_score3(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
                              n_bins, t, pad, budget, ch.groups, partial, st);
@@ -203,7 +217,7 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
 }
 
 int qfca_set_score_kernel(int32_t version) {
-    if (version < 0 || version > 3) return QFCA_ERR_ARG;
+    if (version < 0 || version > 4) return QFCA_ERR_ARG;
     g_score_kernel = version;
     return QFCA_OK;
 }

@@ -246,10 +246,12 @@ def test_large_plane_properties(Q):
                                            ((2, 12, 9, 16), 16, 7, "wrap"),
                                            ((2, 20, 64, 32), 12, 15, "reflect"),
                                            ((1, 24, 16, 128), 16, 11, "wrap"),
-                                           ((1, 8, 1, 64), 16, 5, "wrap")])
+                                           ((1, 8, 1, 64), 16, 5, "wrap"),
+                                           ((2, 30, 48, 64), 16, 7, "reflect"),
+                                           ((1, 9, 32, 128), 10, 1, "reflect")])
 def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
-    """v1 (score.cu), v2 (score2.cu) and v3 (score3.cu) fused kernels all match
-    the oracle wherever they apply."""
+    """v1 (score.cu), v2 (score2.cu), v3 (score3.cu) and v4 (score4.cu) fused
+    kernels all match the oracle wherever they apply."""
     from paper_2510_15602_b200 import _native
     from oracle import qfca_oracle as O
     rng = np.random.default_rng(sum(shape) + n + t)
@@ -257,7 +259,7 @@ def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
     cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
     refs = [O.detect(x[i], n_bins=n, patch_size=t, pad=pad)[0] for i in range(shape[0])]
     try:
-        for ver in (1, 2, 3):
+        for ver in (1, 2, 3, 4):
             _native.call("qfca_set_score_kernel", ver)
             if ver > 1 and Q.fused_supported(cfg):
                 try:
@@ -271,3 +273,23 @@ def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
                 assert e <= TOL, (ver, i, e)
     finally:
         _native.call("qfca_set_score_kernel", 0)
+
+
+@pytest.mark.parametrize("shape,n,t,pad", [((2, 37, 64, 64), 16, 9, "reflect"),
+                                           ((2, 21, 32, 32), 16, 5, "wrap"),
+                                           ((1, 10, 32, 128), 12, 11, "reflect")])
+def test_score4_bit_identical_to_score3(Q, shape, n, t, pad):
+    """score4.cu restates score3.cu's fp32 expressions in the same order: the
+    maps agree bit for bit (both select the reference in-kernel)."""
+    from paper_2510_15602_b200 import _native
+    rng = np.random.default_rng(7 + t)
+    x = torch.from_numpy(np.maximum(rng.standard_normal(shape) + 0.3, 0).astype(np.float32)).cuda()
+    cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
+    out = {}
+    try:
+        for ver in (3, 4):
+            _native.call("qfca_set_score_kernel", ver)
+            out[ver] = Q.detect_batch(x, cfg).scores.cpu().numpy()
+    finally:
+        _native.call("qfca_set_score_kernel", 0)
+    assert np.array_equal(out[3], out[4])
