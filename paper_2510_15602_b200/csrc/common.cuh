@@ -22,6 +22,37 @@ struct Taps {
     int n;
 };
 
+// Channel groups per image for a fused scoring kernel that keeps `per_sm` CTAs
+// resident per SM and scores `cpb` channels per batch: the grid is
+// images x groups CTAs, each scoring batches-per-CTA (bpc) batches, so the
+// run takes ceil(CTAs / resident slots) waves of bpc batch-times.  Minimise
+// waves * (bpc + per-CTA setup), ties to fewer groups (fewer partial maps).
+inline int balanced_groups(int64_t images, int C, int cpb, int per_sm) {
+    static int sms = 0;
+    if (sms <= 0) {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+            sms = n;
+        else
+            sms = 148;
+    }
+    const int64_t slots = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+    const int nb = (C + cpb - 1) / cpb;
+    double best = -1.0;
+    int best_g = 1;
+    for (int bpc = 1; bpc <= nb; ++bpc) {
+        const int g = (nb + bpc - 1) / bpc;
+        const int64_t waves = (images * g + slots - 1) / slots;
+        const double cost = (double)waves * (bpc + 0.25);
+        if (best < 0.0 || cost < best - 1e-9 || (cost < best + 1e-9 && g < best_g)) {
+            best = cost;
+            best_g = g;
+        }
+    }
+    return best_g;
+}
+
 // Padded-plane coordinate -> source index, -1 for zero padding.
 // Restates scoring.py:186-202 (_map_coord): reflect without edge repeat,
 // repeated for large margins; n == 1 -> 0; wrap is toroidal.

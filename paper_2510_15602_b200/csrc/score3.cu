@@ -550,16 +550,10 @@ static int score3_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     if (bytes > 225 * 1024) return QFCA_ERR_UNSUPPORTED;
     const int cpb = 128 / w;
     int groups = groups_hint;
-    if (groups <= 0) {
-        const int64_t want = 4 * 148;
-        int64_t gg = (want + images - 1) / images;
-        gg = gg < 1 ? 1 : gg;
-        const int64_t maxg = (C + cpb - 1) / cpb;
-        gg = gg > maxg ? maxg : gg;
-        groups = (int)gg;
-    }
+    if (groups <= 0) groups = balanced_groups(images, C, cpb, 1);
     groups = groups < 1 ? 1 : (groups > C ? C : groups);
-    g.cpg = (C + groups - 1) / groups;
+    // whole batches per group
+    g.cpg = ((C + groups - 1) / groups + cpb - 1) / cpb * cpb;
     g.groups = (C + g.cpg - 1) / g.cpg;
     *out = g;
     *smem_out = bytes;

@@ -513,8 +513,21 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
             }
             __syncthreads();  // Vb complete
+            // interior columns first, the 2R border columns (padded taps) last,
+            // so that only the last warps take the xmap path
+            constexpr int NI = W - 2 * R;
             for (int task = tid; task < T * W; task += S4_THREADS) {
-                const int rho = task / W, ax = task - rho * W;
+                int rho, ax;
+                if (task < T * NI) {
+                    rho = task / NI;
+                    ax = R + task - rho * NI;
+                } else {
+                    const int b = task - T * NI;
+                    constexpr int NB = 2 * R > 0 ? 2 * R : 1;  // (T = 1: no border)
+                    rho = b / NB;
+                    const int j = b - rho * NB;
+                    ax = j < R ? j : W - 2 * R + j;
+                }
                 const int y = s0 + rho - 2 * R;
                 if (y < 0 || y >= h) continue;
                 float acc = 0.f;
@@ -583,16 +596,10 @@ static int score4_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     if (bytes > (size_t)S4_SMEM_MAX) return QFCA_ERR_UNSUPPORTED;
     const int cpb = 128 / w;
     int groups = groups_hint;
-    if (groups <= 0) {
-        const int64_t want = 4 * 148;
-        int64_t gg = (want + images - 1) / images;
-        gg = gg < 1 ? 1 : gg;
-        const int64_t maxg = (C + cpb - 1) / cpb;
-        gg = gg > maxg ? maxg : gg;
-        groups = (int)gg;
-    }
+    if (groups <= 0) groups = balanced_groups(images, C, cpb, 1);
     groups = groups < 1 ? 1 : (groups > C ? C : groups);
-    g.cpg = (C + groups - 1) / groups;
+    // whole batches per group
+    g.cpg = ((C + groups - 1) / groups + cpb - 1) / cpb * cpb;
     g.groups = (C + g.cpg - 1) / g.cpg;
     *out = g;
     *smem_out = bytes;
