@@ -167,6 +167,17 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
  * top-k subspace eigensolver that replaces np.linalg.eigh, features.py:173) */
 int qfca_cholqr(double* blocks, int64_t batch, int32_t rows, int32_t cols, void* stream);
 
+/* Covariance of pca_fit (features.py:167-171): cov = (x - mean)^T (x - mean) / n
+ * for a batch of images, x (images, C, hw) fp32 channel-major, mean (images, C)
+ * fp64 -> cov (images, C, C) fp64.  fp64-accurate (~1e-11 relative): the
+ * centred values become 32-bit per-channel fixed point, split into int8
+ * digits, and the digit products run exactly on the int8 tensor cores
+ * (tcgen05.mma kind::i8).  Needs hw <= 16384; workspace from
+ * qfca_covariance_workspace_bytes.  Returns 3 (unsupported) otherwise. */
+int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw);
+int qfca_covariance(const float* x, int64_t images, int32_t C, int32_t hw, const double* mean,
+                    void* workspace, int64_t workspace_bytes, double* cov, void* stream);
+
 /* ---- one-call detect (scoring.py:263-327) for the fused configuration ---- */
 typedef struct qfca_config {
     int32_t n_bins;        /* PipelineConfig.n_bins (16) */

@@ -39,6 +39,9 @@ int launch_pca_residual(const float*, int64_t, int, int64_t, const double*, cons
                         int, float*, cudaStream_t);
 int launch_center(const float*, int64_t, int64_t, const double*, float*, cudaStream_t);
 int launch_cholqr(double*, int64_t, int, int, cudaStream_t);
+int64_t cov_i8_workspace(int64_t, int, int);
+int launch_cov_i8(const float*, int64_t, int, int, const double*, void*, int64_t, double*,
+                  cudaStream_t);
 int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int launch_score2(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
@@ -280,6 +283,18 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
 
 int qfca_cholqr(double* blocks, int64_t batch, int32_t rows, int32_t cols, void* stream) {
     return counted(launch_cholqr(blocks, batch, rows, cols, S(stream)), 1);
+}
+
+int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw) {
+    if (images <= 0 || C <= 0 || hw <= 0) return -1;
+    return cov_i8_workspace(images, C, hw);
+}
+
+int qfca_covariance(const float* x, int64_t images, int32_t C, int32_t hw, const double* mean,
+                    void* workspace, int64_t workspace_bytes, double* cov, void* stream) {
+    return counted(launch_cov_i8(x, images, C, hw, mean, workspace, workspace_bytes, cov,
+                                 S(stream)),
+                   2);
 }
 
 // ---------------------------------------------------------------- detect

@@ -135,6 +135,38 @@ def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "fp32"
     return cov / float(hw)
 
 
+_COV_WS: dict = {}
+
+
+def covariance_exact(x: torch.Tensor, mean: torch.Tensor) -> torch.Tensor:
+    """(B, C, H, W) fp32 features, (B, C) fp64 means -> (B, C, C) fp64 covariance
+    (features.py:167-171), fp64-accurate.
+
+    The QFCA+ maps depend on the covariance at the 1e-8 level (an fp32 GEMM
+    moves them by up to 3e-4 on the bench workload through residual bin
+    flips), so the covariance is formed exactly: int8-digit fixed point on
+    the int8 tensor cores (csrc/cov_i8.cu, ~1e-11 relative).  Planes larger
+    than the kernel's exactness bound (hw > 16384) use an fp64 cuBLAS GEMM.
+    """
+    b, c = x.shape[:2]
+    hw = x[0, 0].numel()
+    L = N.lib()
+    need = int(L.qfca_covariance_workspace_bytes(b, c, hw))
+    cov = empty((b, c, c), torch.float64)
+    key = (x.device.index, need)
+    ws = _COV_WS.get(key)
+    if ws is None:
+        _COV_WS.clear()
+        ws = _COV_WS[key] = empty((max(need, 1),), torch.uint8)
+    st = L.qfca_covariance(x.data_ptr(), b, c, hw, mean.data_ptr(), ws.data_ptr(), need,
+                           cov.data_ptr(), N.stream())
+    if st == N.QFCA_ERR_UNSUPPORTED:
+        xd = x.reshape(b, c, hw).double() - mean[:, :, None]
+        return torch.bmm(xd, xd.mT) / float(hw)
+    N.check(st, "qfca_covariance")
+    return cov
+
+
 def _cholqr(y: torch.Tensor) -> torch.Tensor:
     """Orthonormal basis of the columns of y (B, C, p) by Cholesky QR.
 
@@ -193,10 +225,7 @@ def pca_fit_batch(x: torch.Tensor, k: int):
     s = N.stream()
     mean = empty((b, c), torch.float64)
     N.call("qfca_plane_mean", x.data_ptr(), b * c, hw, mean.data_ptr(), s)
-    xc = empty((b, c, hw), torch.float32)
-    N.call("qfca_center", x.data_ptr(), b * c, hw, mean.data_ptr(), xc.data_ptr(), s)
-    cov = covariance_dev(xc)
-    del xc
+    cov = covariance_exact(x, mean)
     # np.argsort(evals, kind="stable")[::-1][:k] of the ascending eigh output is
     # the top-k in descending order (ties keep the higher index first)
     evals, vecs = topk_eigh(cov, k)

@@ -293,3 +293,25 @@ def test_score4_bit_identical_to_score3(Q, shape, n, t, pad):
     finally:
         _native.call("qfca_set_score_kernel", 0)
     assert np.array_equal(out[3], out[4])
+
+
+@pytest.mark.parametrize("b,c,h,w", [(2, 512, 64, 64), (3, 37, 20, 24), (1, 130, 48, 40),
+                                     (2, 64, 128, 128)])
+def test_covariance_exact_vs_fp64(Q, b, c, h, w):
+    """csrc/cov_i8.cu: int8-digit tensor-core covariance against an fp64 GEMM of
+    the fp64-centred values (the reference's arithmetic, features.py:167-171)."""
+    from paper_2510_15602_b200 import features as F
+    from paper_2510_15602_b200 import _native as N
+    rng = np.random.default_rng(b * c + h)
+    x = np.maximum(rng.standard_normal((b, c, h, w)) * rng.uniform(0.1, 30, (b, c, 1, 1)), 0)
+    x[:, 3] = 1.25  # constant channel: zero row / column
+    xt = torch.from_numpy(x.astype(np.float32)).cuda()
+    mean = torch.empty((b, c), dtype=torch.float64, device="cuda")
+    N.call("qfca_plane_mean", xt.data_ptr(), b * c, h * w, mean.data_ptr(), N.stream())
+    cov = F.covariance_exact(xt, mean)
+    xd = xt.reshape(b, c, h * w).double() - mean[:, :, None]
+    ref = torch.bmm(xd, xd.mT) / float(h * w)
+    err = ((cov - ref).abs().amax(dim=(1, 2)) / ref.abs().amax(dim=(1, 2))).max().item()
+    assert err <= 1e-9, err
+    assert torch.equal(cov, cov.mT)  # mirrored tiles are bit-identical
+    assert float(cov[:, 3].abs().max()) == 0.0
