@@ -167,6 +167,18 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
  * top-k subspace eigensolver that replaces np.linalg.eigh, features.py:173) */
 int qfca_cholqr(double* blocks, int64_t batch, int32_t rows, int32_t cols, void* stream);
 
+/* Cholesky-QR factor of a batch of p x p Gram matrices G = Y^T Y (p <= 32):
+ * rinv = R^-1 with G = R^T R, so Y R^-1 has orthonormal columns (subspace
+ * iteration of the top-k eigensolver replacing np.linalg.eigh,
+ * features.py:173).  A numerically singular pivot yields a zero column. */
+int qfca_chol_rinv(const double* gram, int64_t batch, int32_t p, double* rinv, void* stream);
+
+/* Eigen-decomposition of a batch of symmetric p x p matrices (p <= 32) by
+ * cyclic parallel Jacobi: evals (batch, p) descending, evecs (batch, p, p)
+ * with eigenvector j in column j (Rayleigh-Ritz step of the same solver). */
+int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, double* evecs,
+                 void* stream);
+
 /* Covariance of pca_fit (features.py:167-171): cov = (x - mean)^T (x - mean) / n
  * for a batch of images, x (images, C, hw) fp32 channel-major, mean (images, C)
  * fp64 -> cov (images, C, C) fp64.  fp64-accurate (~1e-11 relative): the

@@ -58,6 +58,8 @@ _SIGNATURES = {
     "qfca_plane_mean": ([_P, _I64, _I64, _P, _P], _I32),
     "qfca_center": ([_P, _I64, _I64, _P, _P, _P], _I32),
     "qfca_cholqr": ([_P, _I64, _I32, _I32, _P], _I32),
+    "qfca_chol_rinv": ([_P, _I64, _I32, _P, _P], _I32),
+    "qfca_sym_eig": ([_P, _I64, _I32, _P, _P, _P], _I32),
     "qfca_covariance_workspace_bytes": ([_I64, _I32, _I32], _I64),
     "qfca_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),
     "qfca_pca_residual": ([_P, _I64, _I32, _I64, _P, _P, _I32, _I32, _P, _P], _I32),

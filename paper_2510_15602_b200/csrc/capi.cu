@@ -40,6 +40,8 @@ int launch_pca_residual(const float*, int64_t, int, int64_t, const double*, cons
 int launch_center(const float*, int64_t, int64_t, const double*, float*, cudaStream_t);
 int launch_cholqr(double*, int64_t, int, int, cudaStream_t);
 int64_t cov_i8_workspace(int64_t, int, int);
+int launch_chol_rinv(const double*, int64_t, int, double*, cudaStream_t);
+int launch_sym_eig(const double*, int64_t, int, double*, double*, cudaStream_t);
 int launch_cov_i8(const float*, int64_t, int, int, const double*, void*, int64_t, double*,
                   cudaStream_t);
 int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
@@ -283,6 +285,15 @@ int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t 
 
 int qfca_cholqr(double* blocks, int64_t batch, int32_t rows, int32_t cols, void* stream) {
     return counted(launch_cholqr(blocks, batch, rows, cols, S(stream)), 1);
+}
+
+int qfca_chol_rinv(const double* gram, int64_t batch, int32_t p, double* rinv, void* stream) {
+    return counted(launch_chol_rinv(gram, batch, p, rinv, S(stream)), 1);
+}
+
+int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, double* evecs,
+                 void* stream) {
+    return counted(launch_sym_eig(h, batch, p, evals, evecs, S(stream)), 1);
 }
 
 int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw) {

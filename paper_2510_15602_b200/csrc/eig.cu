@@ -1,0 +1,327 @@
+// eig.cu -- small dense kernels of the top-k eigensolver (features.topk_eigh),
+// which replaces np.linalg.eigh of pca_fit (features.py:173-176).
+//
+//   k_cqr_step    one Cholesky-QR re-orthonormalisation of a subspace-iteration
+//                 block Y (C x p, C <= 512, p <= 32) per CTA: Gram (register
+//                 4 x 4 blocks over 8 row slices), Cholesky + R^-1 on one warp,
+//                 X = Y R^-1 in place, the block resident in shared memory.
+//   k_chol_rinv   the same Cholesky -> R^-1 for a batch of p x p Gram matrices
+//                 (blocks too tall for k_cqr_step).
+//   k_sym_eig     cyclic parallel Jacobi (round-robin pairing, all p/2
+//                 rotations of a round applied at once) for the p x p
+//                 Rayleigh-Ritz matrices, one warp per matrix, eigenpairs
+//                 sorted by descending eigenvalue.
+// They replace cuSOLVER calls whose error checks synchronise the host.
+#include "common.cuh"
+
+namespace qfca {
+
+constexpr int EIG_MAXP = 32;
+constexpr int EIG_LD = EIG_MAXP + 1;  // odd row stride: column walks hit distinct banks
+
+// Cholesky G = L L^T and Rinv = R^-1 = (L^-1)^T on one warp, registers only:
+// lane i holds row i of G / L (l[]) and column i of L^-1 (x[]); the entries a
+// lane needs from another row arrive by shuffle.  A pivot below the floor
+// marks a numerically rank-deficient block: that column of R^-1 is zero (the
+// iteration keeps a zero vector instead of NaN).  G (row-major, ldg) is read
+// from shared memory, Rinv written to shared memory (row-major, EIG_LD).
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __shfl_sync(0xffffffffu, v, src);
+}
+
+__device__ void warp_chol_rinv(const double* G, int ldg, double (*Ls)[EIG_LD], double* sD,
+                               double (*Ri)[EIG_LD], int p, int lane) {
+    {  // Cholesky in registers: lane i holds row i
+        double l[EIG_MAXP];
+#pragma unroll
+        for (int j = 0; j < EIG_MAXP; ++j) l[j] = (lane < p && j < p) ? G[lane * ldg + j] : 0.0;
+        const double floor_ = 1e-300 + 1e-28 * fabs(shfl_d(l[0], 0));
+#pragma unroll
+        for (int k = 0; k < EIG_MAXP; ++k) {
+            const double g = shfl_d(l[k], k);
+            const bool ok = k < p && g > floor_;
+            const double d = ok ? sqrt(g) : 0.0;
+            const double id = ok ? 1.0 / d : 0.0;
+            if (lane == 0) sD[k] = id;
+            if (lane == k) l[k] = d;
+            else if (lane > k) l[k] *= id;
+            const double lk = l[k];  // L[lane][k]
+#pragma unroll
+            for (int j = k + 1; j < EIG_MAXP; ++j) {
+                const double ljk = shfl_d(lk, j);  // L[j][k]
+                if (lane > k) l[j] = fma(-lk, ljk, l[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < EIG_MAXP; ++j) Ls[lane][j] = l[j];
+    }
+    __syncwarp();
+    // x[i] = (L^-1)[i][lane] by forward substitution (rows of L broadcast from smem)
+    double x[EIG_MAXP];
+#pragma unroll
+    for (int i = 0; i < EIG_MAXP; ++i) {
+        double s = i == lane ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < i; ++j) s = fma(-Ls[i][j], x[j], s);
+        x[i] = i < lane ? 0.0 : s * sD[i];
+    }
+    // Rinv[lane][i] = (L^-1)[i][lane]
+    if (lane < p) {
+#pragma unroll
+        for (int i = 0; i < EIG_MAXP; ++i)
+            if (i < p) Ri[lane][i] = x[i];
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- fused CholQR step
+constexpr int CQ_THREADS = 512;
+constexpr int CQ_MAXC = 512;
+constexpr int CQ_SLICES = 8;
+
+__global__ void __launch_bounds__(CQ_THREADS, 1)
+k_cqr_step(double* __restrict__ Y, int C, int p) {
+    extern __shared__ __align__(16) double cq[];
+    double(*sY)[EIG_LD] = reinterpret_cast<double(*)[EIG_LD]>(cq);                   // [C]
+    double(*sP)[EIG_MAXP][EIG_LD] =
+        reinterpret_cast<double(*)[EIG_MAXP][EIG_LD]>(cq + (size_t)C * EIG_LD);      // [8]
+    double(*sR)[EIG_LD] = sP[0];     // R^-1 (slice 0 reused)
+    const int tid = threadIdx.x;
+    double* blk = Y + (size_t)blockIdx.x * C * p;
+    for (int i = tid; i < C * EIG_MAXP; i += CQ_THREADS) {
+        const int r = i / EIG_MAXP, c = i % EIG_MAXP;
+        sY[r][c] = c < p ? blk[r * p + c] : 0.0;
+    }
+    __syncthreads();
+    {  // Gram partials: slice s, 4 x 4 block (bi, bj)
+        const int s = tid / 64, bidx = tid % 64, bi = bidx / 8, bj = bidx % 8;
+        const int r0 = s * C / CQ_SLICES, r1 = (s + 1) * C / CQ_SLICES;
+        double acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+        for (int r = r0; r < r1; ++r) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = sY[r][4 * bi + u];
+                b[u] = sY[r][4 * bj + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();  // (no reader of sP yet; keeps the slices' writes ordered)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) sP[s][4 * bi + u][4 * bj + v] = acc[u][v];
+    }
+    __syncthreads();
+    for (int e = tid; e < EIG_MAXP * EIG_MAXP; e += CQ_THREADS) {
+        const int i = e / EIG_MAXP, j = e % EIG_MAXP;
+        double g = 0.0;
+#pragma unroll
+        for (int s = 0; s < CQ_SLICES; ++s) g += sP[s][i][j];
+        sP[CQ_SLICES - 1][i][j] = g;  // stage in the last slice (slice 0 gets reused)
+    }
+    __syncthreads();
+    if (tid < 32)
+        warp_chol_rinv(&sP[CQ_SLICES - 1][0][0], EIG_LD, sP[1], &sP[2][0][0], sR, p, tid);
+    __syncthreads();
+    // X = Y R^-1 row by row, in place (column j needs Y columns <= j)
+    for (int r = tid; r < C; r += CQ_THREADS) {
+        double y[EIG_MAXP];
+#pragma unroll
+        for (int i = 0; i < EIG_MAXP; ++i) y[i] = sY[r][i];
+#pragma unroll
+        for (int j = EIG_MAXP - 1; j >= 0; --j) {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i <= j; ++i) s = fma(y[i], sR[i][j], s);
+            y[j] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < EIG_MAXP; ++i) sY[r][i] = y[i];
+    }
+    __syncthreads();
+    for (int i = tid; i < C * p; i += CQ_THREADS) blk[i] = sY[i / p][i % p];
+}
+
+size_t cqr_step_smem(int C) {
+    return ((size_t)C * EIG_LD + (size_t)CQ_SLICES * EIG_MAXP * EIG_LD) * sizeof(double);
+}
+
+int launch_cqr_step(double* Y, int64_t batch, int C, int p, cudaStream_t st) {
+    if (batch <= 0 || C <= 0 || p <= 0 || p > C) return QFCA_ERR_ARG;
+    if (p > EIG_MAXP || C > CQ_MAXC) return QFCA_ERR_UNSUPPORTED;
+    const size_t smem = cqr_step_smem(C);
+    if (cudaFuncSetAttribute(k_cqr_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    k_cqr_step<<<(unsigned)batch, CQ_THREADS, smem, st>>>(Y, C, p);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- batched Gram -> R^-1
+constexpr int CR_WARPS = 2;  // matrices per CTA (static shared memory)
+
+__global__ void __launch_bounds__(CR_WARPS * 32)
+k_chol_rinv(const double* __restrict__ gram, int64_t batch, int p, double* __restrict__ rinv) {
+    __shared__ double sL[CR_WARPS][EIG_MAXP][EIG_LD];
+    __shared__ double sI[CR_WARPS][EIG_MAXP][EIG_LD];
+    __shared__ double sD[CR_WARPS][EIG_MAXP];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m = (int64_t)blockIdx.x * CR_WARPS + w;
+    if (m >= batch) return;
+    const double* G = gram + m * p * p;
+    for (int i = 0; i < p; ++i)
+        if (lane < p) sL[w][i][lane] = G[i * p + lane];
+    __syncwarp();
+    warp_chol_rinv(&sL[w][0][0], EIG_LD, sL[w], sD[w], sI[w], p, lane);
+    double* out = rinv + m * p * p;
+    for (int i = 0; i < p; ++i)
+        if (lane < p) out[i * p + lane] = sI[w][i][lane];
+}
+
+int launch_chol_rinv(const double* gram, int64_t batch, int p, double* rinv, cudaStream_t st) {
+    if (batch <= 0 || p <= 0) return QFCA_ERR_ARG;
+    if (p > EIG_MAXP) return QFCA_ERR_UNSUPPORTED;
+    k_chol_rinv<<<(unsigned)((batch + CR_WARPS - 1) / CR_WARPS), CR_WARPS * 32, 0, st>>>(
+        gram, batch, p, rinv);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- parallel Jacobi
+// One round applies the p/2 disjoint rotations J of a round-robin pairing at
+// once: A <- J^T A J acts on 2 x 2 blocks (pair I rows x pair J columns)
+// independently, so each thread updates whole blocks (one barrier per phase);
+// a rotated pair's own block gets the exact zero and the closed-form diagonal.
+constexpr int JAC_THREADS = 128;
+constexpr int JAC_SWEEPS = 30;
+
+__global__ void __launch_bounds__(JAC_THREADS)
+k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict__ evals,
+          double* __restrict__ evecs) {
+    __shared__ double A[EIG_MAXP][EIG_LD];
+    __shared__ double V[EIG_MAXP][EIG_LD];
+    __shared__ double sc[EIG_MAXP / 2][4];  // c, s, app', aqq'
+    __shared__ int sp[EIG_MAXP / 2][2];
+    __shared__ int8_t sched[EIG_MAXP - 1][EIG_MAXP];  // round -> player per position
+    __shared__ int srank[EIG_MAXP];
+    __shared__ int any_rot[2];  // per sweep parity: set by rotations, reset a sweep ahead
+    const int tid = threadIdx.x;
+    const int64_t m = blockIdx.x;
+    const int n = p + (p & 1);  // players incl. a dummy when p is odd
+    const int half = n / 2;
+    const double* H = h + m * p * p;
+    for (int i = tid; i < p * p; i += JAC_THREADS) {
+        const int r = i / p, c = i % p;
+        A[r][c] = 0.5 * (H[r * p + c] + H[c * p + r]);
+        V[r][c] = r == c ? 1.0 : 0.0;
+    }
+    if (tid == 0) any_rot[0] = 0;
+    // circle method: position 0 fixed, the others rotate by one per round
+    for (int i = tid; i < (n - 1) * n; i += JAC_THREADS) {
+        const int rnd = i / n, pos = i % n;
+        sched[rnd][pos] = (int8_t)(pos == 0 ? 0 : 1 + (pos - 1 + rnd) % (n - 1));
+    }
+    __syncthreads();
+    const int nblk = half * half;
+    for (int sweep = 0; sweep < JAC_SWEEPS; ++sweep) {
+        if (tid == 0) any_rot[(sweep + 1) & 1] = 0;
+        for (int rnd = 0; rnd < n - 1; ++rnd) {
+            if (tid < half) {
+                int a = sched[rnd][tid], b = sched[rnd][n - 1 - tid];
+                if (a > b) { const int t = a; a = b; b = t; }
+                double c = 1.0, s = 0.0, app = 0.0, aqq = 0.0;
+                if (b < p) {
+                    const double apq = A[a][b];
+                    app = A[a][a];
+                    aqq = A[b][b];
+                    // skip entries already negligible against their diagonal pair
+                    if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t =
+                            (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        app -= t * apq;  // exact-rotation diagonal
+                        aqq += t * apq;
+                        any_rot[sweep & 1] = 1;
+                    }
+                }
+                sc[tid][0] = c;
+                sc[tid][1] = s;
+                sc[tid][2] = app;
+                sc[tid][3] = aqq;
+                sp[tid][0] = a;
+                sp[tid][1] = b < p ? b : -1;
+            }
+            __syncthreads();
+            for (int k = tid; k < nblk; k += JAC_THREADS) {
+                const int I = k / half, J = k % half;
+                const double c1 = sc[I][0], s1 = sc[I][1], c2 = sc[J][0], s2 = sc[J][1];
+                if (s1 == 0.0 && s2 == 0.0) continue;
+                const int a = sp[I][0], b = sp[I][1], a2 = sp[J][0], b2 = sp[J][1];
+                if (I == J) {  // the rotated pair's own block
+                    A[a][a] = sc[I][2];
+                    A[b][b] = sc[I][3];
+                    A[a][b] = 0.0;
+                    A[b][a] = 0.0;
+                    continue;
+                }
+                // rows (pair I, b may be the dummy), then columns (pair J)
+                const double m00 = A[a][a2];
+                const double m01 = b2 >= 0 ? A[a][b2] : 0.0;
+                const double m10 = b >= 0 ? A[b][a2] : 0.0;
+                const double m11 = (b >= 0 && b2 >= 0) ? A[b][b2] : 0.0;
+                const double r00 = c1 * m00 - s1 * m10, r01 = c1 * m01 - s1 * m11;
+                const double r10 = s1 * m00 + c1 * m10, r11 = s1 * m01 + c1 * m11;
+                A[a][a2] = c2 * r00 - s2 * r01;
+                if (b2 >= 0) A[a][b2] = s2 * r00 + c2 * r01;
+                if (b >= 0) A[b][a2] = c2 * r10 - s2 * r11;
+                if (b >= 0 && b2 >= 0) A[b][b2] = s2 * r10 + c2 * r11;
+            }
+            for (int k = tid; k < half * p; k += JAC_THREADS) {  // V <- V J
+                const int I = k / p, r = k % p;
+                const double c = sc[I][0], s = sc[I][1];
+                const int a = sp[I][0], b = sp[I][1];
+                if (s == 0.0 || b < 0) continue;
+                const double u = V[r][a], v = V[r][b];
+                V[r][a] = c * u - s * v;
+                V[r][b] = s * u + c * v;
+            }
+            __syncthreads();
+        }
+        if (!any_rot[sweep & 1]) break;
+    }
+    // descending order (ties: lower index first)
+    if (tid < p) {
+        const double li = A[tid][tid];
+        int rk = 0;
+        for (int j = 0; j < p; ++j) {
+            const double lj = A[j][j];
+            rk += (lj > li) || (lj == li && j < tid);
+        }
+        srank[tid] = rk;
+        evals[m * p + rk] = li;
+    }
+    __syncthreads();
+    for (int i = tid; i < p * p; i += JAC_THREADS) {
+        const int r = i / p, c = i % p;  // V[r][c]: component r of vector c
+        evecs[m * p * p + r * p + srank[c]] = V[r][c];
+    }
+}
+
+int launch_sym_eig(const double* h, int64_t batch, int p, double* evals, double* evecs,
+                   cudaStream_t st) {
+    if (batch <= 0 || p <= 0) return QFCA_ERR_ARG;
+    if (p > EIG_MAXP) return QFCA_ERR_UNSUPPORTED;
+    k_sym_eig<<<(unsigned)batch, JAC_THREADS, 0, st>>>(h, batch, p, evals, evecs);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+}  // namespace qfca

@@ -147,8 +147,13 @@ k_cholqr(double* __restrict__ Y, int C, int p) {
     for (int i = tid; i < C * p; i += CQR_THREADS) blk[i] = sY[(i / p) * ps + i % p];
 }
 
+int launch_cqr_step(double* Y, int64_t batch, int C, int p, cudaStream_t st);
+
 int launch_cholqr(double* Y, int64_t batch, int C, int p, cudaStream_t st) {
     if (batch <= 0 || C <= 0 || p <= 0 || p > C) return QFCA_ERR_ARG;
+    // fused register-blocked step (eig.cu) for blocks up to 512 x 32
+    const int rc = launch_cqr_step(Y, batch, C, p, st);
+    if (rc != QFCA_ERR_UNSUPPORTED) return rc;
     const size_t smem = ((size_t)C * (p | 1) + (size_t)p * p) * sizeof(double);
     if (smem > 200 * 1024) return QFCA_ERR_UNSUPPORTED;
     if (cudaFuncSetAttribute(k_cholqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

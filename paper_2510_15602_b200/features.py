@@ -167,6 +167,14 @@ def covariance_exact(x: torch.Tensor, mean: torch.Tensor) -> torch.Tensor:
     return cov
 
 
+def _cholqr_inplace(y: torch.Tensor) -> torch.Tensor:
+    """Cholesky QR of a fresh contiguous (B, C, p) block, in place (csrc/eig.cu
+    k_cqr_step: Gram, Cholesky, R^-1 and Y R^-1 in one launch per batch)."""
+    b, c, p = y.shape
+    N.call("qfca_cholqr", y.data_ptr(), b, c, p, N.stream())
+    return y
+
+
 def _cholqr(y: torch.Tensor) -> torch.Tensor:
     """Orthonormal basis of the columns of y (B, C, p) by Cholesky QR.
 
@@ -184,38 +192,82 @@ def _cholqr(y: torch.Tensor) -> torch.Tensor:
     return torch.linalg.solve_triangular(lo.mT, y, upper=True, left=False)
 
 
+_X0: dict = {}
+
+
+def _start_block(c: int, p: int, device) -> torch.Tensor:
+    """Seeded orthonormal start block (c, p), cached per shape and device."""
+    key = (c, p, str(device))
+    if key not in _X0:
+        gen = torch.Generator(device="cpu").manual_seed(20251018)
+        x0 = torch.randn(c, p, generator=gen, dtype=torch.float64)
+        _X0[key] = torch.linalg.qr(x0)[0].contiguous().to(device)
+    return _X0[key]
+
+
+def chol_rinv(g: torch.Tensor) -> torch.Tensor:
+    """(B, p, p) Gram matrices -> R^-1 (Cholesky QR factor), p <= 32 (csrc/eig.cu)."""
+    b, p, _ = g.shape
+    out = empty((b, p, p), torch.float64)
+    N.call("qfca_chol_rinv", g.contiguous().data_ptr(), b, p, out.data_ptr(), N.stream())
+    return out
+
+
+def sym_eig(h: torch.Tensor):
+    """(B, p, p) symmetric -> (evals (B, p) descending, evecs (B, p, p) columns),
+    p <= 32, parallel Jacobi (csrc/eig.cu); no host synchronisation."""
+    b, p, _ = h.shape
+    w = empty((b, p), torch.float64)
+    v = empty((b, p, p), torch.float64)
+    N.call("qfca_sym_eig", h.contiguous().data_ptr(), b, p, w.data_ptr(), v.data_ptr(),
+           N.stream())
+    return w, v
+
+
 def topk_eigh(cov: torch.Tensor, k: int, block: int = 32, iters: int = 30):
     """Top-k eigenpairs of a batch of symmetric PSD matrices (B, C, C), fp64.
 
     Replaces the full ``np.linalg.eigh`` of features.py:173 (only the top-k
     pairs are used, features.py:174-176): block subspace iteration (block p =
-    max(block, k) columns, Cholesky-QR re-orthonormalisation, fp64 batched
-    GEMMs) followed by a Rayleigh-Ritz step.  The error of the k-th vector
-    decays as (lambda_{p+1} / lambda_k)^iters; on random-init WRN50-2
-    block-2 features (lambda_33 / lambda_10 ~ 0.2-0.33) 30 iterations reach the
-    fp64 eigh to ~1e-15.  C <= p degenerates to an exact Rayleigh-Ritz on the
-    whole space.  Returns (eigenvalues (B, k) descending, vectors (B, C, k)).
+    max(block, k) columns) on cov^2, re-orthonormalised by Cholesky QR (fp64
+    batched GEMMs for Y = S X and the Gram, csrc/eig.cu for R^-1), then a
+    Rayleigh-Ritz step on cov with a parallel-Jacobi eigensolver.  The error
+    of the k-th vector decays as (lambda_{p+1} / lambda_k)^iters; on
+    random-init WRN50-2 block-2 features (lambda_33 / lambda_10 ~ 0.2-0.33)
+    30 iterations reach the fp64 eigh to ~1e-15.  C <= p degenerates to an
+    exact eigen-decomposition of the whole matrix.  Returns (eigenvalues
+    (B, k) descending, vectors (B, C, k)).
     """
     b, c, _ = cov.shape
     p = min(c, max(block, k))
-    gen = torch.Generator(device="cpu").manual_seed(20251018)
-    x0 = torch.randn(c, p, generator=gen, dtype=torch.float64).to(cov.device)
+    if p > 32:
+        return _topk_eigh_torch(cov, k, p, iters)
     if p == c:
-        x = torch.eye(c, dtype=torch.float64, device=cov.device).expand(b, c, c)
-    else:
-        # iterate with cov^2 (one fp64 GEMM up front): same subspace, squared
-        # rate, half the iterations; the squaring costs ~eps (lambda_1 /
-        # lambda_k)^2 relative to lambda_k^2 (~1e-12 here), far below the
-        # fp32 covariance's own error
-        sq = cov @ cov
-        x = _cholqr(x0.expand(b, c, p).contiguous())
-        for _ in range((iters + 1) // 2):
-            x = _cholqr(sq @ x)
+        w, u = sym_eig(cov)
+        return w[..., :k], u[..., :k]
+    # iterate with cov^2 (one fp64 GEMM up front): same subspace, squared
+    # rate, half the iterations; the squaring costs ~eps (lambda_1 /
+    # lambda_k)^2 relative to lambda_k^2 (~1e-12 here)
+    sq = cov @ cov
+    x = _start_block(c, p, cov.device).expand(b, c, p)
+    for _ in range((iters + 1) // 2):
+        x = _cholqr_inplace(sq @ x)
+    hm = x.mT @ (cov @ x)
+    w, u = sym_eig(hm)
+    return w[..., :k], x @ u[..., :k]
+
+
+def _topk_eigh_torch(cov: torch.Tensor, k: int, p: int, iters: int):
+    """Blocks wider than 32 columns: the same iteration on torch / cuSOLVER."""
+    b, c, _ = cov.shape
+    sq = cov @ cov
+    x = _start_block(c, p, cov.device).expand(b, c, p)
+    for _ in range((iters + 1) // 2):
+        x = _cholqr(sq @ x)
     hm = x.mT @ (cov @ x)
     hm = 0.5 * (hm + hm.mT)
     w, u = torch.linalg.eigh(hm)  # ascending
-    vec = x @ u[..., -k:].flip(-1)
-    return w[..., -k:].flip(-1), vec
+    return w[..., -k:].flip(-1), x @ u[..., -k:].flip(-1)
 
 
 def pca_fit_batch(x: torch.Tensor, k: int):

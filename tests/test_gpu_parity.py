@@ -315,3 +315,28 @@ def test_covariance_exact_vs_fp64(Q, b, c, h, w):
     assert err <= 1e-9, err
     assert torch.equal(cov, cov.mT)  # mirrored tiles are bit-identical
     assert float(cov[:, 3].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("p", [32, 17, 5, 1])
+def test_sym_eig_and_chol_rinv(Q, p):
+    """csrc/eig.cu: parallel Jacobi eigenpairs and the Cholesky-QR factor
+    against torch / cuSOLVER fp64."""
+    from paper_2510_15602_b200 import features as F
+    g = torch.Generator().manual_seed(p)
+    a = torch.randn(6, 3 * p + 2, p, generator=g, dtype=torch.float64)
+    a[:, :, : max(1, p // 3)] *= 1e3  # spread eigenvalues
+    h = (a.mT @ a).cuda()
+    w, v = F.sym_eig(h)
+    wr = torch.linalg.eigvalsh(h).flip(-1)
+    assert torch.allclose(w, wr, rtol=1e-12, atol=1e-12 * float(wr.abs().max()))
+    # eigen-equation and orthonormality
+    res = (h @ v - v * w[:, None, :]).abs().max() / wr.abs().max()
+    assert float(res) < 1e-12
+    eye = torch.eye(p, dtype=torch.float64, device="cuda")
+    assert float((v.mT @ v - eye).abs().max()) < 1e-12
+    y = a.cuda()
+    x = y @ F.chol_rinv(y.mT @ y)
+    assert float((x.mT @ x - eye).abs().max()) < 1e-9
+    # x spans the columns of y
+    proj = x @ (x.mT @ y)
+    assert float((proj - y).abs().max() / y.abs().max()) < 1e-10

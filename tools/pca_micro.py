@@ -147,6 +147,40 @@ for k, cv in covs.items():
 cov = F.covariance_dev(xc)
 t, _ = timed(lambda: F.topk_eigh(cov, 10))
 res["topk_eigh_ms"] = t
+X32 = F._start_block(c, 32, cov.device).expand(b, c, 32)
+sqm = cov @ cov
+t, Y32 = timed(lambda: sqm @ X32)
+res["it_SX_ms"] = t
+t, G32 = timed(lambda: Y32.mT @ Y32)
+res["it_gram_ms"] = t
+t, R32 = timed(lambda: F.chol_rinv(G32))
+res["it_chol_rinv_ms"] = t
+t, _ = timed(lambda: Y32 @ R32)
+res["it_YR_ms"] = t
+t, _ = timed(lambda: F.sym_eig(G32))
+res["sym_eig_gram_ms"] = t
+xs = X32.contiguous()
+for _ in range(15):
+    xs = F._cholqr_inplace(sqm @ xs)
+hm_ = xs.mT @ (cov @ xs)
+t, _ = timed(lambda: F.sym_eig(hm_))
+res["sym_eig_rr_ms"] = t
+t, _ = timed(lambda: F._cholqr_inplace(sqm @ xs))
+res["iteration_fused_ms"] = t
+
+
+def one_iter():
+    y = sqm @ X32
+    return y @ F.chol_rinv(y.mT @ y)
+
+
+t, _ = timed(one_iter, n=20)
+res["iteration_ms"] = t
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    gout = F.topk_eigh(cov, 10)
+t, _ = timed(lambda: g.replay())
+res["topk_eigh_graph_ms"] = t
 Xs = F._cholqr(torch.randn(b, c, 32, dtype=torch.float64, device="cuda"))
 
 

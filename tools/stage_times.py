@@ -24,10 +24,8 @@ for rep in range(a.reps + 1):
         hw = h * w
         mean = torch.empty((b, c), dtype=torch.float64, device="cuda")
         N.call("qfca_plane_mean", x.data_ptr(), b * c, hw, mean.data_ptr(), N.stream())
-        xc = torch.empty((b, c, hw), dtype=torch.float32, device="cuda")
-        N.call("qfca_center", x.data_ptr(), b * c, hw, mean.data_ptr(), xc.data_ptr(), N.stream())
         e1 = ev()
-        cov = F.covariance_dev(xc)
+        cov = F.covariance_exact(x, mean)
         e2 = ev()
         evals, vecs = F.topk_eigh(cov, a.pca)
         e3 = ev()
@@ -45,7 +43,7 @@ for rep in range(a.reps + 1):
     up = Q.upsample_batch(out.scores, a.size, a.size)
     e6 = ev()
     torch.cuda.synchronize()
-    t = {"mean+center": e0.elapsed_time(e1), "cov": e1.elapsed_time(e2), "eigh": e2.elapsed_time(e3),
+    t = {"mean": e0.elapsed_time(e1), "cov": e1.elapsed_time(e2), "eigh": e2.elapsed_time(e3),
          "residual": e3.elapsed_time(e4), "quant+ref": e4.elapsed_time(s0), "score": s0.elapsed_time(s1),
          "finalize": s1.elapsed_time(e5), "upsample": e5.elapsed_time(e6), "total": e0.elapsed_time(e6)}
     if rep:
