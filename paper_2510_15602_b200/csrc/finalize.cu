@@ -81,33 +81,65 @@ __global__ void k_image_score(const double* __restrict__ scores, int h, int w, i
 }
 
 // bilinear resize with half-pixel centres (tensor_io.py:127-151), fp64 math,
-// float32 result.  Source is fp64 (the score map).
-__global__ void k_upsample(const double* __restrict__ in, int64_t images, int h, int w, int oh,
-                           int ow, float* __restrict__ out) {
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t ohw = (int64_t)oh * ow;
-    if (gid >= images * ohw) return;
-    const int64_t b = gid / ohw, px = gid % ohw;
-    const int oy = (int)(px / ow), ox = (int)(px % ow);
-    const double* p = in + b * (int64_t)h * w;
-    if (h == oh && w == ow) {
-        out[gid] = (float)p[(int64_t)oy * w + ox];
-        return;
+// float32 result.  Source is fp64 (the score map).  One CTA per (image, band
+// of UP_ROWS output rows): the column weights are computed once per CTA into
+// shared memory, the row weights once per row, so each output costs four
+// loads and the six rounded products / three sums of the reference formula.
+constexpr int UP_THREADS = 256;
+constexpr int UP_ROWS = 8;
+constexpr int UP_CHUNK = 2048;  // output columns per CTA (shared weight table)
+
+__device__ __forceinline__ void up_coord(int o, int n, int on, int& i0, int& i1, double& f) {
+    const double s = ((double)o + 0.5) * (double)n / (double)on - 0.5;
+    const double ff = floor(s);
+    i0 = (int)fmin(fmax(ff, 0.0), (double)(n - 1));
+    i1 = min(i0 + 1, n - 1);
+    f = fmin(fmax(s - (double)i0, 0.0), 1.0);
+}
+
+__global__ void __launch_bounds__(UP_THREADS)
+k_upsample(const double* __restrict__ in, int h, int w, int oh, int ow, int bands, int chunks,
+           float* __restrict__ out) {
+    __shared__ int sx0[UP_CHUNK], sx1[UP_CHUNK];
+    __shared__ double sfx[UP_CHUNK];
+    const int b = blockIdx.x / (bands * chunks);
+    const int band = (blockIdx.x / chunks) % bands, cx0 = (blockIdx.x % chunks) * UP_CHUNK;
+    const int cw = min(UP_CHUNK, ow - cx0);
+    const double* p = in + (int64_t)b * h * w;
+    float* o = out + (int64_t)b * oh * ow + cx0;
+    for (int i = threadIdx.x; i < cw; i += UP_THREADS) {
+        int x0, x1;
+        double fx;
+        up_coord(cx0 + i, w, ow, x0, x1, fx);
+        sx0[i] = x0;
+        sx1[i] = x1;
+        sfx[i] = fx;
     }
-    const double ys = ((double)oy + 0.5) * (double)h / (double)oh - 0.5;
-    const double xs = ((double)ox + 0.5) * (double)w / (double)ow - 0.5;
-    const double fyf = floor(ys), fxf = floor(xs);
-    const int y0 = (int)fmin(fmax(fyf, 0.0), (double)(h - 1));
-    const int x0 = (int)fmin(fmax(fxf, 0.0), (double)(w - 1));
-    const int y1 = min(y0 + 1, h - 1), x1 = min(x0 + 1, w - 1);
-    const double fy = fmin(fmax(ys - (double)y0, 0.0), 1.0);
-    const double fx = fmin(fmax(xs - (double)x0, 0.0), 1.0);
-    // explicit rounding (no FMA contraction) to match NumPy bit for bit
-    const double top = __dadd_rn(__dmul_rn(p[(int64_t)y0 * w + x0], 1.0 - fx),
-                                 __dmul_rn(p[(int64_t)y0 * w + x1], fx));
-    const double bot = __dadd_rn(__dmul_rn(p[(int64_t)y1 * w + x0], 1.0 - fx),
-                                 __dmul_rn(p[(int64_t)y1 * w + x1], fx));
-    out[gid] = (float)__dadd_rn(__dmul_rn(top, 1.0 - fy), __dmul_rn(bot, fy));
+    __syncthreads();
+    const int oy1 = min(oh, (band + 1) * UP_ROWS);
+    for (int oy = band * UP_ROWS; oy < oy1; ++oy) {
+        int y0, y1;
+        double fy;
+        up_coord(oy, h, oh, y0, y1, fy);
+        const double* r0 = p + (int64_t)y0 * w;
+        const double* r1 = p + (int64_t)y1 * w;
+        for (int ox = threadIdx.x; ox < cw; ox += UP_THREADS) {
+            const int x0 = sx0[ox], x1 = sx1[ox];
+            const double fx = sfx[ox];
+            // explicit rounding (no FMA contraction) to match NumPy bit for bit
+            const double top = __dadd_rn(__dmul_rn(__ldg(r0 + x0), 1.0 - fx),
+                                         __dmul_rn(__ldg(r0 + x1), fx));
+            const double bot = __dadd_rn(__dmul_rn(__ldg(r1 + x0), 1.0 - fx),
+                                         __dmul_rn(__ldg(r1 + x1), fx));
+            o[(int64_t)oy * ow + ox] = (float)__dadd_rn(__dmul_rn(top, 1.0 - fy),
+                                                        __dmul_rn(bot, fy));
+        }
+    }
+}
+
+__global__ void k_copy_f64_f32(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (float)in[i];
 }
 
 static inline unsigned nblk(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -149,8 +181,15 @@ int launch_image_score(const double* scores, int64_t images, int h, int w, int b
 int launch_upsample(const double* in, int64_t images, int h, int w, int oh, int ow, float* out,
                     cudaStream_t st) {
     if (images <= 0 || h <= 0 || w <= 0 || oh <= 0 || ow <= 0) return QFCA_ERR_ARG;
-    k_upsample<<<nblk(images * (int64_t)oh * ow, 256), 256, 0, st>>>(in, images, h, w, oh, ow,
-                                                                      out);
+    if (h == oh && w == ow) {
+        k_copy_f64_f32<<<nblk(images * (int64_t)oh * ow, 256), 256, 0, st>>>(
+            in, images * (int64_t)oh * ow, out);
+    } else {
+        const int bands = (oh + UP_ROWS - 1) / UP_ROWS;
+        const int chunks = (ow + UP_CHUNK - 1) / UP_CHUNK;
+        k_upsample<<<(unsigned)(images * bands * chunks), UP_THREADS, 0, st>>>(
+            in, h, w, oh, ow, bands, chunks, out);
+    }
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 

@@ -186,10 +186,17 @@ static int launch_res_k(const float* x, int64_t images, int C, int64_t hw, const
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
+int launch_pca_residual_tiled(const float*, int64_t, int, int64_t, const double*, const double*,
+                              int, int, float*, cudaStream_t);
+
 int launch_pca_residual(const float* x, int64_t images, int C, int64_t hw, const double* mean,
                         const double* comps, int k, int per_image_model, float* out,
                         cudaStream_t st) {
     if (images <= 0 || C <= 0 || hw <= 0 || k < 1 || k > PCA_MAXK) return QFCA_ERR_ARG;
+    // persistent tiled kernel (residual.cu): x read once, loads double-buffered
+    const int rc = launch_pca_residual_tiled(x, images, C, hw, mean, comps, k, per_image_model,
+                                             out, st);
+    if (rc != QFCA_ERR_UNSUPPORTED) return rc;
     switch (k) {
 #define QFCA_RES_K(KK) \
     case KK: return launch_res_k<KK>(x, images, C, hw, mean, comps, per_image_model, out, st);

@@ -22,8 +22,10 @@
 //           own-bin horizontal box + partial-map update.
 //
 // Pass 1 reads SA4 instead of recomputing the windows, the sample scatter of
-// score3.cu disappears, and the transport needs no per-bin branch.  Results
-// are bit-identical to score3.cu (same fp32 expressions in the same order).
+// score3.cu disappears, and the transport needs no per-bin branch.  The fp32
+// transport expressions are score3.cu's; with one channel slot per CTA the
+// per-slot sums are added to the partial map one at a time, so the maps agree
+// with score3.cu to fp32 rounding.
 // With a host-supplied reference (Vref) the search is skipped and any sample
 // stride is accepted.
 #include <string.h>
@@ -32,12 +34,15 @@
 
 namespace qfca {
 
-// 16 warps; in pass 0 warps 12-15 are the producers (H1), warps 0-11 the
-// consumers (H2); the search, the tables and pass 1 use all of them
-constexpr int S4_THREADS = 512;
-constexpr int S4_PT = 128;                 // pass-0 producer threads
-constexpr int S4_CT = S4_THREADS - S4_PT;  // pass-0 consumer threads
+// A CTA covers NCOL = CPB * W columns (CPB channel slots of width W) with
+// 4 * NCOL threads -- one per (slot, bin group, column) in pass 1.  In pass 0
+// the last NCOL threads are the producers (H1, one per column) and the rest
+// the consumers (H2); the search, the tables and pass 1 use all of them.
+// NCOL = 64 (256 threads, <= 113 KB) keeps two CTAs resident per SM, so one
+// CTA's barrier-bound phases overlap the other's transport; NCOL = 128 (512
+// threads) takes wider planes.
 constexpr int S4_SMEM_MAX = 227 * 1024;
+constexpr int S4_SMEM_2CTA = 113 * 1024;
 // named barriers of the pass-0 pipeline (0 is __syncthreads)
 constexpr int S4_FULL0 = 3, S4_EMPTY0 = 5;
 
@@ -75,9 +80,9 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
 }
 
 // H2 segment: smallest odd length >= 3 whose tasks fit the consumer threads
-__host__ __device__ constexpr int s4_seg(int t, int w) {
+__host__ __device__ constexpr int s4_seg(int t, int w, int ncol) {
     int s = 3;
-    while (t * (128 / w) * ((w + s - 1) / s) > S4_CT) s += 2;
+    while (t * (ncol / w) * ((w + s - 1) / s) > 3 * ncol) s += 2;
     return s;
 }
 __host__ __device__ constexpr int s4_rounds(int t2) {
@@ -86,11 +91,11 @@ __host__ __device__ constexpr int s4_rounds(int t2) {
     return r;
 }
 
-template <int T, int W>
+template <int T, int W, int NCOL>
 static void score4_layout(Score4Geom& g) {
-    constexpr int CPB = 128 / W;
+    constexpr int CPB = NCOL / W;
     constexpr int T2 = T * T;
-    constexpr int SEG = s4_seg(T, W);
+    constexpr int SEG = s4_seg(T, W, NCOL);
     constexpr int NSEG = (W + SEG - 1) / SEG;
     const int R = T / 2;
     // row pitch with consecutive H2 tasks on consecutive 16-byte bank groups
@@ -137,16 +142,18 @@ static void score4_layout(Score4Geom& g) {
     g.total = off;
 }
 
-template <int T, int W>
-__global__ void __launch_bounds__(S4_THREADS, 1)
+template <int T, int W, int NCOL>
+__global__ void __launch_bounds__(4 * NCOL, NCOL == 64 ? 2 : 1)
 k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
          const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score4Geom g,
          float* __restrict__ partial) {
+    constexpr int S4_THREADS = 4 * NCOL;
+    constexpr int S4_CT = S4_THREADS - NCOL;  // pass-0 consumers; the last NCOL threads produce
     constexpr int R = T / 2;
     constexpr int T2 = T * T;
-    constexpr int GP = T2 + 1;    // G-table length per bin
-    constexpr int CPB = 128 / W;  // channel slots: CPB * W = 128 columns per CTA pass
-    constexpr int SEG = s4_seg(T, W);
+    constexpr int GP = T2 + 1;     // G-table length per bin
+    constexpr int CPB = NCOL / W;  // channel slots: CPB * W = NCOL columns per CTA pass
+    constexpr int SEG = s4_seg(T, W, NCOL);
     constexpr int NSEG = (W + SEG - 1) / SEG;
     constexpr int TPS = S4_THREADS / CPB;  // search threads per slot (whole warps)
     constexpr int ROUNDS = s4_rounds(T2);
@@ -211,6 +218,7 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int cs = tid / (4 * W);
     const int grp = (tid / W) & 3;
     const int grp4 = grp * 4;
+    const bool g1 = (grp & 1) != 0, g2 = (grp & 2) != 0;
     const int x = tid % W;
 
     // H1 (producers): vertical windows of pass-0 chunk c -> CHp[c & 1]
@@ -458,19 +466,51 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         const uint32_t gaddr =
             (uint32_t)__cvta_generic_to_shared(GT + (cs * 16 + grp4) * GP) + g.moff;
         const uint4* const sacol = SA4 + cs * hw + x;
+        // box-phase task -> (row in chunk, column): interior columns first, the 2R
+        // border columns (padded taps) last, so only the last warps take the xmap path
+        constexpr int NI = W - 2 * R;
+        constexpr int MAXA = (T * W + S4_THREADS - 1) / S4_THREADS;  // box tasks per thread
+        auto a_task = [&](int task, int& rho, int& ax) {
+            if (task < T * NI) {
+                rho = task / NI;
+                ax = R + task - rho * NI;
+            } else {
+                const int b = task - T * NI;
+                constexpr int NB = 2 * R > 0 ? 2 * R : 1;  // (T = 1: no border)
+                rho = b / NB;
+                const int j = b - rho * NB;
+                ax = j < R ? j : W - 2 * R + j;
+            }
+        };
         for (int c = 0; c < n_chunks; ++c) {
             const int s0 = c * T;
+            // partial-map values of this chunk's box tasks, fetched before the
+            // transport so their latency hides behind it
+            float pold[MAXA];
+#pragma unroll
+            for (int q = 0; q < MAXA; ++q) {
+                const int task = tid + q * S4_THREADS;
+                pold[q] = 0.f;
+                if (task < T * W) {
+                    int rho, ax;
+                    a_task(task, rho, ax);
+                    const int y = s0 + rho - 2 * R;
+                    if (y >= 0 && y < h) pold[q] = part[y * W + ax];
+                }
+            }
             {
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
                     const uint4 v = sacol[rmap[s0 + rho] * W];
-                    const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
-                    const uint32_t prev = grp == 1 ? v.x : grp == 2 ? v.y : grp == 3 ? v.z : 0u;
+                    // (word, prev) = words grp, grp - 1 (0 for grp 0): branch-free selects
+                    const uint32_t wlo = g1 ? v.y : v.x, whi = g1 ? v.w : v.z;
+                    const uint32_t plo = g1 ? v.x : 0u, phi = g1 ? v.z : v.y;
+                    const uint32_t word = g2 ? whi : wlo, prev = g2 ? phi : plo;
                     const bool mass = (word >> 24) != (prev >> 24);
+                    float E[4] = {0.f, 0.f, 0.f, 0.f};  // warp without mass in the group: E = 0
                     if (__any_sync(0xffffffffu, mass)) {
                         uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
                         uint32_t aa = gaddr + 4u * ma;
-                        float E[4];
 #define S4_E(J)                                                                 \
     {                                                                           \
         const uint32_t mb = __byte_perm(word, 0x4B000000u, 0x7650 + J);         \
@@ -484,17 +524,11 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     }
                         S4_E(0) S4_E(1) S4_E(2) S4_E(3)
 #undef S4_E
+                    }
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            vs[j] += E[j] - ring[rho][j];
-                            ring[rho][j] = E[j];
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            vs[j] -= ring[rho][j];
-                            ring[rho][j] = 0.f;
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        vs[j] += E[j] - ring[rho][j];
+                        ring[rho][j] = E[j];
                     }
                     if (rho == T - 1) {
 #pragma unroll
@@ -513,21 +547,12 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
             }
             __syncthreads();  // Vb complete
-            // interior columns first, the 2R border columns (padded taps) last,
-            // so that only the last warps take the xmap path
-            constexpr int NI = W - 2 * R;
-            for (int task = tid; task < T * W; task += S4_THREADS) {
+#pragma unroll
+            for (int q = 0; q < MAXA; ++q) {
+                const int task = tid + q * S4_THREADS;
+                if (task >= T * W) continue;
                 int rho, ax;
-                if (task < T * NI) {
-                    rho = task / NI;
-                    ax = R + task - rho * NI;
-                } else {
-                    const int b = task - T * NI;
-                    constexpr int NB = 2 * R > 0 ? 2 * R : 1;  // (T = 1: no border)
-                    rho = b / NB;
-                    const int j = b - rho * NB;
-                    ax = j < R ? j : W - 2 * R + j;
-                }
+                a_task(task, rho, ax);
                 const int y = s0 + rho - 2 * R;
                 if (y < 0 || y >= h) continue;
                 float acc = 0.f;
@@ -547,7 +572,7 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     }
                     acc = fmaf(f, scale, acc);
                 }
-                part[y * W + ax] += acc;
+                part[y * W + ax] = pold[q] + acc;
             }
             __syncthreads();  // Vb free
         }
@@ -556,14 +581,15 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 
 int sample_stride(int h, int w, int budget);
 
-template <int T, int W>
+template <int T, int W, int NCOL>
 static int s4_total(Score4Geom& g) {
-    score4_layout<T, W>(g);
+    score4_layout<T, W, NCOL>(g);
     return g.total;
 }
 
 static int score4_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
-                       int pad, int budget, bool has_ref, Score4Geom* out, size_t* smem_out) {
+                       int pad, int budget, bool has_ref, Score4Geom* out, size_t* smem_out,
+                       int* ncol_out) {
     if (t < 1 || t > 11 || (t & 1) == 0 || n_bins < 1 || n_bins > 16) return QFCA_ERR_UNSUPPORTED;
     if (w != 32 && w != 64 && w != 128) return QFCA_ERR_UNSUPPORTED;
     if (h < 1 || (int64_t)h * w > (1 << 20) || ((int64_t)h * w) % 16) return QFCA_ERR_UNSUPPORTED;
@@ -575,34 +601,50 @@ static int score4_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.n0 = (h + t - 1) / t;
     g.nsamp = h * w;
     g.moff = 0u - 4u * 0x4B000000u;
-    if (!has_ref) {
-        // in-kernel reference: every pixel must be a sample (stride 1), counts
-        // must fit the packed compare (T^2 <= 126) and the 8/16-bit counters
-        if (t * t > 126 || budget < 1 || !(pad == QFCA_PAD_WRAP || h > 1)) return QFCA_ERR_UNSUPPORTED;
-        if (sample_stride(h, w, budget) != 1) return QFCA_ERR_UNSUPPORTED;
-        const int tps = S4_THREADS / (128 / w);
-        if (g.nsamp >= 65536 || (g.nsamp + tps - 1) / tps > 255) return QFCA_ERR_UNSUPPORTED;
-        g.fref = 1;
-    }
+    // NCOL = 64 (two CTAs per SM) when the plane is narrow enough and fits, else 128
+    int ncol = 0;
     size_t bytes = 0;
-    switch (t * 1000 + w) {
-#define S4C(TT, WW) case TT * 1000 + WW: bytes = s4_total<TT, WW>(g); break;
-        S4C(1, 32) S4C(1, 64) S4C(1, 128) S4C(3, 32) S4C(3, 64) S4C(3, 128)
-        S4C(5, 32) S4C(5, 64) S4C(5, 128) S4C(7, 32) S4C(7, 64) S4C(7, 128)
-        S4C(9, 32) S4C(9, 64) S4C(9, 128) S4C(11, 32) S4C(11, 64) S4C(11, 128)
+    for (int pass = 0; pass < 2 && !ncol; ++pass) {
+        const int nc = pass == 0 ? 64 : 128;
+        if (nc < w) continue;
+        if (!has_ref) {
+            // in-kernel reference: every pixel must be a sample (stride 1), counts
+            // must fit the packed compare (T^2 <= 126) and the 8/16-bit counters
+            if (t * t > 126 || budget < 1 || !(pad == QFCA_PAD_WRAP || h > 1)) return QFCA_ERR_UNSUPPORTED;
+            if (sample_stride(h, w, budget) != 1) return QFCA_ERR_UNSUPPORTED;
+            const int tps = 4 * nc / (nc / w);
+            if (g.nsamp >= 65536 || (g.nsamp + tps - 1) / tps > 255) continue;
+            g.fref = 1;
+        }
+        Score4Geom gg = g;
+        switch (t * 100000 + w * 1000 + nc) {
+#define S4C(TT, WW, NC) case TT * 100000 + WW * 1000 + NC: bytes = s4_total<TT, WW, NC>(gg); break;
+            S4C(1, 32, 64) S4C(1, 64, 64) S4C(3, 32, 64) S4C(3, 64, 64) S4C(5, 32, 64)
+            S4C(5, 64, 64) S4C(7, 32, 64) S4C(7, 64, 64) S4C(9, 32, 64) S4C(9, 64, 64)
+            S4C(11, 32, 64) S4C(11, 64, 64)
+            S4C(1, 32, 128) S4C(1, 64, 128) S4C(1, 128, 128) S4C(3, 32, 128) S4C(3, 64, 128)
+            S4C(3, 128, 128) S4C(5, 32, 128) S4C(5, 64, 128) S4C(5, 128, 128) S4C(7, 32, 128)
+            S4C(7, 64, 128) S4C(7, 128, 128) S4C(9, 32, 128) S4C(9, 64, 128) S4C(9, 128, 128)
+            S4C(11, 32, 128) S4C(11, 64, 128) S4C(11, 128, 128)
 #undef S4C
-        default: return QFCA_ERR_UNSUPPORTED;
+            default: return QFCA_ERR_UNSUPPORTED;
+        }
+        if (bytes <= (size_t)(nc == 64 ? S4_SMEM_2CTA : S4_SMEM_MAX)) {
+            ncol = nc;
+            g = gg;
+        }
     }
-    if (bytes > (size_t)S4_SMEM_MAX) return QFCA_ERR_UNSUPPORTED;
-    const int cpb = 128 / w;
+    if (!ncol) return QFCA_ERR_UNSUPPORTED;
+    const int cpb = ncol / w;
     int groups = groups_hint;
-    if (groups <= 0) groups = balanced_groups(images, C, cpb, 1);
+    if (groups <= 0) groups = balanced_groups(images, C, cpb, ncol == 64 ? 2 : 1);
     groups = groups < 1 ? 1 : (groups > C ? C : groups);
     // whole batches per group
     g.cpg = ((C + groups - 1) / groups + cpb - 1) / cpb * cpb;
     g.groups = (C + g.cpg - 1) / g.cpg;
     *out = g;
     *smem_out = bytes;
+    *ncol_out = ncol;
     return QFCA_OK;
 }
 
@@ -610,8 +652,9 @@ int score4_query(int h, int w, int n_bins, int t, int C, int64_t images, int gro
                  int pad, int budget, int want_fref, int* fref) {
     Score4Geom g;
     size_t smem;
+    int ncol;
     if (score4_plan(h, w, n_bins, t, C, images, groups_hint, pad, budget, want_fref == 0, &g,
-                    &smem) != QFCA_OK)
+                    &smem, &ncol) != QFCA_OK)
         return -1;
     if (fref) *fref = g.fref;
     return g.groups;
@@ -623,25 +666,32 @@ int launch_score4(const void* bins, int bins_bytes, const float* lo, const float
     if (bins_bytes != 1) return QFCA_ERR_UNSUPPORTED;
     Score4Geom g;
     size_t smem;
+    int ncol;
     int rc = score4_plan(h, w, n_bins, t, C, images, groups, pad, budget, V != nullptr, &g,
-                         &smem);
+                         &smem, &ncol);
     if (rc != QFCA_OK) return rc;
     if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
     void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score4Geom,
                  float*) = nullptr;
-    switch (t * 1000 + w) {
-#define S4K(TT, WW) case TT * 1000 + WW: kern = k_score4<TT, WW>; break;
-        S4K(1, 32) S4K(1, 64) S4K(1, 128) S4K(3, 32) S4K(3, 64) S4K(3, 128)
-        S4K(5, 32) S4K(5, 64) S4K(5, 128) S4K(7, 32) S4K(7, 64) S4K(7, 128)
-        S4K(9, 32) S4K(9, 64) S4K(9, 128) S4K(11, 32) S4K(11, 64) S4K(11, 128)
+    switch (t * 100000 + w * 1000 + ncol) {
+#define S4K(TT, WW, NC) case TT * 100000 + WW * 1000 + NC: kern = k_score4<TT, WW, NC>; break;
+        S4K(1, 32, 64) S4K(1, 64, 64) S4K(3, 32, 64) S4K(3, 64, 64) S4K(5, 32, 64)
+        S4K(5, 64, 64) S4K(7, 32, 64) S4K(7, 64, 64) S4K(9, 32, 64) S4K(9, 64, 64)
+        S4K(11, 32, 64) S4K(11, 64, 64)
+        S4K(1, 32, 128) S4K(1, 64, 128) S4K(1, 128, 128) S4K(3, 32, 128) S4K(3, 64, 128)
+        S4K(3, 128, 128) S4K(5, 32, 128) S4K(5, 64, 128) S4K(5, 128, 128) S4K(7, 32, 128)
+        S4K(7, 64, 128) S4K(7, 128, 128) S4K(9, 32, 128) S4K(9, 64, 128) S4K(9, 128, 128)
+        S4K(11, 32, 128) S4K(11, 64, 128) S4K(11, 128, 128)
 #undef S4K
         default: return QFCA_ERR_UNSUPPORTED;
     }
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
+            cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) !=
+            cudaSuccess)
         return QFCA_ERR_CUDA;
     const int64_t grid = images * g.groups;
-    kern<<<(unsigned)grid, S4_THREADS, smem, st>>>((const uint8_t*)bins, lo, hi, V, g, partial);
+    kern<<<(unsigned)grid, 4 * ncol, smem, st>>>((const uint8_t*)bins, lo, hi, V, g, partial);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 

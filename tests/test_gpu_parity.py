@@ -278,9 +278,10 @@ def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
 @pytest.mark.parametrize("shape,n,t,pad", [((2, 37, 64, 64), 16, 9, "reflect"),
                                            ((2, 21, 32, 32), 16, 5, "wrap"),
                                            ((1, 10, 32, 128), 12, 11, "reflect")])
-def test_score4_bit_identical_to_score3(Q, shape, n, t, pad):
-    """score4.cu restates score3.cu's fp32 expressions in the same order: the
-    maps agree bit for bit (both select the reference in-kernel)."""
+def test_score4_matches_score3(Q, shape, n, t, pad):
+    """score4.cu restates score3.cu's fp32 transport expressions; only the
+    grouping of the per-slot channel sums differs (two-CTA layout), so the
+    maps agree to fp32 rounding (both select the reference in-kernel)."""
     from paper_2510_15602_b200 import _native
     rng = np.random.default_rng(7 + t)
     x = torch.from_numpy(np.maximum(rng.standard_normal(shape) + 0.3, 0).astype(np.float32)).cuda()
@@ -292,7 +293,8 @@ def test_score4_bit_identical_to_score3(Q, shape, n, t, pad):
             out[ver] = Q.detect_batch(x, cfg).scores.cpu().numpy()
     finally:
         _native.call("qfca_set_score_kernel", 0)
-    assert np.array_equal(out[3], out[4])
+    err = np.abs(out[3] - out[4]).max() / np.abs(out[3]).max()
+    assert err <= 2e-6, err
 
 
 @pytest.mark.parametrize("b,c,h,w", [(2, 512, 64, 64), (3, 37, 20, 24), (1, 130, 48, 40),
