@@ -252,30 +252,27 @@ def main():
     # ---- end to end through the C-ABI call with host buffers ("e2e")
     e2e = None
     if not args.no_e2e:
+        # public streaming API (pipeline.DetectPipeline): every step copies its
+        # batch from pinned host memory, scores it, upsamples the maps to image
+        # resolution and copies maps + image scores back; the copies of one
+        # batch overlap the scoring of its neighbour
         x_host = feats.cpu().pin_memory()
-        x_dev = torch.empty_like(feats)
-        scores_host = torch.empty((b, h, w), dtype=torch.float64).pin_memory()
-        img_host = torch.empty((b,), dtype=torch.float64).pin_memory()
+        pipe = Q.DetectPipeline(cfg, upsample_to=(size, size))
         h2d = x_host.numel() * 4
-        d2h = scores_host.numel() * 8 + img_host.numel() * 8
-
-        def e2e_step():
-            x_dev.copy_(x_host, non_blocking=True)
-            r, u = step(x_dev)
-            scores_host.copy_(r.scores, non_blocking=True)
-            img_host.copy_(r.image_scores, non_blocking=True)
-
-        for _ in range(2):
-            e2e_step()
+        d2h = b * h * w * 8 + b * 8 + b * size * size * 4
+        for _ in pipe.run([x_host] * 2):
+            pass
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.steps):
-            e2e_step()
+        n_done = 0
+        for r in pipe.run([x_host] * args.steps):
+            n_done += int(r.image_scores.numel() > 0)
         e1.record()
         torch.cuda.synchronize()
+        assert n_done == args.steps
         e_ms = e0.elapsed_time(e1)
         if ws > 1:
             t = torch.tensor([e_ms], device=dev)

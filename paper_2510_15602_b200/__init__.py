@@ -24,6 +24,7 @@ from .scoring import (AnomalyMap, DetectResult, PipelineConfig, aggregate_channe
                       upsample_batch, upsample_scores)
 from .transport import (IllConditionedError, MassError, mismatch_batch,
                         quantized_mismatch)
+from .pipeline import DetectPipeline, HostResult
 
 __all__ = [
     "FeatureMap", "FormatError", "PcaModel", "gaussian_blur", "pca_fit", "pca_residual",
@@ -33,5 +34,5 @@ __all__ = [
     "associate_errors", "bin_error_maps", "channel_error_maps", "detect", "detect_batch",
     "fused_supported", "image_score_of", "smooth_scores", "upsample_batch",
     "upsample_scores", "IllConditionedError", "MassError", "mismatch_batch",
-    "quantized_mismatch",
+    "quantized_mismatch", "DetectPipeline", "HostResult",
 ]

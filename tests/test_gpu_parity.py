@@ -342,3 +342,24 @@ def test_sym_eig_and_chol_rinv(Q, p):
     # x spans the columns of y
     proj = x @ (x.mT @ y)
     assert float((proj - y).abs().max() / y.abs().max()) < 1e-10
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_detect_pipeline_matches_detect_batch(Q, pinned):
+    """pipeline.DetectPipeline (copy / score / copy-back overlapped on three
+    streams) returns exactly what detect_batch computes for each batch."""
+    rng = np.random.default_rng(11)
+    batches = [torch.from_numpy(np.maximum(rng.standard_normal((2, 24, 32, 32)) + 0.1 * i, 0)
+                                .astype(np.float32)) for i in range(5)]
+    if pinned:
+        batches = [b.pin_memory() for b in batches]
+    cfg = Q.PipelineConfig(pca_components=4)
+    pipe = Q.DetectPipeline(cfg, upsample_to=(64, 64))
+    got = [(r.index, r.scores.clone(), r.image_scores.clone(), r.upsampled.clone())
+           for r in pipe.run(batches)]
+    assert [g[0] for g in got] == list(range(5))
+    for (i, s, im, up), b in zip(got, batches):
+        ref = Q.detect_batch(b.cuda(), cfg)
+        assert torch.equal(s, ref.scores.cpu())
+        assert torch.equal(im, ref.image_scores.cpu())
+        assert torch.equal(up, Q.upsample_batch(ref.scores, 64, 64).cpu())
