@@ -199,7 +199,7 @@ int launch_chol_rinv(const double* gram, int64_t batch, int p, double* rinv, cud
 // once: A <- J^T A J acts on 2 x 2 blocks (pair I rows x pair J columns)
 // independently, so each thread updates whole blocks (one barrier per phase);
 // a rotated pair's own block gets the exact zero and the closed-form diagonal.
-constexpr int JAC_THREADS = 128;
+constexpr int JAC_THREADS = 256;  // one 2 x 2 block and two V row-pairs per thread
 constexpr int JAC_SWEEPS = 30;
 
 __global__ void __launch_bounds__(JAC_THREADS)
@@ -229,7 +229,6 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
         sched[rnd][pos] = (int8_t)(pos == 0 ? 0 : 1 + (pos - 1 + rnd) % (n - 1));
     }
     __syncthreads();
-    const int nblk = half * half;
     for (int sweep = 0; sweep < JAC_SWEEPS; ++sweep) {
         if (tid == 0) any_rot[(sweep + 1) & 1] = 0;
         for (int rnd = 0; rnd < n - 1; ++rnd) {
@@ -243,13 +242,18 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
                     aqq = A[b][b];
                     // skip entries already negligible against their diagonal pair
                     if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        const double t =
-                            (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        app -= t * apq;  // exact-rotation diagonal
-                        aqq += t * apq;
+                        // t = tan(theta) = sgn(d) 2 apq / u with d = aqq - app,
+                        // u = |d| + sqrt(d^2 + 4 apq^2); c = u / sqrt(u^2 + 4 apq^2),
+                        // s = t c: one sqrt, then rsqrt and 1/u side by side
+                        const double d = aqq - app, q2 = 4.0 * apq * apq;
+                        const double u = fabs(d) + sqrt(fma(d, d, q2));
+                        const double w = rsqrt(fma(u, u, q2));
+                        const double sg = d >= 0.0 ? 2.0 * apq : -2.0 * apq;
+                        const double tq = sg * apq / u;  // t * apq
+                        c = u * w;
+                        s = sg * w;
+                        app -= tq;  // exact-rotation diagonal
+                        aqq += tq;
                         any_rot[sweep & 1] = 1;
                     }
                 }
@@ -261,8 +265,9 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
                 sp[tid][1] = b < p ? b : -1;
             }
             __syncthreads();
-            for (int k = tid; k < nblk; k += JAC_THREADS) {
-                const int I = k / half, J = k % half;
+            for (int k = tid; k < EIG_MAXP * EIG_MAXP / 4; k += JAC_THREADS) {
+                const int I = k >> 4, J = k & 15;  // 16 x 16 pair grid, shifts only
+                if (I >= half || J >= half) continue;
                 const double c1 = sc[I][0], s1 = sc[I][1], c2 = sc[J][0], s2 = sc[J][1];
                 if (s1 == 0.0 && s2 == 0.0) continue;
                 const int a = sp[I][0], b = sp[I][1], a2 = sp[J][0], b2 = sp[J][1];
@@ -285,8 +290,9 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
                 if (b >= 0) A[b][a2] = c2 * r10 - s2 * r11;
                 if (b >= 0 && b2 >= 0) A[b][b2] = s2 * r10 + c2 * r11;
             }
-            for (int k = tid; k < half * p; k += JAC_THREADS) {  // V <- V J
-                const int I = k / p, r = k % p;
+            for (int k = tid; k < (EIG_MAXP / 2) * EIG_MAXP; k += JAC_THREADS) {  // V <- V J
+                const int I = k >> 5, r = k & 31;
+                if (I >= half || r >= p) continue;
                 const double c = sc[I][0], s = sc[I][1];
                 const int a = sp[I][0], b = sp[I][1];
                 if (s == 0.0 || b < 0) continue;
