@@ -106,6 +106,12 @@ int qfca_channel_sum(const double* score, int64_t images, int32_t channels, int6
 int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t channels,
                     int32_t* used, void* stream);
 
+/* which fused scoring kernel qfca_score picks for this shape (host-only):
+ * 4 / 3 / 2 / 1 = score4.cu / score3.cu / score2.cu / score.cu, -1 none. */
+int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
+                       int32_t channels, int64_t images, int32_t pad, int32_t sample_budget,
+                       int32_t with_reference);
+
 /* channel groups qfca_score will use (host-only) for groups_hint (<= 0: auto);
  * with_reference = 0 asks for the in-kernel reference selection (returns -1
  * where that is not available). */

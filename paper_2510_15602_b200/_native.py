@@ -46,6 +46,7 @@ _SIGNATURES = {
                             _P, _P], _I32),
     "qfca_channel_sum": ([_P, _I64, _I32, _I64, _P, _I32, _P, _P, _P], _I32),
     "qfca_count_used": ([_P, _P, _I64, _I32, _P, _P], _I32),
+    "qfca_score_version": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32], _I32),
     "qfca_set_score_kernel": ([_I32], _I32),
     "qfca_score_groups": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32], _I32),
     "qfca_score": ([_P, _I32, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,

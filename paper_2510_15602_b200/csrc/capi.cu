@@ -52,16 +52,19 @@ int score3_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int launch_score3(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
 int score4_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
+int score5_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
+int launch_score5(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
+                  int, int, int, int, int, int, float*, cudaStream_t);
 int launch_score4(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
 
-// fused-kernel selection: 0 = auto (v4, else v3, else v2, else v1 -- the
-// first that applies), 1 / 2 / 3 / 4 = force that version
+// fused-kernel selection: 0 = auto (v4, else v3, else v5, else v2, else v1 --
+// the first that applies), 1 .. 5 = force that version
 static int g_score_kernel = 0;
 
 struct ScoreChoice {
     int groups;  // channel groups (partial maps per image); <= 0: unsupported
-    int ver;     // 4: score4.cu, 3: score3.cu, 2: score2.cu, 1: score.cu
+    int ver;     // 5: score5.cu, 4: score4.cu, 3: score3.cu, 2: score2.cu, 1: score.cu
     int fref;    // 1: the reference is selected inside the kernel
 };
 
@@ -85,6 +88,13 @@ static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t 
         if (gg > 0) return ScoreChoice{gg, 3, fr};
     }
     if (g_score_kernel == 3) return ch;
+    if ((g_score_kernel == 0 || g_score_kernel == 5) && bins_bytes == 1) {
+        int fr = 0;
+        const int gg = score5_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
+                                    want_fref, &fr);
+        if (gg > 0 && fr == (want_fref ? 1 : 0)) return ScoreChoice{gg, 5, fr};
+    }
+    if (g_score_kernel == 5) return ch;
     if ((g_score_kernel == 0 || g_score_kernel == 2) && bins_bytes == 1) {
         int fr = 0;
         const int gg = score2_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
@@ -101,6 +111,9 @@ static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_by
                             int C, int h, int w, int n_bins, int t, int pad, int budget,
                             float* partial, cudaStream_t st) {
     if (ch.groups <= 0) return QFCA_ERR_UNSUPPORTED;
+    if (ch.ver == 5)
+        return launch_score5(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
+                             n_bins, t, pad, budget, ch.groups, partial, st);
     if (ch.ver == 4)
         return launch_score4(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
                              n_bins, t, pad, budget, ch.groups, partial, st);
@@ -221,8 +234,18 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
     return ch.groups;
 }
 
+int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
+                       int32_t channels, int64_t images, int32_t pad, int32_t sample_budget,
+                       int32_t with_reference) {
+    const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, 0,
+                                        n_bins <= 256 ? 1 : 2, pad, sample_budget,
+                                        with_reference ? 0 : 1);
+    if (ch.groups <= 0 || (!with_reference && !ch.fref)) return -1;
+    return ch.ver;
+}
+
 int qfca_set_score_kernel(int32_t version) {
-    if (version < 0 || version > 4) return QFCA_ERR_ARG;
+    if (version < 0 || version > 5) return QFCA_ERR_ARG;
     g_score_kernel = version;
     return QFCA_OK;
 }

@@ -248,10 +248,14 @@ def test_large_plane_properties(Q):
                                            ((1, 24, 16, 128), 16, 11, "wrap"),
                                            ((1, 8, 1, 64), 16, 5, "wrap"),
                                            ((2, 30, 48, 64), 16, 7, "reflect"),
-                                           ((1, 9, 32, 128), 10, 1, "reflect")])
+                                           ((1, 9, 32, 128), 10, 1, "reflect"),
+                                           ((2, 12, 32, 32), 16, 17, "reflect"),
+                                           ((1, 10, 64, 64), 16, 33, "wrap"),
+                                           ((1, 6, 40, 128), 13, 25, "reflect"),
+                                           ((1, 8, 20, 32), 16, 65, "reflect")])
 def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
-    """v1 (score.cu), v2 (score2.cu), v3 (score3.cu) and v4 (score4.cu) fused
-    kernels all match the oracle wherever they apply."""
+    """v1 (score.cu), v2 (score2.cu), v3 (score3.cu), v4 (score4.cu) and v5
+    (score5.cu, any T) fused kernels all match the oracle wherever they apply."""
     from paper_2510_15602_b200 import _native
     from oracle import qfca_oracle as O
     rng = np.random.default_rng(sum(shape) + n + t)
@@ -259,7 +263,7 @@ def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
     cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
     refs = [O.detect(x[i], n_bins=n, patch_size=t, pad=pad)[0] for i in range(shape[0])]
     try:
-        for ver in (1, 2, 3, 4):
+        for ver in (1, 2, 3, 4, 5):
             _native.call("qfca_set_score_kernel", ver)
             if ver > 1 and Q.fused_supported(cfg):
                 try:
