@@ -202,9 +202,10 @@ k_score5(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     };
     // consumers: inclusive prefix of each chunk row of CHp[c & 1], in place
     // (one warp per row; uint32 lane words add modulo 2^32 exactly)
-    auto scan_rows = [&](int c) {
+    auto scan_rows = [&](int c, bool samples_only) {
         uint4* base = CHp + (c & 1) * CHS;
         for (int rho = warp; rho < RC; rho += NC / 32) {
+            if (samples_only && stab[c * RC + rho].w < 0) continue;
             uint4* row = base + rho * WP;
             uint32_t cx_ = 0, cy_ = 0, cz_ = 0;
             for (int b0 = 0; b0 < WP; b0 += 32) {
@@ -282,7 +283,7 @@ k_score5(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 } else {
                     for (int ch = 0; ch < n_chunks; ++ch) {
                         bar_sync5(S5_FULL0 + (ch & 1), NT);
-                        scan_rows(ch);
+                        scan_rows(ch, true);
                         asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
                         const uint4* base = CHp + (ch & 1) * CHS;
                         for (int rho = 0; rho < RC; ++rho) {
@@ -397,10 +398,11 @@ k_score5(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 const int b = 4 * gg + cj;
                 const float fi = (float)b, Vm = sVm[b < 16 ? b : 15], Dv = sD[b < 16 ? b : 15];
                 float vs = 0.f;
+                int slot = 0;
                 float* const rcol = ring + cj * W + cx;  // slot q at rcol[q * 4 * W]
                 for (int ch = 0; ch < n_chunks; ++ch) {
                     bar_sync5(S5_FULL0 + (ch & 1), NT);
-                    scan_rows(ch);
+                    scan_rows(ch, false);
                     asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
                     const uint4* base = CHp + (ch & 1) * CHS;
                     for (int rho = 0; rho < RC; ++rho) {
@@ -417,13 +419,14 @@ k_score5(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             const float ga = af < Vm ? nua : Dv - nua;
                             E = (gb - ga) * rcp_approx5(bf - af);
                         }
-                        const int slot = s % T;
-                        vs += E - rcol[slot * 4 * W];
-                        rcol[slot * 4 * W] = E;
-                        if (slot == T - 1) {  // re-anchor the sliding sum
+                        float* const rs = rcol + slot * 4 * W;  // slot = s mod T
+                        vs += E - *rs;
+                        *rs = E;
+                        if (++slot == T) {  // re-anchor the sliding sum
                             float t = 0.f;
                             for (int q = 0; q < T; ++q) t += rcol[q * 4 * W];
                             vs = t;
+                            slot = 0;
                         }
                         if (s >= 2 * R) {
                             float* vrow = Vbp + (rho * 4 + cj) * WP;
