@@ -195,6 +195,10 @@ int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, doubl
 int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw);
 int qfca_covariance(const float* x, int64_t images, int32_t C, int32_t hw, const double* mean,
                     void* workspace, int64_t workspace_bytes, double* cov, void* stream);
+/* Same, also forming the plane means (features.py:170) in the same pass over x:
+ * mean (images, C) fp64 is an output. */
+int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, double* mean,
+                         void* workspace, int64_t workspace_bytes, double* cov, void* stream);
 
 /* ---- one-call detect (scoring.py:263-327) for the fused configuration ---- */
 typedef struct qfca_config {

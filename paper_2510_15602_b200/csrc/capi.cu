@@ -42,8 +42,8 @@ int launch_cholqr(double*, int64_t, int, int, cudaStream_t);
 int64_t cov_i8_workspace(int64_t, int, int);
 int launch_chol_rinv(const double*, int64_t, int, double*, cudaStream_t);
 int launch_sym_eig(const double*, int64_t, int, double*, double*, cudaStream_t);
-int launch_cov_i8(const float*, int64_t, int, int, const double*, void*, int64_t, double*,
-                  cudaStream_t);
+int launch_cov_i8(const float*, int64_t, int, int, const double*, double*, void*, int64_t,
+                  double*, cudaStream_t);
 int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int launch_score2(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
@@ -326,8 +326,17 @@ int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw) {
 
 int qfca_covariance(const float* x, int64_t images, int32_t C, int32_t hw, const double* mean,
                     void* workspace, int64_t workspace_bytes, double* cov, void* stream) {
-    return counted(launch_cov_i8(x, images, C, hw, mean, workspace, workspace_bytes, cov,
-                                 S(stream)),
+    if (!mean) return QFCA_ERR_ARG;
+    return counted(launch_cov_i8(x, images, C, hw, mean, nullptr, workspace, workspace_bytes,
+                                 cov, S(stream)),
+                   2);
+}
+
+int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, double* mean,
+                         void* workspace, int64_t workspace_bytes, double* cov, void* stream) {
+    if (!mean) return QFCA_ERR_ARG;
+    return counted(launch_cov_i8(x, images, C, hw, nullptr, mean, workspace, workspace_bytes,
+                                 cov, S(stream)),
                    2);
 }
 

@@ -108,13 +108,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
 }
 
 // ---------------------------------------------------------------- digits
-// One CTA per (image, channel row < Cp): fixed-point exponent and the four
-// balanced base-256 digit planes D[((img * 4 + k) * Cp + c) * Kp + p].
+// One CTA per (image, channel row < Cp): the plane is staged in shared memory
+// (one HBM read), its mean is formed there when requested (fp64, fixed
+// order), then the fixed-point exponent and the four balanced base-256 digit
+// planes D[((img * 4 + k) * Cp + c) * Kp + p].
 constexpr int DG_THREADS = 256;
+
+__device__ __forceinline__ double block_reduce_dg(double v, bool is_max, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmax(v, u) : v + u;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = red[0];
+#pragma unroll
+    for (int w = 1; w < DG_THREADS / 32; ++w) v = is_max ? fmax(v, red[w]) : v + red[w];
+    return v;
+}
 
 __global__ void __launch_bounds__(DG_THREADS)
 k_cov_digits(const float* __restrict__ x, int C, int hw, int Cp, int Kp,
-             const double* __restrict__ mean, int8_t* __restrict__ D, int* __restrict__ expo) {
+             const double* __restrict__ mean_in, double* __restrict__ mean_out,
+             int8_t* __restrict__ D, int* __restrict__ expo) {
+    extern __shared__ __align__(16) float xs[];  // [hw]
+    __shared__ double red[DG_THREADS / 32];
     const int img = blockIdx.x / Cp, c = blockIdx.x % Cp;
     const int tid = threadIdx.x;
     int8_t* d0 = D + ((int64_t)(img * CV_DIG + 0) * Cp + c) * Kp;
@@ -126,17 +146,32 @@ k_cov_digits(const float* __restrict__ x, int C, int hw, int Cp, int Kp,
         return;
     }
     const float* xp = x + ((int64_t)img * C + c) * hw;
-    const double mu = mean[(int64_t)img * C + c];
-    __shared__ double red[DG_THREADS / 32];
+    double s = 0.0;
+    if ((hw & 3) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(xp);
+        for (int i = tid; i < hw / 4; i += DG_THREADS) {
+            const float4 v = __ldg(x4 + i);
+            reinterpret_cast<float4*>(xs)[i] = v;
+            s += ((double)v.x + (double)v.y) + ((double)v.z + (double)v.w);
+        }
+    } else {
+        for (int i = tid; i < hw; i += DG_THREADS) {
+            const float v = __ldg(xp + i);
+            xs[i] = v;
+            s += (double)v;
+        }
+    }
+    double mu;
+    if (mean_out) {
+        mu = block_reduce_dg(s, false, red) / (double)hw;
+        if (tid == 0) mean_out[(int64_t)img * C + c] = mu;
+    } else {
+        mu = mean_in[(int64_t)img * C + c];
+        __syncthreads();
+    }
     double m = 0.0;
-    for (int p = tid; p < hw; p += DG_THREADS) m = fmax(m, fabs((double)__ldg(xp + p) - mu));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((tid & 31) == 0) red[tid >> 5] = m;
-    __syncthreads();
-    m = red[0];
-#pragma unroll
-    for (int w = 1; w < DG_THREADS / 32; ++w) m = fmax(m, red[w]);
+    for (int p = tid; p < hw; p += DG_THREADS) m = fmax(m, fabs((double)xs[p] - mu));
+    m = block_reduce_dg(m, true, red);
     int e = 0;
     if (m > 0.0) {
         int E;
@@ -155,7 +190,7 @@ k_cov_digits(const float* __restrict__ x, int C, int hw, int Cp, int Kp,
             for (int j = 0; j < 4; ++j) {
                 const int p = p0 + 4 * q + j;
                 int n = 0;
-                if (p < hw) n = (int)rint(((double)__ldg(xp + p) - mu) * sc);
+                if (p < hw) n = (int)rint(((double)xs[p] - mu) * sc);
                 // balanced digits: n = d0 + 256 (d1 + 256 (d2 + 256 d3)), d_k in [-128, 127]
 #pragma unroll
                 for (int k = 0; k < CV_DIG; ++k) {
@@ -324,9 +359,11 @@ int64_t cov_i8_workspace(int64_t images, int C, int hw) {
     return images * CV_DIG * Cp * Kp + ((images * C * 4 + 255) & ~255LL);
 }
 
-// cov (images, C, C) fp64 of the centred features x (images, C, hw) fp32.
+// cov (images, C, C) fp64 of the centred features x (images, C, hw) fp32;
+// mean_out != nullptr: the plane means are formed here (and mean ignored).
 int launch_cov_i8(const float* x, int64_t images, int C, int hw, const double* mean,
-                  void* workspace, int64_t ws_bytes, double* cov, cudaStream_t st) {
+                  double* mean_out, void* workspace, int64_t ws_bytes, double* cov,
+                  cudaStream_t st) {
     if (images <= 0 || C <= 0 || hw <= 0) return QFCA_ERR_ARG;
     const int Cp = (C + CV_BM - 1) / CV_BM * CV_BM;
     const int Kp = (hw + CV_BK - 1) / CV_BK * CV_BK;
@@ -340,7 +377,13 @@ int launch_cov_i8(const float* x, int64_t images, int C, int hw, const double* m
     int8_t* D = reinterpret_cast<int8_t*>(workspace);
     int* expo = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(workspace) +
                                        images * CV_DIG * (int64_t)Cp * Kp);
-    k_cov_digits<<<(unsigned)(images * Cp), DG_THREADS, 0, st>>>(x, C, hw, Cp, Kp, mean, D, expo);
+    const size_t dsmem = (size_t)hw * 4;
+    if (dsmem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_cov_digits, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dsmem) != cudaSuccess)
+        return QFCA_ERR_CUDA;
+    k_cov_digits<<<(unsigned)(images * Cp), DG_THREADS, dsmem, st>>>(x, C, hw, Cp, Kp, mean,
+                                                                      mean_out, D, expo);
     if (cudaGetLastError() != cudaSuccess) return QFCA_ERR_CUDA;
 
     CUtensorMap map;

@@ -138,7 +138,7 @@ def covariance_dev(xc: torch.Tensor, chunk: int = 1024, precise: str = "fp32"
 _COV_WS: dict = {}
 
 
-def covariance_exact(x: torch.Tensor, mean: torch.Tensor) -> torch.Tensor:
+def covariance_exact(x: torch.Tensor, mean: torch.Tensor | None) -> torch.Tensor:
     """(B, C, H, W) fp32 features, (B, C) fp64 means -> (B, C, C) fp64 covariance
     (features.py:167-171), fp64-accurate.
 
@@ -158,6 +158,15 @@ def covariance_exact(x: torch.Tensor, mean: torch.Tensor) -> torch.Tensor:
     if ws is None:
         _COV_WS.clear()
         ws = _COV_WS[key] = empty((max(need, 1),), torch.uint8)
+    if mean is None:  # also form the plane means (features.py:170), returned
+        mean_out = empty((b, c), torch.float64)
+        st = L.qfca_mean_covariance(x.data_ptr(), b, c, hw, mean_out.data_ptr(), ws.data_ptr(),
+                                    need, cov.data_ptr(), N.stream())
+        if st == N.QFCA_ERR_UNSUPPORTED:
+            N.call("qfca_plane_mean", x.data_ptr(), b * c, hw, mean_out.data_ptr(), N.stream())
+            return covariance_exact(x, mean_out), mean_out
+        N.check(st, "qfca_mean_covariance")
+        return cov, mean_out
     st = L.qfca_covariance(x.data_ptr(), b, c, hw, mean.data_ptr(), ws.data_ptr(), need,
                            cov.data_ptr(), N.stream())
     if st == N.QFCA_ERR_UNSUPPORTED:
@@ -275,9 +284,7 @@ def pca_fit_batch(x: torch.Tensor, k: int):
     b, c, h, w = x.shape
     hw = h * w
     s = N.stream()
-    mean = empty((b, c), torch.float64)
-    N.call("qfca_plane_mean", x.data_ptr(), b * c, hw, mean.data_ptr(), s)
-    cov = covariance_exact(x, mean)
+    cov, mean = covariance_exact(x, None)  # means and covariance in one pass over x
     # np.argsort(evals, kind="stable")[::-1][:k] of the ascending eigh output is
     # the top-k in descending order (ties keep the higher index first)
     evals, vecs = topk_eigh(cov, k)
