@@ -118,6 +118,83 @@ int launch_minmax(const float* x, int64_t planes, int64_t plane_len, float* lo, 
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
+// ---- threshold-table binning, bit-exact by construction:
+// bin_of is monotone in v, so bin(v) = #{k >= 1 : v >= tau_k} with tau_k the
+// smallest float32 whose fp64 bin is >= k.  One lane per threshold bisects the
+// ordered float keys between lo and hi (exact bin_of at every probe); the
+// element pass is then float compares only (no fp64 division per element).
+constexpr int BT_MAXN = 64;  // thresholds held per plane in shared memory
+
+__device__ __forceinline__ int fkey(float f) {
+    const int k = __float_as_int(f);
+    return k >= 0 ? k : k ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float fval(int key) {
+    return __int_as_float(key >= 0 ? key : key ^ 0x7FFFFFFF);
+}
+
+__global__ void __launch_bounds__(128)
+k_bin_thresholds(const float* __restrict__ lo, const float* __restrict__ hi, int64_t planes,
+                 int n_bins, float* __restrict__ tau) {
+    const int64_t plane = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (plane >= planes) return;
+    const int lane = threadIdx.x & 31;
+    const float lf = lo[plane], hf = hi[plane];
+    const double l = lf, span = (double)hf - (double)lf;
+    for (int k = 1 + lane; k < n_bins; k += 32) {
+        float t = INFINITY;  // degenerate channel: every bin is 0
+        if (hf > lf) {
+            int64_t a = fkey(lf), b = fkey(hf);  // bin(lo) = 0 < k <= N-1 = bin(hi)
+            while (b - a > 1) {
+                const int64_t m = a + (b - a) / 2;
+                if (bin_of(fval((int)m), l, span, n_bins) >= k) b = m; else a = m;
+            }
+            t = fval((int)b);
+        }
+        tau[plane * (n_bins - 1) + (k - 1)] = t;
+    }
+}
+
+template <typename BT>
+__global__ void __launch_bounds__(256)
+k_bin_table(const float* __restrict__ x, int64_t plane_len, const float* __restrict__ lo,
+            const float* __restrict__ hi, const float* __restrict__ tau, int n_bins,
+            BT* __restrict__ out) {
+    __shared__ float st[BT_MAXN + 1];
+    const int64_t plane = blockIdx.x;  // one CTA per plane: the setup is paid once
+    const int nt = n_bins - 1;
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) st[k] = tau[plane * nt + k];
+    const float lf = lo[plane], hf = hi[plane];
+    const float inv = hf > lf ? (float)((double)n_bins / ((double)hf - (double)lf)) : 0.f;
+    const float top = (float)nt;
+    __syncthreads();
+    const float* p = x + plane * plane_len;
+    BT* o = out + plane * plane_len;
+    // fp32 estimate, then exact fix-up against the thresholds (bin k starts at st[k-1])
+    auto bin = [&](float v) {
+        int b = (int)fminf(fmaxf((v - lf) * inv, 0.f), top);  // NaN -> 0
+        while (b < nt && v >= st[b]) ++b;
+        while (b > 0 && v < st[b - 1]) --b;
+        return b;
+    };
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
+                     (sizeof(BT) == 2 || (reinterpret_cast<uintptr_t>(o) & 3) == 0);
+    const int64_t n4 = vec ? plane_len / 4 : 0;
+    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i);
+        const int b0 = bin(v.x), b1 = bin(v.y), b2 = bin(v.z), b3 = bin(v.w);
+        if (sizeof(BT) == 1) {
+            reinterpret_cast<uint32_t*>(o)[i] =
+                (uint32_t)b0 | ((uint32_t)b1 << 8) | ((uint32_t)b2 << 16) | ((uint32_t)b3 << 24);
+        } else {
+            reinterpret_cast<uint2*>(o)[i] =
+                make_uint2((uint32_t)b0 | ((uint32_t)b1 << 16), (uint32_t)b2 | ((uint32_t)b3 << 16));
+        }
+    }
+    for (int64_t i = 4 * n4 + threadIdx.x; i < plane_len; i += blockDim.x)
+        o[i] = (BT)bin(__ldg(p + i));
+}
+
 int launch_bin(const float* x, int64_t planes, int64_t plane_len, const float* lo,
                const float* hi, int n_bins, void* out, int out_bytes, cudaStream_t st) {
     if (planes <= 0 || plane_len <= 0 || n_bins < 1) return QFCA_ERR_ARG;
@@ -125,6 +202,23 @@ int launch_bin(const float* x, int64_t planes, int64_t plane_len, const float* l
     const int64_t bpp = (plane_len + per - 1) / per;
     const int64_t grid = bpp * planes;
     if (grid > 0x7fffffffLL) return QFCA_ERR_ARG;
+    if (n_bins >= 2 && n_bins <= BT_MAXN + 1 && (out_bytes == 1 || out_bytes == 2)) {
+        // thresholds in a stream-ordered scratch allocation
+        float* tau = nullptr;
+        if (cudaMallocAsync(&tau, (size_t)planes * (n_bins - 1) * sizeof(float), st) !=
+            cudaSuccess)
+            return QFCA_ERR_CUDA;
+        k_bin_thresholds<<<(unsigned)((planes + 3) / 4), 128, 0, st>>>(lo, hi, planes, n_bins, tau);
+        if (out_bytes == 1)
+            k_bin_table<uint8_t><<<(unsigned)planes, 256, 0, st>>>(x, plane_len, lo, hi, tau,
+                                                                    n_bins, (uint8_t*)out);
+        else
+            k_bin_table<uint16_t><<<(unsigned)planes, 256, 0, st>>>(x, plane_len, lo, hi, tau,
+                                                                     n_bins, (uint16_t*)out);
+        const bool ok = cudaGetLastError() == cudaSuccess;
+        cudaFreeAsync(tau, st);
+        return ok ? QFCA_OK : QFCA_ERR_CUDA;
+    }
     if (out_bytes == 1) {
         if (n_bins > 256) return QFCA_ERR_ARG;
         k_bin<uint8_t><<<(unsigned)grid, 256, 0, st>>>(x, plane_len, bpp, lo, hi, n_bins,
