@@ -20,8 +20,8 @@
 //
 // Kernel layout (one 128 x 64 output tile per CTA, lower triangle only, the
 // mirror written by the same CTA):
-//   warp 0   TMA producer: per K-stage of 128 pixels, the 4 digit tiles of the
-//            128 A rows and of the 64 B rows (SWIZZLE_128B, 96 KB), 2 stages;
+//   warp 0   TMA producer: per K-stage of 64 pixels, the 4 digit tiles of the
+//            128 A rows and of the 64 B rows (SWIZZLE_64B, 48 KB), 4 stages;
 //   warp 1   MMA issuer: 13 pairs x 4 k-steps of tcgen05.mma.kind::i8
 //            (M = 128, N = 64, K = 32) into 5 x 64 TMEM columns;
 //   warps 2-5 epilogue: tcgen05.ld, fp64 class combine, scale, store.
@@ -34,13 +34,13 @@ namespace qfca {
 
 constexpr int CV_BM = 128;   // A rows (channels) per tile
 constexpr int CV_BN = 64;    // B rows (channels) per tile
-constexpr int CV_BK = 128;   // K bytes (pixels) per stage = one 128-byte swizzle row
+constexpr int CV_BK = 64;    // K bytes (pixels) per stage = one 64-byte swizzle row
 constexpr int CV_DIG = 4;    // base-256 digits
 constexpr int CV_CLS = 5;    // classes k + l = 2..6
-constexpr int CV_STAGES = 2;
+constexpr int CV_STAGES = 4;
 constexpr int CV_THREADS = 192;
-constexpr int CV_A_BYTES = CV_BM * CV_BK;                              // 16 KB per digit
-constexpr int CV_B_BYTES = CV_BN * CV_BK;                              // 8 KB per digit
+constexpr int CV_A_BYTES = CV_BM * CV_BK;                              // 8 KB per digit
+constexpr int CV_B_BYTES = CV_BN * CV_BK;                              // 4 KB per digit
 constexpr int CV_STAGE_BYTES = CV_DIG * (CV_A_BYTES + CV_B_BYTES);    // 96 KB
 constexpr int CV_SMEM = CV_STAGES * CV_STAGE_BYTES + 1024 + 256;      // + align + barriers
 constexpr int CV_TMEM_COLS = 512;
@@ -73,14 +73,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    // K-major, SWIZZLE_128B: 8-row atoms of 1024 B (SBO), version 1 (sm_100)
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+    // K-major, SWIZZLE_64B: 8-row atoms of 8 x 64 B = 512 B (SBO), version 1 (sm_100)
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+    d |= (uint64_t)(512 >> 4) << 32;        // SBO
     d |= (uint64_t)1 << 46;                 // descriptor version
-    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+    d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
     return d;
 }
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
@@ -216,8 +216,8 @@ k_cov_i8(const __grid_constant__ CUtensorMap tmap, int C, int Cp, int Kp, int hw
     extern __shared__ uint8_t cv_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)cv_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + CV_STAGES * CV_STAGE_BYTES);
-    // bars[0..1] full, [2..3] empty, [4] tmem full; tmem base after them
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    // bars[s] full, bars[CV_STAGES + s] empty, bars[2 CV_STAGES] tmem full; tmem base after
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * CV_STAGES + 2);
 
     const int nI = Cp / CV_BM;
     const int tiles = nI * (nI + 1);  // lower-triangle 128 x 64 tiles: 2I + 2 per row block
@@ -231,9 +231,9 @@ k_cov_i8(const __grid_constant__ CUtensorMap tmap, int C, int Cp, int Kp, int hw
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < CV_STAGES; ++s) {
             mbar_init(smem_u32(&bars[s]), 1);
-            mbar_init(smem_u32(&bars[2 + s]), 1);
+            mbar_init(smem_u32(&bars[CV_STAGES + s]), 1);
         }
-        mbar_init(smem_u32(&bars[4]), 1);
+        mbar_init(smem_u32(&bars[2 * CV_STAGES]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
@@ -254,7 +254,7 @@ k_cov_i8(const __grid_constant__ CUtensorMap tmap, int C, int Cp, int Kp, int hw
             const int rowB = img * CV_DIG * Cp + J * CV_BN;
             for (int kb = 0; kb < nkb; ++kb) {
                 const int s = kb % CV_STAGES;
-                if (kb >= CV_STAGES) mbar_wait(smem_u32(&bars[2 + s]), ((kb / CV_STAGES) & 1) ^ 1);
+                if (kb >= CV_STAGES) mbar_wait(smem_u32(&bars[CV_STAGES + s]), ((kb / CV_STAGES) & 1) ^ 1);
                 const uint32_t full = smem_u32(&bars[s]);
                 mbar_expect_tx(full, CV_STAGE_BYTES);
                 const uint32_t base = smem_u32(sm + s * CV_STAGE_BYTES);
@@ -286,24 +286,24 @@ k_cov_i8(const __grid_constant__ CUtensorMap tmap, int C, int Cp, int Kp, int hw
                         for (int l = 0; l < CV_DIG; ++l) {
                             if (k + l < 2) continue;
                             const int cls = k + l - 2;
-                            const uint64_t ad = sw128_desc(base + k * CV_A_BYTES + kk * 32);
+                            const uint64_t ad = sw64_desc(base + k * CV_A_BYTES + kk * 32);
                             const uint64_t bd =
-                                sw128_desc(base + CV_DIG * CV_A_BYTES + l * CV_B_BYTES + kk * 32);
+                                sw64_desc(base + CV_DIG * CV_A_BYTES + l * CV_B_BYTES + kk * 32);
                             const uint32_t acc = (kb > 0 || kk > 0 || !first[cls]) ? 1u : 0u;
                             first[cls] = false;
                             mma_i8(tmem + cls * CV_BN, ad, bd, idesc, acc);
                         }
                 }
-                mma_commit(smem_u32(&bars[2 + s]));  // stage free once these MMAs complete
+                mma_commit(smem_u32(&bars[CV_STAGES + s]));  // stage free once these MMAs complete
             }
-            mma_commit(smem_u32(&bars[4]));  // accumulators complete
+            mma_commit(smem_u32(&bars[2 * CV_STAGES]));  // accumulators complete
         }
         __syncwarp();
     } else {
         // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31
         const int q = warp & 3;
         const int r = I * CV_BM + q * 32 + lane;  // channel row
-        mbar_wait(smem_u32(&bars[4]), 0);
+        mbar_wait(smem_u32(&bars[2 * CV_STAGES]), 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int er = r < C ? expo[(int64_t)img * C + r] : 0;
         double* cimg = cov + (int64_t)img * C * C;
@@ -392,7 +392,7 @@ int launch_cov_i8(const float* x, int64_t images, int C, int hw, const double* m
     const cuuint32_t box[2] = {CV_BK, 64};
     const cuuint32_t estride[2] = {1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, D, gdim, gstride, box, estride,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return QFCA_ERR_CUDA;
     if (cudaFuncSetAttribute(k_cov_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, CV_SMEM) !=
