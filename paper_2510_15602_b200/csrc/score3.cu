@@ -40,7 +40,9 @@ struct Score3Geom {
     int WP;    // padded row length w + 2r
     int S;     // stream rows h + 2r
     int fref, stride, nsx, nsamp, sp;
-    int o_bins, o_pj, o_vd, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, o_sv, o_sa, total;
+    uint32_t moff;  // -4 * 0x4B000000 (mod 2^32): magic-float -> G-table byte offset
+    int o_bins, o_pj, o_vd, o_gt, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, o_sv, o_sa,
+        total;
 };
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
@@ -48,6 +50,12 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ float lds3_f32(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+    return v;
 }
 __device__ __forceinline__ float rcp_approx3(float x) {
     float y;
@@ -74,6 +82,7 @@ static void score3_layout(Score3Geom& g) {
     g.o_bins = take((long long)CPB * g.h * W);
     g.o_pj = take((long long)CPB * (T * T + 1) * 4);
     g.o_vd = take((long long)CPB * 16 * 2 * 4);
+    g.o_gt = take((long long)CPB * 16 * (T * T + 1) * 4);  // G_i(v) tables
     g.o_stab = take((long long)((g.S + T - 1) / T) * T * 16);
     g.o_chp = take((long long)2 * T * CPB * g.WP * 16);   // double-buffered column words
     g.o_wh = take((long long)T * CPB * W * 16);           // row windows (uint4 per pixel)
@@ -104,6 +113,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     uint8_t* const sb = sm + g.o_bins;
     float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
     float* const sVD = reinterpret_cast<float*>(sm + g.o_vd);
+    float* const sGT = reinterpret_cast<float*>(sm + g.o_gt);
     int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);
     uint4* const CHp = reinterpret_cast<uint4*>(sm + g.o_chp);
     uint4* const WH = reinterpret_cast<uint4*>(sm + g.o_wh);
@@ -400,18 +410,32 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             sVD[(k * 16 + i) * 2] = vm;
             sVD[(k * 16 + i) * 2 + 1] = d;
         }
+        // G_i(v) for every bin and count (same fp32 operations as the inline form)
+        for (int idx = tid; idx < CPB * 16 * (T2 + 1); idx += S3_THREADS) {
+            const int ki = idx / (T2 + 1), v = idx - ki * (T2 + 1);
+            const int k = ki >> 4, i = ki & 15;
+            const float* pjk = sPJ + k * (T2 + 1);
+            float vm = 0.f, d = 0.f;
+            if (i < g.n_bins) {
+                const int vmi = i > 0 ? sV[k * 16 + i - 1] : 0;
+                vm = (float)vmi;
+                d = 2.f * ((float)i * vm - pjk[vmi]);
+            }
+            const float fv = (float)v;
+            const float nu = fmaf((float)i, fv, -pjk[v]);
+            sGT[idx] = fv < vm ? nu : d - nu;
+        }
         __syncthreads();
 
         // ---- pass 1: scoring
         if (is_p) {
             produce();
         } else {
-            float Vm[4], Dv[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                Vm[j] = sVD[(cs * 16 + grp4 + j) * 2];
-                Dv[j] = sVD[(cs * 16 + grp4 + j) * 2 + 1];
-            }
+            constexpr int GP = T2 + 1;
+            const bool g1 = (grp & 1) != 0, g2 = (grp & 2) != 0;
+            // G-table address of count b = gaddr + 4 * magic(b) (see score4.cu)
+            const uint32_t gaddr =
+                (uint32_t)__cvta_generic_to_shared(sGT + (cs * 16 + grp4) * GP) + g.moff;
             float ring[T][4];
             float vs[4];
 #pragma unroll
@@ -428,36 +452,33 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
                     const uint4 v = WH[(rho * CPB + cs) * W + x];
-                    const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
-                    const uint32_t prev = grp == 1 ? v.x : grp == 2 ? v.y : grp == 3 ? v.z : 0u;
+                    // (word, prev) = words grp, grp - 1 (0 for grp 0): branch-free selects
+                    const uint32_t wlo = g1 ? v.y : v.x, whi = g1 ? v.w : v.z;
+                    const uint32_t plo = g1 ? v.x : 0u, phi = g1 ? v.z : v.y;
+                    const uint32_t word = g2 ? whi : wlo, prev = g2 ? phi : plo;
                     const bool mass = (word >> 24) != (prev >> 24);
+                    float E[4] = {0.f, 0.f, 0.f, 0.f};  // no mass in the group: E = 0
                     if (__any_sync(0xffffffffu, mass)) {
-                        const uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
-                        float af = __uint_as_float(ma) - 8388608.0f;
-                        float pja = pj[ma - 0x4B000000u];
+                        uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                        uint32_t aa = gaddr + 4u * ma;
+#define S3_E(J)                                                                 \
+    {                                                                           \
+        const uint32_t mb = __byte_perm(word, 0x4B000000u, 0x7650 + J);         \
+        const uint32_t ab = gaddr + 4u * mb;                                    \
+        const float gb = lds3_f32<J * GP * 4>(ab);                              \
+        const float ga = lds3_f32<J * GP * 4>(aa);                              \
+        const float pc = __uint_as_float(mb) - __uint_as_float(ma);             \
+        E[J] = (gb - ga) * rcp_approx3(fmaxf(pc, 1.f));                         \
+        ma = mb;                                                                \
+        aa = ab;                                                                \
+    }
+                        S3_E(0) S3_E(1) S3_E(2) S3_E(3)
+#undef S3_E
+                    }
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint32_t mbits = __byte_perm(word, 0x4B000000u, 0x7650 + j);
-                            const float bf = __uint_as_float(mbits) - 8388608.0f;
-                            const float pjb = pj[mbits - 0x4B000000u];
-                            const float fi = (float)(grp4 + j);
-                            const float nua = fmaf(fi, af, -pja);
-                            const float nub = fmaf(fi, bf, -pjb);
-                            const float ga = af < Vm[j] ? nua : Dv[j] - nua;
-                            const float gb = bf < Vm[j] ? nub : Dv[j] - nub;
-                            const float pc = bf - af;
-                            const float E = (gb - ga) * rcp_approx3(fmaxf(pc, 1.f));
-                            vs[j] += E - ring[rho][j];
-                            ring[rho][j] = E;
-                            af = bf;
-                            pja = pjb;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            vs[j] -= ring[rho][j];
-                            ring[rho][j] = 0.f;
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        vs[j] += E[j] - ring[rho][j];
+                        ring[rho][j] = E[j];
                     }
                     if (rho == T - 1) {
 #pragma unroll
@@ -523,6 +544,7 @@ static int score3_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     Score3Geom g;
     memset(&g, 0, sizeof(g));
     g.h = h; g.n_bins = n_bins; g.pad = pad; g.C = C;
+    g.moff = 0u - 4u * 0x4B000000u;
     g.WP = w + 2 * (t / 2);
     g.S = h + 2 * (t / 2);
     g.fref = fused_ref && t * t <= 126 && budget >= 1 && (pad == QFCA_PAD_WRAP || h > 1) ? 1 : 0;
