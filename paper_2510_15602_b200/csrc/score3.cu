@@ -446,8 +446,18 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
             consume_h2(0, false);
             bar_sync(BAR_C, S3_CT);  // WH(0) complete
+            constexpr int MAXA = (T + A_ROWS - 1) / A_ROWS;  // box rows per thread
             for (int c = 0; c < n_chunks; ++c) {
                 const int s0 = c * T;
+                // partial-map values of this chunk's box rows, fetched before the
+                // transport so their latency hides behind it
+                float pold[MAXA];
+#pragma unroll
+                for (int q = 0; q < MAXA; ++q) {
+                    const int rho = a_r0 + q * A_ROWS;
+                    const int y = s0 + rho - 2 * R;
+                    pold[q] = (rho < T && y >= 0 && y < h) ? part[y * W + a_x] : 0.f;
+                }
                 // ---- E(c): closed-form transport, register ring, vertical box
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
@@ -497,9 +507,11 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
                 bar_sync(BAR_C, S3_CT);  // Vb complete, WH free
                 // ---- A(c): own-bin horizontal box, slots in fixed order, partial RMW
-                for (int rho = a_r0; rho < T; rho += A_ROWS) {
+#pragma unroll
+                for (int q = 0; q < MAXA; ++q) {
+                    const int rho = a_r0 + q * A_ROWS;
                     const int y = s0 + rho - 2 * R;
-                    if (y < 0 || y >= h) continue;
+                    if (rho >= T || y < 0 || y >= h) continue;
                     float acc = 0.f;
 #pragma unroll
                     for (int k = 0; k < CPB; ++k) {
@@ -517,7 +529,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         }
                         acc = fmaf(f, scale, acc);
                     }
-                    part[y * W + a_x] += acc;
+                    part[y * W + a_x] = pold[q] + acc;
                 }
                 // ---- H2(c+1) in the same phase (WH is free, Vb is only read)
                 if (c + 1 < n_chunks) consume_h2(c + 1, false);
