@@ -42,7 +42,7 @@ struct Score3Geom {
     int fref, stride, nsx, nsamp, sp;
     uint32_t moff;  // -4 * 0x4B000000 (mod 2^32): magic-float -> G-table byte offset
     int o_bins, o_pj, o_vd, o_gt, o_stab, o_chp, o_wh, o_vb, o_xmap, o_scale, o_th, o_sv, o_sa,
-        total;
+        o_srch, total;
 };
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
@@ -87,13 +87,14 @@ static void score3_layout(Score3Geom& g) {
     g.o_chp = take((long long)2 * T * CPB * g.WP * 16);   // double-buffered column words
     g.o_wh = take((long long)T * CPB * W * 16);           // row windows (uint4 per pixel)
     const long long vb = (long long)T * CPB * 16 * W * 4;
-    const long long sa = g.fref ? (long long)CPB * 16 * g.sp : 0;
+    const long long sa = g.fref ? (long long)CPB * 16 * g.nsamp : 0;  // uint4 per sample
     g.o_vb = take(vb > sa ? vb : sa);
     g.o_sa = g.o_vb;
     g.o_xmap = take((long long)g.WP * 4);
     g.o_scale = take((long long)CPB * 4);
     g.o_th = take((long long)256 * 16);
     g.o_sv = take((long long)CPB * 16 * 4);
+    g.o_srch = take(1024);  // search counters, packed mids, brackets
     g.total = off;
 }
 
@@ -122,7 +123,11 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     float* const sscale = reinterpret_cast<float*>(sm + g.o_scale);
     uint4* const TH = reinterpret_cast<uint4*>(sm + g.o_th);
     int* const sV = reinterpret_cast<int*>(sm + g.o_sv);
-    uint8_t* const SA = sm + g.o_sa;
+    uint4* const SA4 = reinterpret_cast<uint4*>(sm + g.o_sa);  // [CPB][nsamp] sample windows
+    uint32_t* const scnt = reinterpret_cast<uint32_t*>(sm + g.o_srch);        // [2][CPB][8]
+    uint8_t* const sqm8 = sm + g.o_srch + 256;                                 // [CPB][16]
+    int* const sblo = reinterpret_cast<int*>(sm + g.o_srch + 320);            // [CPB * 16]
+    int* const sbhi = reinterpret_cast<int*>(sm + g.o_srch + 576);            // [CPB * 16]
 
     const int tid = threadIdx.x;
     const bool is_p = tid >= S3_CT;
@@ -320,49 +325,78 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 for (int c = 0; c < n_chunks; ++c) {
                     consume_h2(c, true);
                     bar_sync(BAR_C, S3_CT);  // WH complete
-                    if (xsamp >= 0) {
-                        uint8_t* sa = SA + (cs * 16 + grp4) * g.sp + xsamp;
+                    if (xsamp >= 0 && grp == 0) {  // sample windows, pixel-major (uint4)
 #pragma unroll
                         for (int rho = 0; rho < T; ++rho) {
                             const int si = stab[c * T + rho].w;
                             if (si < 0) continue;
-                            const uint4 v = WH[(rho * CPB + cs) * W + x];
-                            const uint32_t word = grp == 0 ? v.x : grp == 1 ? v.y : grp == 2 ? v.z : v.w;
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) sa[j * g.sp + si] = (word >> (8 * j)) & 0xff;
+                            SA4[cs * g.nsamp + si + xsamp] = WH[(rho * CPB + cs) * W + x];
                         }
                     }
                     bar_sync(BAR_C, S3_CT);  // WH may be overwritten
                 }
             }
             __syncthreads();
-            for (int idx = tid; idx < CPB * 16 * (g.sp - g.nsamp); idx += S3_THREADS) {
-                const int row = idx / (g.sp - g.nsamp), k = idx % (g.sp - g.nsamp);
-                SA[row * g.sp + g.nsamp + k] = 127;
-            }
-            __syncthreads();
-            {  // one warp per (slot, bin): smallest v with #{A <= v} >= S - m
-                const int warp = tid >> 5, lane = tid & 31;
+            {  // all 16 bins at once: lock-step binary search with packed 8-bit
+               // compares (see score4.cu): smallest v with #{A <= v} >= S - m
+                constexpr int TPS = S3_THREADS / CPB;  // search threads per slot
+                static_assert(TPS % 32 == 0, "search warps must not straddle slots");
+                constexpr int ROUNDS = T2 < 2 ? 1 : (T2 < 4 ? 2 : (T2 < 8 ? 3 : (T2 < 16 ? 4 :
+                                       (T2 < 32 ? 5 : (T2 < 64 ? 6 : 7)))));
                 const int c0 = g.nsamp - (g.nsamp - 1) / 2;
-                for (int task = warp; task < CPB * 16; task += S3_THREADS / 32) {
-                    const int k = task / 16, i = task % 16;
-                    int res = T2;
-                    if (i < g.n_bins - 1 && sscale[k] != 0.f) {
-                        const uint32_t* row = reinterpret_cast<const uint32_t*>(SA + task * g.sp);
-                        int a = 0, bnd = T2;
-                        while (a < bnd) {
-                            const int mid = (a + bnd) >> 1;
-                            const uint32_t q = 0x80808080u | ((uint32_t)mid * 0x01010101u);
-                            int cnt = 0;
-                            for (int wi = lane; wi < g.sp / 4; wi += 32)
-                                cnt += __popc((q - row[wi]) & 0x80808080u);
-                            cnt = warp_sum_i(cnt);
-                            if (cnt >= c0) bnd = mid; else a = mid + 1;
-                        }
-                        res = a;
-                    }
-                    if (lane == 0) sV[task] = res;
+                if (tid < CPB * 16) {
+                    const int k = tid >> 4, i = tid & 15;
+                    const int top = (i < g.n_bins - 1 && sscale[k] != 0.f) ? 0 : T2;
+                    sblo[tid] = top;
+                    sbhi[tid] = T2;
+                    sqm8[tid] = (uint8_t)((top + T2) >> 1);
                 }
+                for (int i = tid; i < 2 * CPB * 8; i += S3_THREADS) scnt[i] = 0;
+                __syncthreads();
+                const int k = tid / TPS, lt = tid - k * TPS, lane = tid & 31;
+                const uint4* sa = SA4 + (size_t)k * g.nsamp;
+                const uint32_t* sqm = reinterpret_cast<const uint32_t*>(sqm8);
+#pragma unroll 1
+                for (int r = 0; r < ROUNDS; ++r) {
+                    const int par = r & 1;
+                    uint32_t Q[4], acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) Q[q] = 0x80808080u | sqm[k * 4 + q];
+                    for (int smp = lt; smp < g.nsamp; smp += TPS) {
+                        const uint4 v = sa[smp];
+                        acc[0] += __umulhi((Q[0] - v.x) & 0x80808080u, 1u << 25);
+                        acc[1] += __umulhi((Q[1] - v.y) & 0x80808080u, 1u << 25);
+                        acc[2] += __umulhi((Q[2] - v.z) & 0x80808080u, 1u << 25);
+                        acc[3] += __umulhi((Q[3] - v.w) & 0x80808080u, 1u << 25);
+                    }
+                    uint32_t* cp = scnt + (par * CPB + k) * 8;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t ev = __reduce_add_sync(0xffffffffu, acc[q] & 0x00FF00FFu);
+                        const uint32_t od =
+                            __reduce_add_sync(0xffffffffu, (acc[q] >> 8) & 0x00FF00FFu);
+                        if (lane == 0) {
+                            atomicAdd(cp + 2 * q, ev);
+                            atomicAdd(cp + 2 * q + 1, od);
+                        }
+                    }
+                    __syncthreads();
+                    if (tid < CPB * 16) {
+                        const int kk = tid >> 4, i = tid & 15, j = i & 3, q = i >> 2;
+                        const uint32_t word = scnt[(par * CPB + kk) * 8 + 2 * q + (j & 1)];
+                        const int count = (int)((j >> 1) ? word >> 16 : word & 0xFFFFu);
+                        int a = sblo[tid], bnd = sbhi[tid];
+                        const int mid = (a + bnd) >> 1;
+                        if (count >= c0) bnd = mid; else a = mid + 1;
+                        sblo[tid] = a;
+                        sbhi[tid] = bnd;
+                        sqm8[tid] = (uint8_t)((a + bnd) >> 1);
+                    }
+                    for (int i = tid; i < CPB * 8; i += S3_THREADS)
+                        scnt[((par ^ 1) * CPB) * 8 + i] = 0;
+                    __syncthreads();
+                }
+                if (tid < CPB * 16) sV[tid] = sblo[tid];
             }
             __syncthreads();
         }
