@@ -185,6 +185,24 @@ int qfca_chol_rinv(const double* gram, int64_t batch, int32_t p, double* rinv, v
 int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, double* evecs,
                  void* stream);
 
+/* Block Lanczos (8-column blocks, full reorthogonalisation) on a batch of
+ * symmetric C x C fp64 matrices (C % 64 == 0, C <= 512), the Krylov stage of the
+ * top-k eigensolver replacing np.linalg.eigh of pca_fit (features.py:173):
+ * q0 (C, 8) seeded start block R (the kernel starts from qr(cov R)); basis (batch, 8*passes, C) receives the
+ * Krylov basis (vector-contiguous), h (batch, n, n) row-major the upper block
+ * triangle of H = basis^T cov basis (n = 8*passes <= C, passes <= 32);
+ * passes + 1 sweeps over cov in all. */
+int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, const double* q0,
+                 double* basis, double* h, void* stream);
+
+/* Top-32 subspace of the Lanczos projection (batch, n, n), n <= 128, n % 8 == 0,
+ * as qfca_lanczos writes it (upper block triangle): x <- qr(H (H x)) for `iters`
+ * steps from the seeded start block x0 (n, 32); outputs x (batch, n, 32) and
+ * the Rayleigh-Ritz matrix hm = x^T H x (batch, 32, 32), whose eigenpairs
+ * (qfca_sym_eig) give the Ritz pairs (Ritz vectors basis^T x u). */
+int qfca_ritz(const double* h, int64_t batch, int32_t n, const double* x0, int32_t iters,
+              double* x, double* hm, void* stream);
+
 /* Covariance of pca_fit (features.py:167-171): cov = (x - mean)^T (x - mean) / n
  * for a batch of images, x (images, C, hw) fp32 channel-major, mean (images, C)
  * fp64 -> cov (images, C, C) fp64.  fp64-accurate (~1e-11 relative): the

@@ -42,6 +42,8 @@ int launch_cholqr(double*, int64_t, int, int, cudaStream_t);
 int64_t cov_i8_workspace(int64_t, int, int);
 int launch_chol_rinv(const double*, int64_t, int, double*, cudaStream_t);
 int launch_sym_eig(const double*, int64_t, int, double*, double*, cudaStream_t);
+int launch_lanczos(const double*, int64_t, int, int, const double*, double*, double*, cudaStream_t);
+int launch_ritz(const double*, int64_t, int, const double*, int, double*, double*, cudaStream_t);
 int launch_cov_i8(const float*, int64_t, int, int, const double*, double*, void*, int64_t,
                   double*, cudaStream_t);
 int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
@@ -317,6 +319,16 @@ int qfca_chol_rinv(const double* gram, int64_t batch, int32_t p, double* rinv, v
 int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, double* evecs,
                  void* stream) {
     return counted(launch_sym_eig(h, batch, p, evals, evecs, S(stream)), 1);
+}
+
+int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, const double* q0,
+                 double* basis, double* h, void* stream) {
+    return counted(launch_lanczos(cov, batch, C, passes, q0, basis, h, S(stream)), 1);
+}
+
+int qfca_ritz(const double* h, int64_t batch, int32_t n, const double* x0, int32_t iters,
+              double* x, double* hm, void* stream) {
+    return counted(launch_ritz(h, batch, n, x0, iters, x, hm, S(stream)), 1);
 }
 
 int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw) {

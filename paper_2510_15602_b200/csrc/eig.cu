@@ -330,4 +330,227 @@ int launch_sym_eig(const double* h, int64_t batch, int p, double* evals, double*
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
+
+// ---------------------------------------------------------------- Ritz pairs of H
+// Top-p subspace of the small Lanczos projection H = B^T S B (n <= 128, p = 32)
+// in one CTA per image: X <- qr(H (H X)) for `iters` steps (m8n8k4 fp64 MMAs,
+// Gram + warp Cholesky + X R^-1), then Hm = X^T H X.  Same iteration as
+// features.topk_eigh on cov^2 (fifteen steps: (theta_33 / theta_10)^30 ~ 1e-16),
+// fused so that the small problem costs one launch instead of ~35.  H arrives
+// as lanczos.cu writes it (upper block triangle); X0 is the seeded start block.
+namespace {
+constexpr int RZ_P = 32;
+constexpr int RZ_MAXN = 128;
+constexpr int RZ_THREADS = 256;
+constexpr int RZ_NW = RZ_THREADS / 32;
+constexpr int RZ_XP = RZ_P + 4;  // padded pitch of the n x 32 blocks (conflict-free fragments)
+
+__device__ __forceinline__ void rz_dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// out (n x 32) = A (n x n, pitch ha) . X (n x 32, pitch RZ_XP); warp w owns row
+// tiles w and w + 8 (n = 128; fewer rows: tiles past n/8 idle) and all four
+// column tiles: eight independent accumulator chains per warp
+__device__ __forceinline__ void rz_mul(const double* A, int ha, const double* X, double* out,
+                                       int n, int warp, int lr, int lc) {
+    const int nt = n / 8;
+    const int r0 = warp, r1 = warp + RZ_NW;
+    const bool v0 = r0 < nt, v1 = r1 < nt;
+    double d[2][4][2] = {};
+    for (int k = 0; k < n; k += 4) {
+        double b[4];
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) b[ct] = X[(k + lc) * RZ_XP + ct * 8 + lr];
+        if (v0) {
+            const double a = A[(r0 * 8 + lr) * ha + k + lc];
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct) rz_dmma(d[0][ct][0], d[0][ct][1], a, b[ct]);
+        }
+        if (v1) {
+            const double a = A[(r1 * 8 + lr) * ha + k + lc];
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct) rz_dmma(d[1][ct][0], d[1][ct][1], a, b[ct]);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int rt = h ? r1 : r0;
+        if (h ? !v1 : !v0) continue;
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) {
+            out[(rt * 8 + lr) * RZ_XP + ct * 8 + 2 * lc] = d[h][ct][0];
+            out[(rt * 8 + lr) * RZ_XP + ct * 8 + 2 * lc + 1] = d[h][ct][1];
+        }
+    }
+}
+
+// G (32 x 32, pitch EIG_LD) = Y^T Z over n rows; warp w owns tiles 2w, 2w + 1,
+// each over two interleaved k halves (four independent chains)
+__device__ __forceinline__ void rz_gram(const double* Y, const double* Z, double* G, int n,
+                                        int warp, int lr, int lc) {
+    double d[2][2][2] = {};
+    const int t0 = 2 * warp;
+    for (int k = 0; k < n; k += 8) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int mt = (t0 + h) >> 2, ntl = (t0 + h) & 3;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int kk = k + 4 * s + lc;
+                rz_dmma(d[h][s][0], d[h][s][1], Y[kk * RZ_XP + mt * 8 + lr], Z[kk * RZ_XP + ntl * 8 + lr]);
+            }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int mt = (t0 + h) >> 2, ntl = (t0 + h) & 3;
+        G[(mt * 8 + lr) * EIG_LD + ntl * 8 + 2 * lc] = d[h][0][0] + d[h][1][0];
+        G[(mt * 8 + lr) * EIG_LD + ntl * 8 + 2 * lc + 1] = d[h][0][1] + d[h][1][1];
+    }
+}
+}  // namespace
+
+// Cholesky G = L L^T (32 x 32, G in shared memory, pitch EIG_LD) and
+// Ri = R^-1 = L^-T on one warp.  Lane i holds the trailing part of row i in
+// registers (shifted left every step, so no register array is indexed at run
+// time); column k of L goes through shared memory transposed (LT[k][i], rows
+// contiguous: one broadcast vector load per two entries) -- LT may alias G.
+// Lane c then forward-substitutes column c of L^-1, which is row c of R^-1.
+// One rsqrt per pivot; a pivot below 1e-28 of the trace leaves a zero column.
+__device__ __forceinline__ void rz_chol_rinv32(const double* G, double* LT, double* sD,
+                                               double (*Ri)[EIG_LD], int lane) {
+    double l[RZ_P];  // l[j] = G'[lane][k + j] at step k
+#pragma unroll
+    for (int j = 0; j < RZ_P; ++j) l[j] = G[lane * EIG_LD + j];
+    double tr = G[lane * EIG_LD + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    const double fl = 1e-300 + 1e-28 * tr;
+    __syncwarp();  // G fully read before LT overwrites it
+#pragma unroll 1
+    for (int k = 0; k < RZ_P; ++k) {
+        const double d = __shfl_sync(0xffffffffu, l[0], k);
+        const double rs = d > fl ? rsqrt(d) : 0.0;
+        double lk = 0.0;  // L[lane][k]
+        if (lane == k) {
+            lk = d * rs;
+            sD[k] = rs;
+        } else if (lane > k) {
+            lk = l[0] * rs;
+        }
+        LT[k * RZ_P + lane] = lk;
+        __syncwarp();
+        const double* col = LT + k * RZ_P;
+#pragma unroll
+        for (int j = 0; j < RZ_P - 1; ++j) {
+            // L[k+1+j][k]; entries past row 31 are never used (read col[31])
+            const int src = k + 1 + j < RZ_P ? k + 1 + j : RZ_P - 1;
+            l[j] = lane > k ? fma(-lk, col[src], l[j + 1]) : l[j + 1];
+        }
+        l[RZ_P - 1] = 0.0;
+    }
+    __syncwarp();
+    // x = column c of L^-1: x[r] = (delta_rc - sum_{m < r} L[r][m] x[m]) / L[r][r]
+    const int c = lane;
+#pragma unroll
+    for (int r = 0; r < RZ_P; ++r) {
+        double a0 = (r == c) ? 1.0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int m = 0; m < r; ++m) {
+            const double t = -LT[m * RZ_P + r] * l[m];  // L[r][m] x[m]
+            if ((m & 3) == 0) a0 += t;
+            else if ((m & 3) == 1) a1 += t;
+            else if ((m & 3) == 2) a2 += t;
+            else a3 += t;
+        }
+        l[r] = r < c ? 0.0 : ((a0 + a1) + (a2 + a3)) * sD[r];  // (l reused as x)
+    }
+    // Ri[c][q] = (R^-1)[c][q] = Linv[q][c] = x[q]
+#pragma unroll
+    for (int q = 0; q < RZ_P; ++q) Ri[c][q] = l[q];
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(RZ_THREADS, 1)
+k_ritz(const double* __restrict__ h, int n, const double* __restrict__ x0, int iters,
+       double* __restrict__ xout, double* __restrict__ hm) {
+    extern __shared__ __align__(16) double rz[];
+    const int hp = n + 4;  // Hs pitch: (4 lr + lc) mod 16 distinct -> conflict-free A fragments
+    double* const Hs = rz;                                          // n x hp
+    double* bufA = Hs + (size_t)n * hp;                             // n x RZ_XP
+    double* bufB = bufA + (size_t)n * RZ_XP;                        // n x RZ_XP
+    double(*G)[EIG_LD] = reinterpret_cast<double(*)[EIG_LD]>(bufB + (size_t)n * RZ_XP);
+    double(*Ri)[EIG_LD] = G + RZ_P;
+    double* sD = &Ri[RZ_P][0];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int lr = lane >> 2, lc = lane & 3;
+    const int64_t m = blockIdx.x;
+    const double* H = h + m * n * n;
+    for (int e = tid; e < n * n; e += RZ_THREADS) {
+        const int i = e / n, j = e % n;
+        Hs[i * hp + j] = i <= j ? H[i * n + j] : H[j * n + i];
+    }
+    for (int e = tid; e < n * RZ_P; e += RZ_THREADS) bufA[(e / RZ_P) * RZ_XP + e % RZ_P] = x0[e];
+    __syncthreads();
+    for (int it = 0; it < iters; ++it) {
+        rz_mul(Hs, hp, bufA, bufB, n, warp, lr, lc);  // T = H X
+        __syncthreads();
+        rz_mul(Hs, hp, bufB, bufA, n, warp, lr, lc);  // Y = H T
+        __syncthreads();
+        rz_gram(bufA, bufA, &G[0][0], n, warp, lr, lc);
+        __syncthreads();
+        if (warp == 0) rz_chol_rinv32(&G[0][0], &G[0][0], sD, Ri, lane);
+        __syncthreads();
+        // X = Y R^-1 -> bufB
+        for (int rt = warp; rt < n / 8; rt += RZ_NW) {
+            double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+            for (int k = 0; k < RZ_P; k += 4) {
+                const double a = bufA[(rt * 8 + lr) * RZ_XP + k + lc];
+#pragma unroll
+                for (int ct = 0; ct < 4; ++ct) rz_dmma(d[ct][0], d[ct][1], a, Ri[k + lc][ct * 8 + lr]);
+            }
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct) {
+                bufB[(rt * 8 + lr) * RZ_XP + ct * 8 + 2 * lc] = d[ct][0];
+                bufB[(rt * 8 + lr) * RZ_XP + ct * 8 + 2 * lc + 1] = d[ct][1];
+            }
+        }
+        __syncthreads();
+        double* t = bufA;
+        bufA = bufB;
+        bufB = t;
+    }
+    // Rayleigh-Ritz matrix Hm = X^T (H X)
+    rz_mul(Hs, hp, bufA, bufB, n, warp, lr, lc);
+    __syncthreads();
+    rz_gram(bufA, bufB, &G[0][0], n, warp, lr, lc);
+    __syncthreads();
+    for (int e = tid; e < RZ_P * RZ_P; e += RZ_THREADS) {
+        const int i = e / RZ_P, j = e % RZ_P;
+        hm[m * RZ_P * RZ_P + e] = 0.5 * (G[i][j] + G[j][i]);
+    }
+    for (int e = tid; e < n * RZ_P; e += RZ_THREADS)
+        xout[m * n * RZ_P + e] = bufA[(e / RZ_P) * RZ_XP + e % RZ_P];
+}
+
+size_t ritz_smem(int n) {
+    return ((size_t)n * (n + 4) + 2 * (size_t)n * RZ_XP + 2 * (size_t)RZ_P * EIG_LD + RZ_P) *
+           sizeof(double);
+}
+
+int launch_ritz(const double* h, int64_t batch, int n, const double* x0, int iters, double* xout,
+                double* hm, cudaStream_t st) {
+    if (batch <= 0 || n <= 0 || iters < 0) return QFCA_ERR_ARG;
+    if (n > RZ_MAXN || n % 8 || n < RZ_P) return QFCA_ERR_UNSUPPORTED;  // (n % 8: k steps of 8 in rz_gram)
+    const size_t smem = ritz_smem(n);
+    if (cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    k_ritz<<<(unsigned)batch, RZ_THREADS, smem, st>>>(h, n, x0, iters, xout, hm);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
 }  // namespace qfca

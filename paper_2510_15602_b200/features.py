@@ -233,7 +233,38 @@ def sym_eig(h: torch.Tensor):
     return w, v
 
 
-def topk_eigh(cov: torch.Tensor, k: int, block: int = 32, iters: int = 30):
+LANCZOS_BW, LANCZOS_PASSES = 8, 16  # csrc/lanczos.cu block width; passes over cov
+LANCZOS_DIM = LANCZOS_BW * LANCZOS_PASSES
+
+
+def _topk_eigh_lanczos(cov: torch.Tensor, k: int, block: int, iters: int):
+    """Block Lanczos (csrc/lanczos.cu: 16 passes of an 8-column block over cov,
+    full reorthogonalisation) -> the 128 x 128 projection H = B^T cov B, whose
+    top-k Ritz pairs come from the small-matrix path of topk_eigh below and map
+    back as V = B u (csrc/eig.cu k_ritz: the subspace iteration of this
+    function on the small matrix, one launch).  Same answer as the subspace iteration on cov (the Krylov
+    space holds the top-10 eigenvectors of the WRN50-2 covariances to ~1e-15,
+    tools/lanczos_proto.py) for ~1/8 of its passes over cov and no C^3 product."""
+    b, c, _ = cov.shape
+    n = LANCZOS_DIM
+    cov = cov.contiguous()
+    q0 = _start_block(c, LANCZOS_BW, cov.device).contiguous()
+    basis = empty((b, n, c), torch.float64)
+    h = empty((b, n, n), torch.float64)
+    N.call("qfca_lanczos", cov.data_ptr(), b, c, LANCZOS_PASSES, q0.data_ptr(),
+           basis.data_ptr(), h.data_ptr(), N.stream())
+    p = 32
+    x0 = _start_block(n, p, cov.device).contiguous()
+    x = empty((b, n, p), torch.float64)
+    hm = empty((b, p, p), torch.float64)
+    N.call("qfca_ritz", h.data_ptr(), b, n, x0.data_ptr(), (iters + 1) // 2, x.data_ptr(),
+           hm.data_ptr(), N.stream())
+    w, u = sym_eig(hm)
+    return w[..., :k], basis.mT @ (x @ u[..., :k])
+
+
+def topk_eigh(cov: torch.Tensor, k: int, block: int = 32, iters: int = 30,
+              lanczos: bool = True):
     """Top-k eigenpairs of a batch of symmetric PSD matrices (B, C, C), fp64.
 
     Replaces the full ``np.linalg.eigh`` of features.py:173 (only the top-k
@@ -251,6 +282,8 @@ def topk_eigh(cov: torch.Tensor, k: int, block: int = 32, iters: int = 30):
     p = min(c, max(block, k))
     if p > 32:
         return _topk_eigh_torch(cov, k, p, iters)
+    if lanczos and k <= 16 and c >= 2 * LANCZOS_DIM and c <= 512 and c % 64 == 0:
+        return _topk_eigh_lanczos(cov, k, block, iters)
     if p == c:
         w, u = sym_eig(cov)
         return w[..., :k], u[..., :k]
