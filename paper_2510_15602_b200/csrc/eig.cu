@@ -434,7 +434,7 @@ __device__ __forceinline__ void rz_chol_rinv32(const double* G, double* LT, doub
     for (int k = 0; k < RZ_P; ++k) {
         const double d = __shfl_sync(0xffffffffu, l[0], k);
         const double rs = d > fl ? rsqrt(d) : 0.0;
-        double lk = 0.0;  // L[lane][k]
+        double lk = 0.0;  // L[lane][k] (0 above the diagonal)
         if (lane == k) {
             lk = d * rs;
             sD[k] = rs;
@@ -443,13 +443,13 @@ __device__ __forceinline__ void rz_chol_rinv32(const double* G, double* LT, doub
         }
         LT[k * RZ_P + lane] = lk;
         __syncwarp();
-        const double* col = LT + k * RZ_P;
+        // trailing update + shift: l[j] <- G'[lane][k+1+j] - L[lane][k] L[k+1+j][k].
+        // Lanes < k have lk = 0 (no change); lane k's row is final and no longer
+        // read.  Entries k+1+j > 31 read on into the next LT rows / the rest of
+        // the G area (finite values) and only feed columns past 31, never used.
+        const double* col = LT + k * RZ_P + k + 1;
 #pragma unroll
-        for (int j = 0; j < RZ_P - 1; ++j) {
-            // L[k+1+j][k]; entries past row 31 are never used (read col[31])
-            const int src = k + 1 + j < RZ_P ? k + 1 + j : RZ_P - 1;
-            l[j] = lane > k ? fma(-lk, col[src], l[j + 1]) : l[j + 1];
-        }
+        for (int j = 0; j < RZ_P - 1; ++j) l[j] = fma(-lk, col[j], l[j + 1]);
         l[RZ_P - 1] = 0.0;
     }
     __syncwarp();

@@ -6,10 +6,11 @@
 // window counts of the whole channel batch fit in shared memory, so each
 // channel batch runs as
 //
-//   pass 0  producers (4 warps) slide the vertical windows (H1) into a double
-//           buffer; consumers (12 warps) form the row windows (H2) and store
-//           the cumulative counts of every pixel, pixel-major (one uint4 = 16
-//           8-bit thermometer lanes per pixel) -> SA4;
+//   pass 0  all warps: vertical windows (H1, four threads per column, each
+//           sliding over a quarter of the rows) into SA4 in place, then the
+//           row windows (H2) over 2T staged rows at a time -> the cumulative
+//           counts of every pixel, pixel-major (one uint4 = 16 8-bit
+//           thermometer lanes per pixel) in SA4;
 //   search  all 16 warps: the median-quan reference V_i of all 16 bins at once
 //           -- a lock-step binary search whose counting pass compares the 16
 //           lanes of each SA4 word against 16 packed thresholds
@@ -35,16 +36,14 @@
 namespace qfca {
 
 // A CTA covers NCOL = CPB * W columns (CPB channel slots of width W) with
-// 4 * NCOL threads -- one per (slot, bin group, column) in pass 1.  In pass 0
-// the last NCOL threads are the producers (H1, one per column) and the rest
-// the consumers (H2); the search, the tables and pass 1 use all of them.
+// 4 * NCOL threads -- one per (slot, bin group, column) in pass 1; every phase
+// uses all of them.
 // NCOL = 64 (256 threads, <= 113 KB) keeps two CTAs resident per SM, so one
 // CTA's barrier-bound phases overlap the other's transport; NCOL = 128 (512
-// threads) takes wider planes.
+// threads) takes wider planes.  (Pass 0 uses all 4 NCOL threads: 4 per column
+// in H1, SEG-column tasks in H2.)
 constexpr int S4_SMEM_MAX = 227 * 1024;
 constexpr int S4_SMEM_2CTA = 113 * 1024;
-// named barriers of the pass-0 pipeline (0 is __syncthreads)
-constexpr int S4_FULL0 = 3, S4_EMPTY0 = 5;
 
 struct Score4Geom {
     int h, n_bins, pad, C, groups, cpg;
@@ -59,12 +58,6 @@ struct Score4Geom {
     int a_chp, a_th, a_cnt, a_qm, a_lo, a_hi, a_pj;
 };
 
-__device__ __forceinline__ void bar_sync4(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive4(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ float rcp_approx4(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -124,7 +117,7 @@ static void score4_layout(Score4Geom& g) {
         a = (int)((a + bytes + 15) & ~15LL);
         return o;
     };
-    g.a_chp = atake((long long)2 * T * CPB * g.WPP * 16);
+    g.a_chp = atake((long long)2 * T * CPB * g.WPP * 16);  // pass-0 H2 staging: 2T padded rows
     g.a_th = atake(256 * 16);
     const int pass0 = a;
     a = 0;
@@ -148,7 +141,6 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
          const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score4Geom g,
          float* __restrict__ partial) {
     constexpr int S4_THREADS = 4 * NCOL;
-    constexpr int S4_CT = S4_THREADS - NCOL;  // pass-0 consumers; the last NCOL threads produce
     constexpr int R = T / 2;
     constexpr int T2 = T * T;
     constexpr int GP = T2 + 1;     // G-table length per bin
@@ -179,14 +171,12 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     float* const Vb = reinterpret_cast<float*>(al);
 
     const int tid = threadIdx.x;
-    const bool is_p = tid >= S4_CT;
     const int h = g.h;
     const int hw = h * W;
     const int img = blockIdx.x / g.groups, cgi = blockIdx.x % g.groups;
     const int c_begin = cgi * g.cpg, c_end = min(g.C, c_begin + g.cpg);
     float* const part = partial + ((int64_t)img * g.groups + cgi) * hw;
     const int n_chunks = (g.S + T - 1) / T;
-    const int CHSTRIDE = T * CPB * g.WPP;  // uint4 per CHp buffer
 
     // ---- per-CTA tables: padded-x map, pass-1 row map, pass-0 slide rows
     for (int p = tid; p < W + 2 * R; p += S4_THREADS) xmap[p] = map_coord(p - R, W, g.pad);
@@ -198,99 +188,12 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                                      map_coord(e - 1 - R, h, g.pad) * W);
     __syncthreads();
 
-    // ---- producer role (pass 0): thread (slot pcs, column px)
-    const int pt = tid - S4_CT;
-    const int px = pt % W, pcs = is_p ? pt / W : 0;
-    int halo0 = -1, halo1 = -1;
-    if (is_p) {
-        for (int j = 0; j < 2 * R; ++j) {
-            const int p = j < R ? j : W + j;
-            if (xmap[p] == px) {
-                if (halo0 < 0) halo0 = p;
-                else if (halo1 < 0) halo1 = p;
-            }
-        }
-    }
-    const bool many_halo = W <= R;
-    const uint8_t* const pbx = sb + pcs * hw + px;
-
     // ---- pass-1 role: thread (slot cs, group grp, column x)
     const int cs = tid / (4 * W);
     const int grp = (tid / W) & 3;
     const int grp4 = grp * 4;
     const bool g1 = (grp & 1) != 0, g2 = (grp & 2) != 0;
     const int x = tid % W;
-
-    // H1 (producers): vertical windows of pass-0 chunk c -> CHp[c & 1]
-    uint4 cst = make_uint4(0, 0, 0, 0);
-    auto h1_chunk = [&](int c) {
-        uint4* base = CHp + (c & 1) * CHSTRIDE + pcs * g.WPP;
-#pragma unroll
-        for (int rho = 0; rho < T; ++rho) {
-            const int e = c * T + rho;
-            if (e >= h) break;
-            if (e == 0) {
-                cst = make_uint4(0, 0, 0, 0);
-#pragma unroll 1
-                for (int dy = -R; dy <= R; ++dy) {
-                    const uint4 a = TH[pbx[map_coord(dy, h, g.pad) * W]];
-                    cst.x += a.x;
-                    cst.y += a.y;
-                    cst.z += a.z;
-                    cst.w += a.w;
-                }
-            } else {
-                const int2 st = stab[e];
-                const uint4 a = TH[pbx[st.x]], r = TH[pbx[st.y]];
-                cst.x += a.x - r.x;
-                cst.y += a.y - r.y;
-                cst.z += a.z - r.z;
-                cst.w += a.w - r.w;
-            }
-            uint4* row = base + rho * CPB * g.WPP;
-            row[px + R] = cst;
-            if (halo0 >= 0) row[halo0] = cst;
-            if (halo1 >= 0) row[halo1] = cst;
-            if (many_halo) {
-                for (int j = 0; j < 2 * R; ++j) {
-                    const int p = j < R ? j : W + j;
-                    if (xmap[p] == px) row[p] = cst;
-                }
-            }
-        }
-    };
-    // H2 (consumers): CHp[c & 1] -> SA4 rows of pass-0 chunk c
-    auto h2_chunk = [&](int c) {
-        for (int task = tid; task < T * CPB * NSEG; task += S4_CT) {
-            const int rc = task / NSEG;  // rho * CPB + slot
-            const int x0 = (task - rc * NSEG) * SEG;
-            const int e = c * T + rc / CPB;
-            if (e >= h) continue;
-            const uint4* src = CHp + (c & 1) * CHSTRIDE + rc * g.WPP + x0;
-            uint4* dst = SA4 + ((rc % CPB) * h + e) * W + x0;
-            uint4 sum = make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int p = 0; p < T; ++p) {
-                const uint4 v = src[p];
-                sum.x += v.x;
-                sum.y += v.y;
-                sum.z += v.z;
-                sum.w += v.w;
-            }
-            dst[0] = sum;
-            const int n = x0 + SEG <= W ? SEG : W - x0;
-#pragma unroll
-            for (int k = 1; k < SEG; ++k) {
-                if (k >= n) break;
-                const uint4 a = src[k + 2 * R], r = src[k - 1];
-                sum.x += a.x - r.x;
-                sum.y += a.y - r.y;
-                sum.z += a.z - r.z;
-                sum.w += a.w - r.w;
-                dst[k] = sum;
-            }
-        }
-    };
 
     for (int cb = c_begin; cb < c_end; cb += CPB) {
         // ---- load the slot channels (all warps)
@@ -329,22 +232,79 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         }
         __syncthreads();
 
-        // ---- pass 0: window counts of every pixel -> SA4
-        if (is_p) {
-            for (int c = 0; c < g.n0; ++c) {
-                const int b = c & 1;
-                if (c >= 2) bar_sync4(S4_EMPTY0 + b, S4_THREADS);
-                h1_chunk(c);
-                bar_arrive4(S4_FULL0 + b, S4_THREADS);
-            }
-        } else {
-            for (int c = 0; c < g.n0; ++c) {
-                bar_sync4(S4_FULL0 + (c & 1), S4_THREADS);
-                h2_chunk(c);
-                if (c + 2 < g.n0) bar_arrive4(S4_EMPTY0 + (c & 1), S4_THREADS);
+        // ---- pass 0: window counts of every pixel -> SA4, all warps.
+        // (a) vertical windows (H1): four threads per column, each sliding over a
+        //     quarter of the rows (one T-row start-up per quarter) -> SA4 in place
+        {
+            const int col = tid % NCOL, q = tid / NCOL;
+            const int slot = col / W, x = col % W;
+            const int y0 = q * h / 4, y1 = (q + 1) * h / 4;
+            const uint8_t* pb = sb + slot * hw + x;
+            uint4* dst = SA4 + slot * hw + x;
+            if (y0 < y1) {
+                uint4 cst = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+                for (int dy = -R; dy <= R; ++dy) {
+                    const uint4 a = TH[pb[map_coord(y0 + dy, h, g.pad) * W]];
+                    cst.x += a.x;
+                    cst.y += a.y;
+                    cst.z += a.z;
+                    cst.w += a.w;
+                }
+                dst[y0 * W] = cst;
+                for (int y = y0 + 1; y < y1; ++y) {
+                    const int2 st = stab[y];
+                    const uint4 a = TH[pb[st.x]], r = TH[pb[st.y]];
+                    cst.x += a.x - r.x;
+                    cst.y += a.y - r.y;
+                    cst.z += a.z - r.z;
+                    cst.w += a.w - r.w;
+                    dst[y * W] = cst;
+                }
             }
         }
         __syncthreads();
+        // (b) row windows (H2), 2T rows at a time: copy the rows with their padded
+        //     halo into CHp, then sliding sums over segments of SEG columns -> SA4
+        for (int yb = 0; yb < h; yb += 2 * T) {
+            const int nr = min(2 * T, h - yb);
+            constexpr int PW = W + 2 * R;
+            for (int idx = tid; idx < nr * CPB * PW; idx += S4_THREADS) {
+                const int rc = idx / PW, pp = idx - rc * PW;  // rc = r * CPB + slot
+                const int r = rc / CPB, slot = rc - r * CPB;
+                CHp[rc * g.WPP + pp] = SA4[(slot * h + yb + r) * W + xmap[pp]];
+            }
+            __syncthreads();
+            for (int task = tid; task < nr * CPB * NSEG; task += S4_THREADS) {
+                const int rc = task / NSEG;
+                const int x0 = (task - rc * NSEG) * SEG;
+                const int r = rc / CPB, slot = rc - r * CPB;
+                const uint4* src = CHp + rc * g.WPP + x0;
+                uint4* dst = SA4 + (slot * h + yb + r) * W + x0;
+                uint4 sum = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int pq = 0; pq < T; ++pq) {
+                    const uint4 v = src[pq];
+                    sum.x += v.x;
+                    sum.y += v.y;
+                    sum.z += v.z;
+                    sum.w += v.w;
+                }
+                dst[0] = sum;
+                const int nn = x0 + SEG <= W ? SEG : W - x0;
+#pragma unroll
+                for (int k = 1; k < SEG; ++k) {
+                    if (k >= nn) break;
+                    const uint4 a = src[k + 2 * R], rr = src[k - 1];
+                    sum.x += a.x - rr.x;
+                    sum.y += a.y - rr.y;
+                    sum.z += a.z - rr.z;
+                    sum.w += a.w - rr.w;
+                    dst[k] = sum;
+                }
+            }
+            __syncthreads();
+        }
 
         if (g.fref) {
             // ---- reference: smallest v with #{samples: A_i <= v} >= S - m, all bins at once
