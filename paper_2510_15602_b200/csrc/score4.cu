@@ -121,7 +121,7 @@ static void score4_layout(Score4Geom& g) {
     g.a_th = atake(256 * 16);
     const int pass0 = a;
     a = 0;
-    g.a_cnt = atake((long long)2 * CPB * 8 * 4);
+    g.a_cnt = atake((long long)(4 * NCOL / 32) * 8 * 4);  // per-warp search counts
     g.a_qm = atake((long long)CPB * 16);
     g.a_lo = atake((long long)CPB * 16 * 4);
     g.a_hi = atake((long long)CPB * 16 * 4);
@@ -316,13 +316,12 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 bhi[tid] = T2;
                 qm8[tid] = (uint8_t)((top + T2) >> 1);
             }
-            for (int i = tid; i < 2 * CPB * 8; i += S4_THREADS) cnt[i] = 0;
             __syncthreads();
             const int k = tid / TPS, lt = tid - k * TPS;
+            constexpr int WPS = TPS / 32;  // search warps per slot
             const uint4* sa = SA4 + (size_t)k * g.nsamp;
 #pragma unroll 1
             for (int r = 0; r < ROUNDS; ++r) {
-                const int par = r & 1;
                 uint32_t Q[4], acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) Q[q] = 0x80808080u | qm[k * 4 + q];
@@ -333,20 +332,23 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     acc[2] += __umulhi((Q[2] - v.z) & 0x80808080u, 1u << 25);
                     acc[3] += __umulhi((Q[3] - v.w) & 0x80808080u, 1u << 25);
                 }
-                uint32_t* cp = cnt + (par * CPB + k) * 8;
+                // per-warp sums of the 16-bit count fields (no shared atomics)
+                uint32_t* cp = cnt + (tid >> 5) * 8;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t ev = __reduce_add_sync(0xffffffffu, acc[q] & 0x00FF00FFu);
                     const uint32_t od = __reduce_add_sync(0xffffffffu, (acc[q] >> 8) & 0x00FF00FFu);
                     if ((tid & 31) == 0) {
-                        atomicAdd(cp + 2 * q, ev);
-                        atomicAdd(cp + 2 * q + 1, od);
+                        cp[2 * q] = ev;
+                        cp[2 * q + 1] = od;
                     }
                 }
                 __syncthreads();
                 if (tid < CPB * 16) {
                     const int kk = tid >> 4, i = tid & 15, j = i & 3, q = i >> 2;
-                    const uint32_t word = cnt[(par * CPB + kk) * 8 + 2 * q + (j & 1)];
+                    uint32_t word = 0;  // fields stay < 65536: nsamp < 65536
+#pragma unroll
+                    for (int w = 0; w < WPS; ++w) word += cnt[(kk * WPS + w) * 8 + 2 * q + (j & 1)];
                     const int count = (int)((j >> 1) ? word >> 16 : word & 0xFFFFu);
                     int a = blo[tid], bnd = bhi[tid];
                     const int mid = (a + bnd) >> 1;
@@ -355,7 +357,6 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     bhi[tid] = bnd;
                     qm8[tid] = (uint8_t)((a + bnd) >> 1);
                 }
-                for (int i = tid; i < CPB * 8; i += S4_THREADS) cnt[((par ^ 1) * CPB) * 8 + i] = 0;
                 __syncthreads();
             }
             if (tid < CPB * 16) sV[tid] = blo[tid];
