@@ -94,7 +94,7 @@ static void score3_layout(Score3Geom& g) {
     g.o_scale = take((long long)CPB * 4);
     g.o_th = take((long long)256 * 16);
     g.o_sv = take((long long)CPB * 16 * 4);
-    g.o_srch = take(1024);  // search counters, packed mids, brackets
+    g.o_srch = take(1024 + (S3_THREADS / 32) * 32);  // search brackets, packed mids, per-warp counts
     g.total = off;
 }
 
@@ -124,7 +124,7 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     uint4* const TH = reinterpret_cast<uint4*>(sm + g.o_th);
     int* const sV = reinterpret_cast<int*>(sm + g.o_sv);
     uint4* const SA4 = reinterpret_cast<uint4*>(sm + g.o_sa);  // [CPB][nsamp] sample windows
-    uint32_t* const scnt = reinterpret_cast<uint32_t*>(sm + g.o_srch);        // [2][CPB][8]
+    uint32_t* const scnt = reinterpret_cast<uint32_t*>(sm + g.o_srch + 1024); // [warps][8]
     uint8_t* const sqm8 = sm + g.o_srch + 256;                                 // [CPB][16]
     int* const sblo = reinterpret_cast<int*>(sm + g.o_srch + 320);            // [CPB * 16]
     int* const sbhi = reinterpret_cast<int*>(sm + g.o_srch + 576);            // [CPB * 16]
@@ -351,14 +351,13 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     sbhi[tid] = T2;
                     sqm8[tid] = (uint8_t)((top + T2) >> 1);
                 }
-                for (int i = tid; i < 2 * CPB * 8; i += S3_THREADS) scnt[i] = 0;
                 __syncthreads();
                 const int k = tid / TPS, lt = tid - k * TPS, lane = tid & 31;
+                constexpr int WPS = TPS / 32;  // search warps per slot
                 const uint4* sa = SA4 + (size_t)k * g.nsamp;
                 const uint32_t* sqm = reinterpret_cast<const uint32_t*>(sqm8);
 #pragma unroll 1
                 for (int r = 0; r < ROUNDS; ++r) {
-                    const int par = r & 1;
                     uint32_t Q[4], acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) Q[q] = 0x80808080u | sqm[k * 4 + q];
@@ -369,21 +368,24 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         acc[2] += __umulhi((Q[2] - v.z) & 0x80808080u, 1u << 25);
                         acc[3] += __umulhi((Q[3] - v.w) & 0x80808080u, 1u << 25);
                     }
-                    uint32_t* cp = scnt + (par * CPB + k) * 8;
+                    // per-warp sums of the 16-bit count fields (no shared atomics)
+                    uint32_t* cp = scnt + (tid >> 5) * 8;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint32_t ev = __reduce_add_sync(0xffffffffu, acc[q] & 0x00FF00FFu);
                         const uint32_t od =
                             __reduce_add_sync(0xffffffffu, (acc[q] >> 8) & 0x00FF00FFu);
                         if (lane == 0) {
-                            atomicAdd(cp + 2 * q, ev);
-                            atomicAdd(cp + 2 * q + 1, od);
+                            cp[2 * q] = ev;
+                            cp[2 * q + 1] = od;
                         }
                     }
                     __syncthreads();
                     if (tid < CPB * 16) {
                         const int kk = tid >> 4, i = tid & 15, j = i & 3, q = i >> 2;
-                        const uint32_t word = scnt[(par * CPB + kk) * 8 + 2 * q + (j & 1)];
+                        uint32_t word = 0;  // fields stay < 65536: nsamp < 65536
+#pragma unroll
+                        for (int w = 0; w < WPS; ++w) word += scnt[(kk * WPS + w) * 8 + 2 * q + (j & 1)];
                         const int count = (int)((j >> 1) ? word >> 16 : word & 0xFFFFu);
                         int a = sblo[tid], bnd = sbhi[tid];
                         const int mid = (a + bnd) >> 1;
@@ -392,8 +394,6 @@ k_score3(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         sbhi[tid] = bnd;
                         sqm8[tid] = (uint8_t)((a + bnd) >> 1);
                     }
-                    for (int i = tid; i < CPB * 8; i += S3_THREADS)
-                        scnt[((par ^ 1) * CPB) * 8 + i] = 0;
                     __syncthreads();
                 }
                 if (tid < CPB * 16) sV[tid] = sblo[tid];
