@@ -13,7 +13,7 @@
 // (warp w: rows 64w .. 64w+63, eight 8 x 8 tiles):
 //
 //   S pass    W = S Q_j     (S symmetric, so A = S^T tiles come straight from
-//             rows of S; the rows stream through a 3-stage cp.async.bulk +
+//             rows of S; the rows stream through a 5-stage cp.async.bulk +
 //             mbarrier ring fed by a producer warp, 8 rows of S per stage,
 //             further chunks prefetched into L2)
 //   H column  c1 = B^T W over the basis B = [Q_0 .. Q_j], the basis blocks
@@ -41,7 +41,7 @@ constexpr int LZ_CTA = LZ_THREADS + 32;  // + one producer warp (ring refills)
 constexpr int LZ_MAXC = 64 * LZ_NW;
 constexpr int LZ_RT = 8;         // max 8-row tiles per warp
 constexpr int LZ_KC = 8;         // rows per ring chunk
-constexpr int LZ_NST = 3;        // ring stages
+constexpr int LZ_NST = 5;        // ring stages
 constexpr int LZ_MAXP = 32;      // passes (n = 8 P <= 256)
 constexpr int LZ_PF = 6;         // S chunks prefetched into L2 beyond the ring
 
@@ -106,8 +106,8 @@ __host__ __device__ inline LzSmem lz_layout(int C, int n) {
     off += C * LZ_BW * 8;
     L.o_cf = off;
     off += n * LZ_BW * 8;
-    L.o_part = off;  // [P][warps][64] MMA partials of one sweep, reduced over the warps
-    off += (n / LZ_BW) * LZ_NW * 64 * 8;
+    L.o_part = off;  // [2][warps][64] MMA partials, reduced over the warps per block
+    off += 2 * LZ_NW * 64 * 8;
     L.o_g = off;     // Gram / L | R^-1 | 1 / diag(L)
     off += (2 * LZ_BW * LZ_BW + LZ_BW) * 8;
     L.total = off;
@@ -127,6 +127,7 @@ __host__ __device__ inline int lz_pass_chunks(int C, int P, int j) {
     return C / LZ_KC + nsweep * nb;
 }
 
+template <int NT>  // 8-row tiles per warp: C = 64 NT
 __global__ void __launch_bounds__(LZ_CTA, 1)
 k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__ Q0,
           double* __restrict__ Bm, double* __restrict__ H) {
@@ -188,8 +189,8 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
     }
 
     // ---------------- consumers (8 warps)
-    const int wrows = C / LZ_NW;  // rows per warp (multiple of 8)
-    const int ntile = wrows / 8;
+    constexpr int ntile = NT;
+    const int wrows = 8 * NT;  // rows per warp
     const int wr0 = warp * wrows;
     uint32_t consumed = 0;
     auto acquire = [&]() -> const double* {
@@ -204,11 +205,10 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
     };
 
     // W tiles: acc[t] = W[wr0 + 8t + lr][2 lc + {0, 1}]
-    double acc[LZ_RT][2];
+    double acc[NT][2];
     auto store_w = [&]() {  // acc -> Ws (row-major C x 8)
 #pragma unroll
-        for (int t = 0; t < LZ_RT; ++t)
-            if (t < ntile)
+        for (int t = 0; t < NT; ++t)
                 *reinterpret_cast<double2*>(Ws + (wr0 + 8 * t + lr) * LZ_BW + 2 * lc) =
                     make_double2(acc[t][0], acc[t][1]);
     };
@@ -220,7 +220,7 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
         // range(S): zero rows of S (all-zero channels) stay exact zeros in every
         // Ritz vector, as with the subspace iteration.
 #pragma unroll
-        for (int t = 0; t < LZ_RT; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
         for (int c = 0; c < nS; ++c) {
             const double* st = acquire();
 #pragma unroll
@@ -228,8 +228,8 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
                 const double b = Ws[(c * LZ_KC + 4 * ks + lc) * LZ_BW + lr];  // Q[k][q]
                 const double* arow = st + (4 * ks + lc) * CP + wr0 + lr;      // S[k][r]
 #pragma unroll
-                for (int t = 0; t < LZ_RT; ++t)
-                    if (t < ntile) lz_dmma(acc[t][0], acc[t][1], arow[8 * t], b);
+                for (int t = 0; t < NT; ++t)
+                    lz_dmma(acc[t][0], acc[t][1], arow[8 * t], b);
             }
             release();
         }
@@ -248,17 +248,19 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
                     lz_dmma(d0, d1, st[lr * CP + r], Ws[r * LZ_BW + lr]);
                 }
                 release();
-                double* pp = part + (i * LZ_NW + warp) * 64 + lr * 8 + 2 * lc;
+                double* pp = part + ((i & 1) * LZ_NW + warp) * 64 + lr * 8 + 2 * lc;
                 pp[0] = d0;
                 pp[1] = d1;
-            }
-            lz_csync();
-            for (int e = tid; e < nb * 64; e += LZ_THREADS) {
-                const double* src = part + (e / 64) * LZ_NW * 64 + (e % 64);
-                double a = 0.0;
+                // block i's partials complete (and block i-2's reduction done, so
+                // its half of the double buffer is free again)
+                lz_csync();
+                if (tid < 64) {
+                    const double* src = part + (i & 1) * LZ_NW * 64 + tid;
+                    double a = 0.0;
 #pragma unroll
-                for (int ww = 0; ww < LZ_NW; ++ww) a += src[ww * 64];
-                cf[e] = a;
+                    for (int ww = 0; ww < LZ_NW; ++ww) a += src[ww * 64];
+                    cf[i * 64 + tid] = a;
+                }
             }
             lz_csync();
         };
@@ -271,8 +273,8 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
                     const double b = -cf[(i * LZ_BW + 4 * ks + lc) * LZ_BW + lr];  // -cf[c][q]
                     const double* arow = st + (4 * ks + lc) * CP + wr0 + lr;       // B_i[c][r]
 #pragma unroll
-                    for (int t = 0; t < LZ_RT; ++t)
-                        if (t < ntile) lz_dmma(acc[t][0], acc[t][1], arow[8 * t], b);
+                    for (int t = 0; t < NT; ++t)
+                        lz_dmma(acc[t][0], acc[t][1], arow[8 * t], b);
                 }
                 release();
             }
@@ -365,15 +367,13 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
             lz_csync();
             // W <- W R^-1 on the MMAs (A = W tiles from Ws, B = R^-1)
 #pragma unroll
-            for (int t = 0; t < LZ_RT; ++t) acc[t][0] = acc[t][1] = 0.0;
+            for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
                 const double b = Ri[(4 * ks + lc) * LZ_BW + lr];
 #pragma unroll
-                for (int t = 0; t < LZ_RT; ++t)
-                    if (t < ntile)
-                        lz_dmma(acc[t][0], acc[t][1], Ws[(wr0 + 8 * t + lr) * LZ_BW + 4 * ks + lc],
-                                b);
+                for (int t = 0; t < NT; ++t)
+                    lz_dmma(acc[t][0], acc[t][1], Ws[(wr0 + 8 * t + lr) * LZ_BW + 4 * ks + lc], b);
             }
         }
         // ---------------- Q_{j+1} -> shared (next S pass) and global (later sweeps,
@@ -382,12 +382,10 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
         lz_csync();
         store_w();
 #pragma unroll
-        for (int t = 0; t < LZ_RT; ++t) {
-            if (t < ntile) {
-                const int r = wr0 + 8 * t + lr;
-                Bi[(size_t)(cols + 2 * lc) * C + r] = acc[t][0];
-                Bi[(size_t)(cols + 2 * lc + 1) * C + r] = acc[t][1];
-            }
+        for (int t = 0; t < NT; ++t) {
+            const int r = wr0 + 8 * t + lr;
+            Bi[(size_t)(cols + 2 * lc) * C + r] = acc[t][0];
+            Bi[(size_t)(cols + 2 * lc + 1) * C + r] = acc[t][1];
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
         lz_csync();
@@ -402,10 +400,21 @@ int launch_lanczos(const double* S, int64_t batch, int C, int P, const double* Q
     if (C > LZ_MAXC || C % 64 || P > LZ_MAXP || P * LZ_BW > C) return QFCA_ERR_UNSUPPORTED;
     const size_t smem = lanczos_smem(C, P);
     if (smem > 227 * 1024) return QFCA_ERR_UNSUPPORTED;
-    if (cudaFuncSetAttribute(k_lanczos, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    void (*kern)(const double*, int, int, const double*, double*, double*) = nullptr;
+    switch (C / 64) {
+        case 1: kern = k_lanczos<1>; break;
+        case 2: kern = k_lanczos<2>; break;
+        case 3: kern = k_lanczos<3>; break;
+        case 4: kern = k_lanczos<4>; break;
+        case 5: kern = k_lanczos<5>; break;
+        case 6: kern = k_lanczos<6>; break;
+        case 7: kern = k_lanczos<7>; break;
+        default: kern = k_lanczos<8>; break;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return QFCA_ERR_CUDA;
-    k_lanczos<<<(unsigned)batch, LZ_CTA, smem, st>>>(S, C, P, Q0, Bm, H);
+    kern<<<(unsigned)batch, LZ_CTA, smem, st>>>(S, C, P, Q0, Bm, H);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
