@@ -9,6 +9,16 @@
   used channels -- combines them; every rank then finalises (channel mean,
   Gaussian, image score) identically.  NCCL over NVLink in production, gloo
   in the CPU tests.
+
+Feature planes wider than the fused kernels' 128 columns (configs[4]: 1024 x
+1024 per channel) are scored in full-height column strips of 128 (``strips``):
+strip s covers columns [a_s, a_s + 128) and owns the outputs more than 2R
+columns from its inner edges (an output needs E within R, E needs bins within
+R), so the strips' own border padding never reaches an owned output; the true
+image borders are strip borders and keep the reference's reflect padding.  The
+median-quan reference of each channel comes from the whole plane (K3), so every
+strip scores against the same reference; the strips run as one batched launch
+of the plane-width-128 fused kernel.
 """
 
 from __future__ import annotations
@@ -21,7 +31,31 @@ from .features import _gauss_kernel, sep_convolve_dev
 from .quantize import bins_dev, minmax_dev
 
 __all__ = ["shard_range", "shard_batch", "combine_partials", "channel_partial",
-           "detect_channel_sharded"]
+           "detect_channel_sharded", "strips"]
+
+STRIP_W = 128  # widest plane of the fused kernels
+USE_STRIPS = True  # route wide planes through strips (False: whole-plane generic kernel)
+
+
+def strips(w: int, t: int, sw: int = STRIP_W):
+    """Column strips for a plane of width w > sw and patch size t (reflect pad):
+    returns (starts, owner strip per column, local column per column)."""
+    import numpy as np
+    halo = 2 * (t // 2)
+    step = sw - 2 * halo
+    if w <= sw or step <= 0:
+        raise ValueError("strips need w > strip width > 4 (T // 2)")
+    starts = [0]
+    while starts[-1] + sw < w:
+        starts.append(min(starts[-1] + step, w - sw))
+    owner = np.empty(w, np.int64)
+    x = 0
+    for s_, a in enumerate(starts):
+        hi = w if s_ == len(starts) - 1 else a + sw - halo
+        owner[x:hi] = s_
+        x = max(x, hi)
+    local = np.arange(w) - np.asarray(starts)[owner]
+    return starts, owner, local
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -70,6 +104,10 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
                                  cfg.sample_budget, 0)
     ref = None
+    if (USE_STRIPS and w > STRIP_W and cfg.pad == "reflect" and bins.element_size() == 1
+            and L.qfca_score_groups(h, STRIP_W, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                    cfg.sample_budget, 1) > 0):
+        return _strip_partial(bins, lo, hi, cfg, c, h, w), _used(lo, hi, c)
     if groups <= 0:  # kernel without in-kernel reference selection: run K3 first
         groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
                                      cfg.sample_budget, 1)
@@ -88,6 +126,46 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     N.call("qfca_reduce_partials", partial.data_ptr(), 1, groups, hw, ones.data_ptr(),
            acc.data_ptr(), s)
     return acc.reshape(h, w), int(used[0])
+
+
+def _used(lo, hi, c) -> int:
+    used = empty((1,), torch.int32)
+    N.call("qfca_count_used", lo.data_ptr(), hi.data_ptr(), 1, c, used.data_ptr(), N.stream())
+    return int(used[0])
+
+
+def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
+    """Channel-sum map (h, w) fp64 of a wide plane from 128-column strips."""
+    s = N.stream()
+    pad = N.PAD_CODES[cfg.pad]
+    starts, owner, local = strips(w, cfg.patch_size)
+    ns = len(starts)
+    ref = empty((c, cfg.n_bins), torch.int32)  # whole-plane reference (K3)
+    N.call("qfca_select_reference", bins.data_ptr(), bins.element_size(), lo.data_ptr(),
+           hi.data_ptr(), c, h, w, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, 0,
+           ref.data_ptr(), s)
+    b3 = bins.view(c, h, w)
+    sb = torch.stack([b3[:, :, a:a + STRIP_W] for a in starts]).contiguous()  # (ns, c, h, 128)
+    lo_r = lo.repeat(ns).contiguous()
+    hi_r = hi.repeat(ns).contiguous()
+    ref_r = ref.repeat(ns, 1).contiguous()
+    L = N.lib()
+    groups = L.qfca_score_groups(h, STRIP_W, cfg.n_bins, cfg.patch_size, c, ns, 0, pad,
+                                 cfg.sample_budget, 1)
+    if groups <= 0:
+        raise NotImplementedError("no fused kernel for the strip shape")
+    hw = h * STRIP_W
+    partial = zeros((ns * groups, hw), torch.float32)
+    N.call("qfca_score", sb.data_ptr(), 1, lo_r.data_ptr(), hi_r.data_ptr(), ref_r.data_ptr(),
+           ns, c, h, STRIP_W, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, groups,
+           partial.data_ptr(), s)
+    ones = torch.ones((ns,), dtype=torch.int32, device=bins.device)
+    acc = empty((ns, hw), torch.float64)
+    N.call("qfca_reduce_partials", partial.data_ptr(), ns, groups, hw, ones.data_ptr(),
+           acc.data_ptr(), s)
+    own = torch.as_tensor(owner, device=bins.device)
+    loc = torch.as_tensor(local, device=bins.device)
+    return acc.view(ns, h, STRIP_W)[own, :, loc].T.contiguous()  # (h, w)
 
 
 def detect_channel_sharded(values_local: torch.Tensor, cfg=None, group=None):

@@ -408,3 +408,29 @@ def test_topk_eigh_lanczos_vs_eigh(Q):
     assert float(proj.abs().max()) < 1e-11, float(proj.abs().max())
     w2, v2 = F.topk_eigh(cov, 10, lanczos=False)
     assert float((v @ v.mT - v2 @ v2.mT).abs().max()) < 1e-11
+
+
+@pytest.mark.parametrize("c,h,w,t", [(6, 96, 300, 9), (4, 64, 1024, 9), (5, 130, 257, 3),
+                                     (3, 40, 420, 15)])
+def test_wide_plane_strips_match_whole_plane(Q, c, h, w, t):
+    """sharding.channel_partial on planes wider than 128 columns (configs[4]:
+    1024^2 feature planes) runs the fused kernel on 128-column strips; it must
+    match the whole-plane generic kernel to fp32 summation rounding, and the
+    oracle on the final map."""
+    from paper_2510_15602_b200 import sharding
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(c * w + t)
+    x = np.maximum(rng.standard_normal((c, h, w)), 0).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    cfg = Q.PipelineConfig(patch_size=t)
+    acc, used = sharding.channel_partial(xt, cfg)
+    sharding.USE_STRIPS = False
+    try:
+        acc_w, used_w = sharding.channel_partial(xt, cfg)
+    finally:
+        sharding.USE_STRIPS = True
+    assert used == used_w
+    assert rel_err(acc.cpu().numpy(), acc_w.cpu().numpy()) <= 2e-6
+    ref_map, _, _ = O.detect(x, n_bins=cfg.n_bins, patch_size=t)
+    got = sharding.detect_channel_sharded(xt, cfg)[0].cpu().numpy()
+    assert rel_err(got, ref_map) <= TOL
