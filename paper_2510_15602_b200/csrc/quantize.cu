@@ -157,19 +157,25 @@ k_bin_thresholds(const float* __restrict__ lo, const float* __restrict__ hi, int
 
 template <typename BT>
 __global__ void __launch_bounds__(256)
-k_bin_table(const float* __restrict__ x, int64_t plane_len, const float* __restrict__ lo,
-            const float* __restrict__ hi, const float* __restrict__ tau, int n_bins,
-            BT* __restrict__ out) {
+k_bin_table(const float* __restrict__ x, int64_t plane_len, int splits,
+            const float* __restrict__ lo, const float* __restrict__ hi,
+            const float* __restrict__ tau, int n_bins, BT* __restrict__ out) {
     __shared__ float st[BT_MAXN + 1];
-    const int64_t plane = blockIdx.x;  // one CTA per plane: the setup is paid once
+    // one CTA per plane (the setup is paid once), or per 1/splits of a large plane
+    const int64_t plane = blockIdx.x / splits;
+    const int part = blockIdx.x - (int)(plane * splits);
     const int nt = n_bins - 1;
     for (int k = threadIdx.x; k < nt; k += blockDim.x) st[k] = tau[plane * nt + k];
     const float lf = lo[plane], hf = hi[plane];
     const float inv = hf > lf ? (float)((double)n_bins / ((double)hf - (double)lf)) : 0.f;
     const float top = (float)nt;
     __syncthreads();
-    const float* p = x + plane * plane_len;
-    BT* o = out + plane * plane_len;
+    // this CTA's range of the plane (multiples of 4 elements)
+    const int64_t q4 = (plane_len / 4 + splits - 1) / splits * 4;
+    const int64_t b0_ = part * q4;
+    const int64_t len = splits == 1 ? plane_len : max((int64_t)0, min(q4, plane_len - b0_));
+    const float* p = x + plane * plane_len + b0_;
+    BT* o = out + plane * plane_len + b0_;
     // fp32 estimate, then exact fix-up against the thresholds (bin k starts at st[k-1])
     auto bin = [&](float v) {
         int b = (int)fminf(fmaxf((v - lf) * inv, 0.f), top);  // NaN -> 0
@@ -179,7 +185,7 @@ k_bin_table(const float* __restrict__ x, int64_t plane_len, const float* __restr
     };
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
                      (sizeof(BT) == 2 || (reinterpret_cast<uintptr_t>(o) & 3) == 0);
-    const int64_t n4 = vec ? plane_len / 4 : 0;
+    const int64_t n4 = vec ? len / 4 : 0;
     for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i);
         const int b0 = bin(v.x), b1 = bin(v.y), b2 = bin(v.z), b3 = bin(v.w);
@@ -191,7 +197,7 @@ k_bin_table(const float* __restrict__ x, int64_t plane_len, const float* __restr
                 make_uint2((uint32_t)b0 | ((uint32_t)b1 << 16), (uint32_t)b2 | ((uint32_t)b3 << 16));
         }
     }
-    for (int64_t i = 4 * n4 + threadIdx.x; i < plane_len; i += blockDim.x)
+    for (int64_t i = 4 * n4 + threadIdx.x; i < len; i += blockDim.x)
         o[i] = (BT)bin(__ldg(p + i));
 }
 
@@ -209,12 +215,17 @@ int launch_bin(const float* x, int64_t planes, int64_t plane_len, const float* l
             cudaSuccess)
             return QFCA_ERR_CUDA;
         k_bin_thresholds<<<(unsigned)((planes + 3) / 4), 128, 0, st>>>(lo, hi, planes, n_bins, tau);
+        // large planes (few of them) split so the grid fills the GPU; the vector
+        // path needs every part to start on a 4-element boundary (plane_len % 4)
+        const int splits = (plane_len % 4 == 0 && plane_len >= (1 << 17))
+                               ? (int)min((int64_t)64, plane_len / (1 << 16)) : 1;
+        const unsigned g2 = (unsigned)(planes * splits);
         if (out_bytes == 1)
-            k_bin_table<uint8_t><<<(unsigned)planes, 256, 0, st>>>(x, plane_len, lo, hi, tau,
-                                                                    n_bins, (uint8_t*)out);
+            k_bin_table<uint8_t><<<g2, 256, 0, st>>>(x, plane_len, splits, lo, hi, tau, n_bins,
+                                                     (uint8_t*)out);
         else
-            k_bin_table<uint16_t><<<(unsigned)planes, 256, 0, st>>>(x, plane_len, lo, hi, tau,
-                                                                     n_bins, (uint16_t*)out);
+            k_bin_table<uint16_t><<<g2, 256, 0, st>>>(x, plane_len, splits, lo, hi, tau, n_bins,
+                                                      (uint16_t*)out);
         const bool ok = cudaGetLastError() == cudaSuccess;
         cudaFreeAsync(tau, st);
         return ok ? QFCA_OK : QFCA_ERR_CUDA;

@@ -34,17 +34,21 @@ __all__ = ["shard_range", "shard_batch", "combine_partials", "channel_partial",
            "detect_channel_sharded", "strips"]
 
 STRIP_W = 128  # widest plane of the fused kernels
+STRIP_H = 256  # tile height: the whole-tile bins + row tables stay in shared memory
 USE_STRIPS = True  # route wide planes through strips (False: whole-plane generic kernel)
 
 
 def strips(w: int, t: int, sw: int = STRIP_W):
-    """Column strips for a plane of width w > sw and patch size t (reflect pad):
-    returns (starts, owner strip per column, local column per column)."""
+    """Segments of length sw along an axis of length w (reflect pad, patch t):
+    returns (starts, owner segment per index, local index per index).  A single
+    segment when w <= sw."""
     import numpy as np
     halo = 2 * (t // 2)
     step = sw - 2 * halo
-    if w <= sw or step <= 0:
-        raise ValueError("strips need w > strip width > 4 (T // 2)")
+    if w <= sw:
+        return [0], np.zeros(w, np.int64), np.arange(w)
+    if step <= 0:
+        raise ValueError("segments need length > 4 (T // 2)")
     starts = [0]
     while starts[-1] + sw < w:
         starts.append(min(starts[-1] + step, w - sw))
@@ -105,8 +109,8 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
                                  cfg.sample_budget, 0)
     ref = None
     if (USE_STRIPS and w > STRIP_W and cfg.pad == "reflect" and bins.element_size() == 1
-            and L.qfca_score_groups(h, STRIP_W, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
-                                    cfg.sample_budget, 1) > 0):
+            and L.qfca_score_groups(min(h, STRIP_H), STRIP_W, cfg.n_bins, cfg.patch_size, c,
+                                    1, 0, pad, cfg.sample_budget, 1) > 0):
         return _strip_partial(bins, lo, hi, cfg, c, h, w), _used(lo, hi, c)
     if groups <= 0:  # kernel without in-kernel reference selection: run K3 first
         groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
@@ -135,37 +139,55 @@ def _used(lo, hi, c) -> int:
 
 
 def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
-    """Channel-sum map (h, w) fp64 of a wide plane from 128-column strips."""
+    """Channel-sum map (h, w) fp64 of a wide plane from 128-column strips, cut
+    into row bands of STRIP_H (same halo rule along rows), scored as one batch
+    of tiles."""
     s = N.stream()
     pad = N.PAD_CODES[cfg.pad]
-    starts, owner, local = strips(w, cfg.patch_size)
-    ns = len(starts)
+    cst, cown, cloc = strips(w, cfg.patch_size, STRIP_W)
+    rst, rown, rloc = strips(h, cfg.patch_size, STRIP_H)
+    th = min(h, STRIP_H)
+    nt = len(rst) * len(cst)
     ref = empty((c, cfg.n_bins), torch.int32)  # whole-plane reference (K3)
     N.call("qfca_select_reference", bins.data_ptr(), bins.element_size(), lo.data_ptr(),
            hi.data_ptr(), c, h, w, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, 0,
            ref.data_ptr(), s)
     b3 = bins.view(c, h, w)
-    sb = torch.stack([b3[:, :, a:a + STRIP_W] for a in starts]).contiguous()  # (ns, c, h, 128)
-    lo_r = lo.repeat(ns).contiguous()
-    hi_r = hi.repeat(ns).contiguous()
-    ref_r = ref.repeat(ns, 1).contiguous()
+    sb = torch.stack([b3[:, r:r + th, a:a + STRIP_W] for r in rst for a in cst]).contiguous()
+    lo_r = lo.repeat(nt).contiguous()
+    hi_r = hi.repeat(nt).contiguous()
+    ref_r = ref.repeat(nt, 1).contiguous()
     L = N.lib()
-    groups = L.qfca_score_groups(h, STRIP_W, cfg.n_bins, cfg.patch_size, c, ns, 0, pad,
+    groups = L.qfca_score_groups(th, STRIP_W, cfg.n_bins, cfg.patch_size, c, nt, 0, pad,
                                  cfg.sample_budget, 1)
     if groups <= 0:
-        raise NotImplementedError("no fused kernel for the strip shape")
-    hw = h * STRIP_W
-    partial = zeros((ns * groups, hw), torch.float32)
+        raise NotImplementedError("no fused kernel for the tile shape")
+    hw = th * STRIP_W
+    partial = zeros((nt * groups, hw), torch.float32)
     N.call("qfca_score", sb.data_ptr(), 1, lo_r.data_ptr(), hi_r.data_ptr(), ref_r.data_ptr(),
-           ns, c, h, STRIP_W, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, groups,
+           nt, c, th, STRIP_W, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, groups,
            partial.data_ptr(), s)
-    ones = torch.ones((ns,), dtype=torch.int32, device=bins.device)
-    acc = empty((ns, hw), torch.float64)
-    N.call("qfca_reduce_partials", partial.data_ptr(), ns, groups, hw, ones.data_ptr(),
+    ones = torch.ones((nt,), dtype=torch.int32, device=bins.device)
+    acc = empty((nt, hw), torch.float64)
+    N.call("qfca_reduce_partials", partial.data_ptr(), nt, groups, hw, ones.data_ptr(),
            acc.data_ptr(), s)
-    own = torch.as_tensor(owner, device=bins.device)
-    loc = torch.as_tensor(local, device=bins.device)
-    return acc.view(ns, h, STRIP_W)[own, :, loc].T.contiguous()  # (h, w)
+    ro, rl, co, cl = _tile_index(h, w, cfg.patch_size, bins.device, rown, rloc, cown, cloc)
+    a4 = acc.view(len(rst), len(cst), th, STRIP_W)
+    return a4[ro, co, rl, cl].contiguous()  # (h, w)
+
+
+_TILE_IDX: dict = {}
+
+
+def _tile_index(h, w, t, dev, rown, rloc, cown, cloc):
+    """Owner / local index tensors of the tile decomposition, cached on the device."""
+    key = (h, w, t, str(dev))
+    if key not in _TILE_IDX:
+        _TILE_IDX[key] = (torch.as_tensor(rown, device=dev)[:, None],
+                          torch.as_tensor(rloc, device=dev)[:, None],
+                          torch.as_tensor(cown, device=dev)[None, :],
+                          torch.as_tensor(cloc, device=dev)[None, :])
+    return _TILE_IDX[key]
 
 
 def detect_channel_sharded(values_local: torch.Tensor, cfg=None, group=None):
