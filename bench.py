@@ -31,6 +31,9 @@ WORKLOADS = {
                                   "synthetic textures, WRN50-2 random-init block-2 features"),
     "qfca1024": (1024, 64, 0, "configs[2]: QFCA, batch 64 per GPU of 1024x1024 synthetic "
                               "textures, WRN50-2 random-init block-2 features"),
+    "qfca8192": (8192, 1, 0, "configs[4]: one 8192x8192 synthetic texture (512 x 1024^2 "
+                             "WRN50-2 random-init block-2 features), channels sharded across "
+                             "the ranks, one all-reduce of the channel-sum map"),
 }
 METRIC = "images/sec (megapixels/sec) of QFCA scoring; % of HBM roofline"
 
@@ -192,6 +195,9 @@ def main():
     from paper_2510_15602_b200 import _native
     import workloads
 
+    if args.workload == "qfca8192":
+        return run_sharded_image(args, ws, rank, local, config, size, mp_per_image)
+
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -318,6 +324,133 @@ def main():
                 "mp_per_s": ips * mp_per_image, "n_gpus": ws, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u8 bins / i32 counts / f32+f64 errors", "data": "synthetic",
+                "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_sharded_image(args, ws, rank, local, config, size, mp_per_image):
+    """configs[4]: one image, channels sharded over the ranks (sharding.py); a
+    step = score this rank's channel slice + one all-reduce of the (h*w + 1)
+    channel-sum buffer + finalise (mean, Gaussian, image score)."""
+    import numpy as np
+    import torch
+    import paper_2510_15602_b200 as Q
+    from paper_2510_15602_b200 import _native, sharding
+    import workloads
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    with torch.no_grad():
+        feats, _ = workloads.make_features(1, size, seed=1000, device=dev)
+    c_all = feats.shape[1]
+    c0, c1 = sharding.shard_range(c_all, ws, rank)
+    x = feats[0, c0:c1].contiguous()
+    h, w = x.shape[1:]
+    del feats
+    torch.cuda.empty_cache()
+    cfg = Q.PipelineConfig()
+    config.update({"channels": c_all, "channels_per_rank": c1 - c0, "feature_size": h,
+                   "global_batch": 1, "images_per_gpu": None,
+                   "parallelism": f"channel-sharded x{ws}, one all-reduce per image",
+                   "l2": "inputs larger than L2 (features 2 GiB per image)"})
+
+    def step(xx):
+        torch.cuda.nvtx.range_push("qfca_step")
+        out = sharding.detect_channel_sharded(xx, cfg)
+        torch.cuda.nvtx.range_pop()
+        return out
+
+    for _ in range(max(3, args.warmup)):
+        step(x)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches0 = _native.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step(x)
+        e1.record()
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    ms_per_step = ms / args.steps
+    ips = 1e3 / ms_per_step
+
+    e2e = None
+    if not args.no_e2e:  # host slice in, map + image score out, every step
+        xh = x.cpu().pin_memory()
+        xd = torch.empty_like(x)
+        for _ in range(2):
+            xd.copy_(xh, non_blocking=True)
+            m, _, _ = step(xd)
+            m.cpu()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            xd.copy_(xh, non_blocking=True)
+            m, _, _ = step(xd)
+            m.cpu()
+        f1.record()
+        torch.cuda.synchronize()
+        e_ms = f0.elapsed_time(f1)
+        if ws > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": 1e3 * args.steps / e_ms, "unit": "images/s",
+               "h2d_bytes_per_step": xh.numel() * 4, "d2h_bytes_per_step": h * w * 8,
+               "mp_per_s": 1e3 * args.steps / e_ms * mp_per_image}
+
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback"
+    if os.path.exists(peaks_path):
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "measured"
+    alg = alg_bytes_per_image(size, False)
+    achieved = alg / (ms_per_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "kernel": "whole step (wide-plane tiles on the fused kernel + K3 + K1/K2 + "
+                      "all-reduce + finalise)", "kernel_ms_per_launch": ms_per_step,
+            "step_ms": ms_per_step, "kernel_share_of_step": 1.0,
+            "step_alg_bytes_frac": achieved / peak}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        from oracle import qfca_oracle as O
+        sub = x[:16].cpu().numpy()
+        O.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        O.detect(np.ascontiguousarray(sub))
+        el = time.perf_counter() - t0
+        per_img = el * c_all / sub.shape[0]  # scoring and reference are linear in C
+        cpu = {"value": 1.0 / per_img, "unit": "images/s", "cores": O.num_threads(),
+               "kind": "port",
+               "sample": f"16 of the {c_all} channels of the 1024x1024 feature plane through "
+                         f"the C oracle ({el:.1f} s), extrapolated x{c_all // 16} (linear in C)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": ips, "unit": "images/s",
+                "mp_per_s": ips * mp_per_image, "n_gpus": ws, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "u8 bins / i32 counts / f32+f64 errors", "data": "synthetic",
                 "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary()}
