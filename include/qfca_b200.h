@@ -56,6 +56,13 @@ int qfca_bin_indices(const float* x, int64_t planes, int64_t plane_len, const fl
                      const float* hi, int32_t n_bins, void* bins, int32_t bins_bytes,
                      void* stream);
 
+/* fit_quantizer + bin_indices in one call (quantize.py:61-82): lo/hi/nonfinite
+ * as qfca_fit_quantizer, bins as qfca_bin_indices, bit-identical to the two
+ * calls; one pass over x when a plane fits in shared memory (<= 16384 values,
+ * plane_len % 4 == 0, 2 <= n_bins <= 65), else the two kernels. */
+int qfca_quantize(const float* x, int64_t planes, int64_t plane_len, int32_t n_bins, float* lo,
+                  float* hi, int32_t* nonfinite, void* bins, int32_t bins_bytes, void* stream);
+
 /* _sample_grid stride (quantize.py:109-116); host-only helper */
 int qfca_sample_stride(int32_t h, int32_t w, int32_t sample_budget);
 

@@ -35,6 +35,7 @@ _SIGNATURES = {
     "qfca_status_str": ([_I32], ctypes.c_char_p),
     "qfca_fit_quantizer": ([_P, _I64, _I64, _P, _P, _P, _P], _I32),
     "qfca_bin_indices": ([_P, _I64, _I64, _P, _P, _I32, _P, _I32, _P], _I32),
+    "qfca_quantize": ([_P, _I64, _I64, _I32, _P, _P, _P, _P, _I32, _P], _I32),
     "qfca_sample_stride": ([_I32, _I32, _I32], _I32),
     "qfca_select_reference": ([_P, _I32, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32,
                                _I32, _P, _P], _I32),

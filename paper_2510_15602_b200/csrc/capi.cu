@@ -8,6 +8,8 @@
 
 namespace qfca {
 int launch_minmax(const float*, int64_t, int64_t, float*, float*, int*, cudaStream_t);
+int launch_quantize_fused(const float*, int64_t, int64_t, int, float*, float*, int*, void*, int,
+                          cudaStream_t);
 int launch_bin(const float*, int64_t, int64_t, const float*, const float*, int, void*, int,
                cudaStream_t);
 int launch_plane_mean(const float*, int64_t, int64_t, double*, cudaStream_t);
@@ -168,6 +170,16 @@ int qfca_fit_quantizer(const float* x, int64_t planes, int64_t plane_len, float*
 int qfca_bin_indices(const float* x, int64_t planes, int64_t plane_len, const float* lo,
                      const float* hi, int32_t n_bins, void* bins, int32_t bins_bytes,
                      void* stream) {
+    return counted(launch_bin(x, planes, plane_len, lo, hi, n_bins, bins, bins_bytes, S(stream)), 1);
+}
+
+int qfca_quantize(const float* x, int64_t planes, int64_t plane_len, int32_t n_bins, float* lo,
+                  float* hi, int32_t* nonfinite, void* bins, int32_t bins_bytes, void* stream) {
+    int rc = launch_quantize_fused(x, planes, plane_len, n_bins, lo, hi, nonfinite, bins,
+                                   bins_bytes, S(stream));
+    if (rc != QFCA_ERR_UNSUPPORTED) return counted(rc, 1);
+    if ((rc = counted(launch_minmax(x, planes, plane_len, lo, hi, nonfinite, S(stream)), 1)))
+        return rc;
     return counted(launch_bin(x, planes, plane_len, lo, hi, n_bins, bins, bins_bytes, S(stream)), 1);
 }
 
@@ -433,9 +445,18 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
     double* agg = (double*)(ws + L.agg);
     double* tmp = (double*)(ws + L.tmp);
     const int64_t planes = images * C, hw = (int64_t)h * w;
-    if ((rc = counted(launch_minmax(features, planes, hw, lo, hi, nonfinite, st), 1))) return rc;
-    if ((rc = counted(launch_bin(features, planes, hw, lo, hi, cfg->n_bins, bins, L.bins_bytes, st), 1)))
+    // K1 + K2 fused (one read of the features) when the planes fit in shared memory
+    rc = launch_quantize_fused(features, planes, hw, cfg->n_bins, lo, hi, nonfinite, bins,
+                               L.bins_bytes, st);
+    if (rc == QFCA_OK) {
+        counted(rc, 1);
+    } else if (rc == QFCA_ERR_UNSUPPORTED) {
+        if ((rc = counted(launch_minmax(features, planes, hw, lo, hi, nonfinite, st), 1))) return rc;
+        if ((rc = counted(launch_bin(features, planes, hw, lo, hi, cfg->n_bins, bins, L.bins_bytes, st), 1)))
+            return rc;
+    } else {
         return rc;
+    }
     if (!L.choice.fref &&  // else the scoring kernel selects the reference itself
         (rc = counted(launch_reference(bins, L.bins_bytes, lo, hi, planes, h, w, cfg->n_bins,
                                        cfg->patch_size, cfg->pad, cfg->sample_budget, 0, V, st),

@@ -133,6 +133,33 @@ __device__ __forceinline__ float fval(int key) {
     return __int_as_float(key >= 0 ? key : key ^ 0x7FFFFFFF);
 }
 
+// smallest float32 v with bin_of(v) >= k (lo < hi, 1 <= k <= n_bins - 1): start
+// at the fp32 rounding of the exact boundary lo + k span / N (a few ulps off at
+// most), walk a few ulps, fall back to bisection over the ordered keys
+__device__ __forceinline__ float fq_threshold(int k, float lf, float hf, int n_bins) {
+    const double l = lf, span = (double)hf - (double)lf;
+    const int64_t klo = fkey(lf), khi = fkey(hf);
+    int64_t key = fkey((float)(l + (double)k * span / (double)n_bins));
+    key = key < klo + 1 ? klo + 1 : (key > khi ? khi : key);
+    // invariant sought: bin(key) >= k > bin(key - 1)
+    for (int it = 0; it < 6; ++it) {
+        const bool ge = bin_of(fval((int)key), l, span, n_bins) >= k;
+        if (ge) {
+            if (key - 1 <= klo || bin_of(fval((int)(key - 1)), l, span, n_bins) < k)
+                return fval((int)key);
+            --key;
+        } else {
+            ++key;
+        }
+    }
+    int64_t a = klo, b = khi;  // bin(a) = 0 < k <= n_bins - 1 = bin(b)
+    while (b - a > 1) {
+        const int64_t m = a + (b - a) / 2;
+        if (bin_of(fval((int)m), l, span, n_bins) >= k) b = m; else a = m;
+    }
+    return fval((int)b);
+}
+
 __global__ void __launch_bounds__(128)
 k_bin_thresholds(const float* __restrict__ lo, const float* __restrict__ hi, int64_t planes,
                  int n_bins, float* __restrict__ tau) {
@@ -140,18 +167,9 @@ k_bin_thresholds(const float* __restrict__ lo, const float* __restrict__ hi, int
     if (plane >= planes) return;
     const int lane = threadIdx.x & 31;
     const float lf = lo[plane], hf = hi[plane];
-    const double l = lf, span = (double)hf - (double)lf;
     for (int k = 1 + lane; k < n_bins; k += 32) {
-        float t = INFINITY;  // degenerate channel: every bin is 0
-        if (hf > lf) {
-            int64_t a = fkey(lf), b = fkey(hf);  // bin(lo) = 0 < k <= N-1 = bin(hi)
-            while (b - a > 1) {
-                const int64_t m = a + (b - a) / 2;
-                if (bin_of(fval((int)m), l, span, n_bins) >= k) b = m; else a = m;
-            }
-            t = fval((int)b);
-        }
-        tau[plane * (n_bins - 1) + (k - 1)] = t;
+        // degenerate channel: every bin is 0
+        tau[plane * (n_bins - 1) + (k - 1)] = hf > lf ? fq_threshold(k, lf, hf, n_bins) : INFINITY;
     }
 }
 
@@ -199,6 +217,113 @@ k_bin_table(const float* __restrict__ x, int64_t plane_len, int splits,
     }
     for (int64_t i = 4 * n4 + threadIdx.x; i < len; i += blockDim.x)
         o[i] = (BT)bin(__ldg(p + i));
+}
+
+// ---- fused K1 + K2 for planes that fit in shared memory (one CTA per plane):
+// the plane is read from HBM once (min/max + finiteness from the staged copy,
+// thresholds, bins) instead of twice.  Thresholds as k_bin_thresholds (the
+// smallest float32 whose fp64 bin is >= k), one thread per threshold, started
+// at the rounded exact boundary and corrected by a few ulps (instead of ~31
+// serial bisection probes).  Bit-identical to K1 + K2.
+constexpr int FQ_THREADS = 256;
+constexpr int FQ_MAXLEN = 16384;  // 64 KB of fp32 staged per plane
+
+template <typename BT>
+__global__ void __launch_bounds__(FQ_THREADS)
+k_quantize_plane(const float* __restrict__ x, int plane_len, int n_bins, float* __restrict__ lo,
+                 float* __restrict__ hi, int* __restrict__ nonfinite, BT* __restrict__ out) {
+    extern __shared__ __align__(16) float fq_x[];  // [plane_len]
+    __shared__ float st[BT_MAXN + 1];
+    __shared__ float smn[FQ_THREADS / 32], smx[FQ_THREADS / 32];
+    __shared__ int sbad;
+    const int64_t plane = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float4* p4 = reinterpret_cast<const float4*>(x + plane * plane_len);
+    float mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
+    if (tid == 0) sbad = 0;
+    for (int i = tid; i < plane_len / 4; i += FQ_THREADS) {
+        const float4 v = __ldg(p4 + i);
+        reinterpret_cast<float4*>(fq_x)[i] = v;
+        mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    bad = __any_sync(0xffffffffu, bad);
+    __syncthreads();
+    if (lane == 0) {
+        smn[warp] = mn;
+        smx[warp] = mx;
+        if (bad) sbad = 1;
+    }
+    __syncthreads();
+    mn = smn[0];
+    mx = smx[0];
+#pragma unroll
+    for (int w = 1; w < FQ_THREADS / 32; ++w) {
+        mn = fminf(mn, smn[w]);
+        mx = fmaxf(mx, smx[w]);
+    }
+    if (tid == 0) {
+        lo[plane] = mn;
+        hi[plane] = mx;
+        if (sbad && nonfinite) atomicOr(nonfinite, 1);
+    }
+    const int nt = n_bins - 1;
+    for (int k = 1 + tid; k <= nt; k += FQ_THREADS)
+        st[k - 1] = mx > mn ? fq_threshold(k, mn, mx, n_bins) : INFINITY;
+    const float inv = mx > mn ? (float)((double)n_bins / ((double)mx - (double)mn)) : 0.f;
+    const float top = (float)nt;
+    __syncthreads();
+    auto bin = [&](float v) {
+        int b = (int)fminf(fmaxf((v - mn) * inv, 0.f), top);  // NaN -> 0
+        while (b < nt && v >= st[b]) ++b;
+        while (b > 0 && v < st[b - 1]) --b;
+        return b;
+    };
+    BT* o = out + plane * plane_len;
+    for (int i = tid; i < plane_len / 4; i += FQ_THREADS) {
+        const float4 v = reinterpret_cast<const float4*>(fq_x)[i];
+        const int b0 = bin(v.x), b1 = bin(v.y), b2 = bin(v.z), b3 = bin(v.w);
+        if (sizeof(BT) == 1) {
+            reinterpret_cast<uint32_t*>(o)[i] =
+                (uint32_t)b0 | ((uint32_t)b1 << 8) | ((uint32_t)b2 << 16) | ((uint32_t)b3 << 24);
+        } else {
+            reinterpret_cast<uint2*>(o)[i] =
+                make_uint2((uint32_t)b0 | ((uint32_t)b1 << 16), (uint32_t)b2 | ((uint32_t)b3 << 16));
+        }
+    }
+}
+
+// K1 + K2 in one pass when the planes fit; QFCA_ERR_UNSUPPORTED otherwise (the
+// caller then runs launch_minmax + launch_bin)
+int launch_quantize_fused(const float* x, int64_t planes, int64_t plane_len, int n_bins,
+                          float* lo, float* hi, int* nonfinite, void* out, int out_bytes,
+                          cudaStream_t st) {
+    if (planes <= 0 || plane_len <= 0 || n_bins < 1) return QFCA_ERR_ARG;
+    if (plane_len > FQ_MAXLEN || plane_len % 4 || n_bins < 2 || n_bins > BT_MAXN + 1 ||
+        (out_bytes != 1 && out_bytes != 2) || planes > 0x7fffffffLL ||
+        (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 7))
+        return QFCA_ERR_UNSUPPORTED;
+    const size_t smem = (size_t)plane_len * sizeof(float);
+    if (out_bytes == 1) {
+        if (cudaFuncSetAttribute(k_quantize_plane<uint8_t>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return QFCA_ERR_CUDA;
+        k_quantize_plane<uint8_t><<<(unsigned)planes, FQ_THREADS, smem, st>>>(
+            x, (int)plane_len, n_bins, lo, hi, nonfinite, (uint8_t*)out);
+    } else {
+        if (cudaFuncSetAttribute(k_quantize_plane<uint16_t>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return QFCA_ERR_CUDA;
+        k_quantize_plane<uint16_t><<<(unsigned)planes, FQ_THREADS, smem, st>>>(
+            x, (int)plane_len, n_bins, lo, hi, nonfinite, (uint16_t*)out);
+    }
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
 int launch_bin(const float* x, int64_t planes, int64_t plane_len, const float* lo,

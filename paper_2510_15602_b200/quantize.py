@@ -93,6 +93,19 @@ def bins_dev(x: torch.Tensor, lo: torch.Tensor, hi: torch.Tensor, planes: int, p
     return out
 
 
+def quantize_dev(x: torch.Tensor, planes: int, plane_len: int, n_bins: int):
+    """minmax_dev + bins_dev in one C-ABI call (qfca_quantize: one pass over x
+    when a plane fits in shared memory).  Returns (lo, hi, flag, bins)."""
+    dtype, nb = bins_dtype(n_bins)
+    lo = empty((planes,), torch.float32)
+    hi = empty((planes,), torch.float32)
+    flag = zeros((1,), torch.int32)
+    out = empty((planes * plane_len,), dtype)
+    N.call("qfca_quantize", x.data_ptr(), planes, plane_len, n_bins, lo.data_ptr(),
+           hi.data_ptr(), flag.data_ptr(), out.data_ptr(), nb, N.stream())
+    return lo, hi, flag, out
+
+
 def reference_stats_dev(bins: torch.Tensor, lo: torch.Tensor, hi: torch.Tensor, planes: int,
                         h: int, w: int, n_bins: int, t: int, pad: str, budget: int,
                         mode: str) -> torch.Tensor:

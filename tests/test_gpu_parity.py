@@ -411,7 +411,7 @@ def test_topk_eigh_lanczos_vs_eigh(Q):
 
 
 @pytest.mark.parametrize("c,h,w,t", [(6, 96, 300, 9), (4, 64, 1024, 9), (5, 130, 257, 3),
-                                     (3, 40, 420, 15)])
+                                     (3, 40, 420, 15), (3, 600, 200, 9), (2, 257, 129, 5)])
 def test_wide_plane_strips_match_whole_plane(Q, c, h, w, t):
     """sharding.channel_partial on planes wider than 128 columns (configs[4]:
     1024^2 feature planes) runs the fused kernel on 128-column strips; it must
@@ -434,3 +434,25 @@ def test_wide_plane_strips_match_whole_plane(Q, c, h, w, t):
     ref_map, _, _ = O.detect(x, n_bins=cfg.n_bins, patch_size=t)
     got = sharding.detect_channel_sharded(xt, cfg)[0].cpu().numpy()
     assert rel_err(got, ref_map) <= TOL
+
+
+@pytest.mark.parametrize("planes,h,w,n", [(37, 64, 64, 16), (5, 128, 128, 16), (9, 32, 32, 2),
+                                          (4, 20, 24, 65), (3, 128, 128, 64), (2, 300, 300, 16),
+                                          (6, 7, 9, 16)])
+def test_fused_quantize_matches_two_kernels(Q, planes, h, w, n):
+    """csrc/quantize.cu k_quantize_plane (min/max + thresholds + bins from one
+    staged read) is bit-identical to K1 + K2, incl. constant planes and inf."""
+    from paper_2510_15602_b200 import quantize as QZ
+    rng = np.random.default_rng(planes * h + n)
+    x = (np.maximum(rng.standard_normal((planes, h * w)), 0) *
+         rng.uniform(1e-3, 1e3, (planes, 1))).astype(np.float32)
+    x[0] = 0.75                      # degenerate plane
+    if planes > 2:
+        x[1, 5] = np.inf             # non-finite flag
+    xt = torch.from_numpy(x).cuda()
+    lo, hi, flag, b = QZ.quantize_dev(xt, planes, h * w, n)
+    lo2, hi2, flag2 = QZ.minmax_dev(xt, planes, h * w)
+    b2 = QZ.bins_dev(xt, lo2, hi2, planes, h * w, n)
+    assert torch.equal(lo, lo2) and torch.equal(hi, hi2)
+    assert int(flag[0]) == int(flag2[0]) == (1 if planes > 2 else 0)
+    assert torch.equal(b, b2)
