@@ -259,8 +259,35 @@ def detect_batch(values: torch.Tensor, cfg: PipelineConfig | None = None,
         mean, comps, _ = pca_fit_batch(x, k)
         x = pca_residual_batch(x, mean, comps)
     if fused_supported(cfg):
+        from .sharding import wide_supported
+        if wide_supported(cfg, x.shape[2], x.shape[3], x.shape[1]):
+            return _wide_detect(x, cfg)
         return _fused_detect(x, cfg, groups, out, score_events)
     return _general_detect(x, cfg)
+
+
+def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
+    """Feature planes wider than the fused kernels' 128 columns (an 8192^2
+    texture: 1024^2 per channel): each image through the tiled fused path of
+    sharding.py (one rank holding every channel), then the channel mean,
+    Gaussian and image score as in _fused_detect (scoring.py:286-327)."""
+    from .sharding import _channel_partial
+    b, c, h, w = x.shape
+    out = DetectResult(scores=empty((b, h, w), torch.float64),
+                       image_scores=empty((b,), torch.float64),
+                       used=empty((b,), torch.int32), nonfinite=zeros((1,), torch.int32))
+    taps = _gauss_kernel(cfg.sigma_s) if cfg.sigma_s > 0 else None
+    for i in range(b):
+        acc, used, flag = _channel_partial(x[i], cfg)
+        out.nonfinite.bitwise_or_(flag)
+        out.used[i] = used
+        agg = acc / used if used > 0 else acc
+        final = sep_convolve_dev(agg[None].contiguous(), taps, cfg.pad)[0] \
+            if taps is not None else agg
+        out.scores[i] = final
+        N.call("qfca_image_score", out.scores[i].data_ptr(), 1, h, w, cfg.border,
+               out.image_scores[i:i + 1].data_ptr(), N.stream())
+    return out
 
 
 def detect(f: FeatureMap, cfg: PipelineConfig | None = None,

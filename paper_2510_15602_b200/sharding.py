@@ -94,6 +94,21 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     """Channel-sum map (h, w) fp64 and used-channel count for this rank's
     channel slice (C_local, h, w), fused path (scoring.py:286-309 without the
     division)."""
+    acc, used, _ = _channel_partial(values, cfg)
+    return acc, used
+
+
+def wide_supported(cfg, h: int, w: int, c: int) -> bool:
+    """Planes wider than STRIP_W that the tiled fused path takes."""
+    if not (USE_STRIPS and w > STRIP_W and cfg.pad == "reflect" and cfg.n_bins <= 256):
+        return False
+    L = N.lib()
+    return L.qfca_score_groups(min(h, STRIP_H), STRIP_W, cfg.n_bins, cfg.patch_size, c, 1, 0,
+                               N.PAD_CODES[cfg.pad], cfg.sample_budget, 1) > 0
+
+
+def _channel_partial(values: torch.Tensor, cfg):
+    """channel_partial + the device non-finite flag of the slice."""
     from .scoring import fused_supported
     if not fused_supported(cfg):
         raise NotImplementedError("channel sharding covers the fused configuration")
@@ -108,10 +123,8 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
                                  cfg.sample_budget, 0)
     ref = None
-    if (USE_STRIPS and w > STRIP_W and cfg.pad == "reflect" and bins.element_size() == 1
-            and L.qfca_score_groups(min(h, STRIP_H), STRIP_W, cfg.n_bins, cfg.patch_size, c,
-                                    1, 0, pad, cfg.sample_budget, 1) > 0):
-        return _strip_partial(bins, lo, hi, cfg, c, h, w), _used(lo, hi, c)
+    if bins.element_size() == 1 and wide_supported(cfg, h, w, c):
+        return _strip_partial(bins, lo, hi, cfg, c, h, w), _used(lo, hi, c), flag
     if groups <= 0:  # kernel without in-kernel reference selection: run K3 first
         groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
                                      cfg.sample_budget, 1)
@@ -129,7 +142,7 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     acc = empty((1, hw), torch.float64)
     N.call("qfca_reduce_partials", partial.data_ptr(), 1, groups, hw, ones.data_ptr(),
            acc.data_ptr(), s)
-    return acc.reshape(h, w), int(used[0])
+    return acc.reshape(h, w), int(used[0]), flag
 
 
 def _used(lo, hi, c) -> int:

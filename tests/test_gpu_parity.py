@@ -456,3 +456,17 @@ def test_fused_quantize_matches_two_kernels(Q, planes, h, w, n):
     assert torch.equal(lo, lo2) and torch.equal(hi, hi2)
     assert int(flag[0]) == int(flag2[0]) == (1 if planes > 2 else 0)
     assert torch.equal(b, b2)
+
+
+def test_wide_plane_detect_batch(Q):
+    """detect_batch on feature planes wider than 128 columns takes the tiled path
+    and matches the oracle (map, image score)."""
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(3)
+    x = np.maximum(rng.standard_normal((2, 5, 70, 260)), 0).astype(np.float32)
+    res = Q.detect_batch(torch.from_numpy(x).cuda(), Q.PipelineConfig())
+    for i in range(2):
+        ref, img, _ = O.detect(x[i])
+        assert rel_err(res.scores[i].cpu().numpy(), ref) <= TOL
+        assert abs(float(res.image_scores[i]) - img) <= TOL * np.abs(ref).max()
+        assert int(res.used[i]) == 5

@@ -17,12 +17,14 @@ ver = L.qfca_score_version(h, w, cfg.n_bins, cfg.patch_size, c, 1, N.PAD_CODES[c
                            cfg.sample_budget, 0)
 acc, used = sharding.channel_partial(x, cfg)
 torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(3):
+times = []
+for _ in range(10):  # per call (each ends in a host sync for the used count)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     acc, used = sharding.channel_partial(x, cfg)
-e1.record()
-torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / 3
+    e1.record()
+    torch.cuda.synchronize()
+    times.append(e0.elapsed_time(e1))
+ms = min(times)
 print(json.dumps({"channels": c, "plane": [h, w], "score_version": ver, "ms": round(ms, 2),
                   "ms_per_channel": round(ms / c, 3), "used": used}))
