@@ -153,10 +153,12 @@ def covariance_exact(x: torch.Tensor, mean: torch.Tensor | None) -> torch.Tensor
     L = N.lib()
     need = int(L.qfca_covariance_workspace_bytes(b, c, hw))
     cov = empty((b, c, c), torch.float64)
-    key = (x.device.index, need)
+    # one cached workspace per (device, stream, size): calls on different streams may overlap
+    key = (x.device.index, torch.cuda.current_stream(x.device).cuda_stream, need)
     ws = _COV_WS.get(key)
     if ws is None:
-        _COV_WS.clear()
+        if len(_COV_WS) > 8:
+            _COV_WS.clear()
         ws = _COV_WS[key] = empty((max(need, 1),), torch.uint8)
     if mean is None:  # also form the plane means (features.py:170), returned
         mean_out = empty((b, c), torch.float64)

@@ -108,7 +108,9 @@ _WS_CACHE: dict = {}
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    key = (device.index if device.index is not None else torch.cuda.current_device())
+    # one cached workspace per (device, stream): calls on different streams may overlap
+    key = (device.index if device.index is not None else torch.cuda.current_device(),
+           torch.cuda.current_stream(device).cuda_stream)
     ws = _WS_CACHE.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty((max(nbytes, 1),), dtype=torch.uint8, device=device)
