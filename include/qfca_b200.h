@@ -210,6 +210,14 @@ int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, co
 int qfca_ritz(const double* h, int64_t batch, int32_t n, const double* x0, int32_t iters,
               double* x, double* hm, void* stream);
 
+/* Tiles of wide uint8 bin planes (channels, h, w), w % 4 == 0: out[t][c][y][x]
+ * = bins[c][row_starts[t / n_cols] + y][col_starts[t % n_cols] + x] for tile_h x
+ * tile_w tiles, column starts multiples of 4 (the 128-column fused kernel on
+ * the 1024^2 feature planes of configs[4]; device arrays of starts). */
+int qfca_gather_tiles(const void* bins, int32_t channels, int32_t h, int32_t w,
+                      const int32_t* row_starts, int32_t n_rows, const int32_t* col_starts,
+                      int32_t n_cols, int32_t tile_h, int32_t tile_w, void* out, void* stream);
+
 /* Covariance of pca_fit (features.py:167-171): cov = (x - mean)^T (x - mean) / n
  * for a batch of images, x (images, C, hw) fp32 channel-major, mean (images, C)
  * fp64 -> cov (images, C, C) fp64.  fp64-accurate (~1e-11 relative): the

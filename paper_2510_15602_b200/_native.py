@@ -64,6 +64,7 @@ _SIGNATURES = {
     "qfca_sym_eig": ([_P, _I64, _I32, _P, _P, _P], _I32),
     "qfca_lanczos": ([_P, _I64, _I32, _I32, _P, _P, _P, _P], _I32),
     "qfca_ritz": ([_P, _I64, _I32, _P, _I32, _P, _P, _P], _I32),
+    "qfca_gather_tiles": ([_P, _I32, _I32, _I32, _P, _I32, _P, _I32, _I32, _I32, _P, _P], _I32),
     "qfca_covariance_workspace_bytes": ([_I64, _I32, _I32], _I64),
     "qfca_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),
     "qfca_mean_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),

@@ -46,6 +46,8 @@ int launch_chol_rinv(const double*, int64_t, int, double*, cudaStream_t);
 int launch_sym_eig(const double*, int64_t, int, double*, double*, cudaStream_t);
 int launch_lanczos(const double*, int64_t, int, int, const double*, double*, double*, cudaStream_t);
 int launch_ritz(const double*, int64_t, int, const double*, int, double*, double*, cudaStream_t);
+int launch_gather_tiles(const void*, int, int, int, const int*, int, const int*, int, int, int, void*,
+                        cudaStream_t);
 int launch_cov_i8(const float*, int64_t, int, int, const double*, double*, void*, int64_t,
                   double*, cudaStream_t);
 int score2_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
@@ -341,6 +343,13 @@ int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, co
 int qfca_ritz(const double* h, int64_t batch, int32_t n, const double* x0, int32_t iters,
               double* x, double* hm, void* stream) {
     return counted(launch_ritz(h, batch, n, x0, iters, x, hm, S(stream)), 1);
+}
+
+int qfca_gather_tiles(const void* bins, int32_t channels, int32_t h, int32_t w,
+                      const int32_t* row_starts, int32_t n_rows, const int32_t* col_starts,
+                      int32_t n_cols, int32_t tile_h, int32_t tile_w, void* out, void* stream) {
+    return counted(launch_gather_tiles(bins, channels, h, w, row_starts, n_rows, col_starts,
+                                       n_cols, tile_h, tile_w, out, S(stream)), 1);
 }
 
 int64_t qfca_covariance_workspace_bytes(int64_t images, int32_t C, int32_t hw) {

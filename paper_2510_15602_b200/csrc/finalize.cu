@@ -60,11 +60,20 @@ __global__ void k_image_score(const double* __restrict__ scores, int h, int w, i
     bb = min(bb, (h - 1) / 2);
     bb = min(bb, (w - 1) / 2);
     if (bb < 0) bb = 0;
-    const int ih = h - 2 * bb, iw = w - 2 * bb;
+    const int iw = w - 2 * bb;
     double m = -INFINITY;
-    for (int64_t i = threadIdx.x; i < (int64_t)ih * iw; i += blockDim.x) {
-        const int y = bb + (int)(i / iw), x = bb + (int)(i % iw);
-        m = fmax(m, p[(int64_t)y * w + x]);
+    if (iw >= (int)blockDim.x) {  // wide rows: coalesced row sweeps, no index division
+        for (int y = bb; y < h - bb; ++y) {
+            const double* row = p + (int64_t)y * w + bb;
+#pragma unroll 4
+            for (int x = threadIdx.x; x < iw; x += blockDim.x) m = fmax(m, row[x]);
+        }
+    } else {
+        const int ih = h - 2 * bb;
+        for (int64_t i = threadIdx.x; i < (int64_t)ih * iw; i += blockDim.x) {
+            const int y = bb + (int)(i / iw), x = bb + (int)(i % iw);
+            m = fmax(m, p[(int64_t)y * w + x]);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -174,7 +183,9 @@ int launch_sep_conv(const double* in, int64_t images, int h, int w, int axis,
 int launch_image_score(const double* scores, int64_t images, int h, int w, int border,
                        double* image_score, cudaStream_t st) {
     if (images <= 0 || h <= 0 || w <= 0) return QFCA_ERR_ARG;
-    k_image_score<<<(unsigned)images, 256, 0, st>>>(scores, h, w, border, image_score);
+    // one CTA per image; large maps (an 8192^2 texture's 1024^2 map) get 1024 threads
+    const int threads = (int64_t)h * w > 65536 ? 1024 : 256;
+    k_image_score<<<(unsigned)images, threads, 0, st>>>(scores, h, w, border, image_score);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 

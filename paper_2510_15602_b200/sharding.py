@@ -165,8 +165,15 @@ def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
     N.call("qfca_select_reference", bins.data_ptr(), bins.element_size(), lo.data_ptr(),
            hi.data_ptr(), c, h, w, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, 0,
            ref.data_ptr(), s)
-    b3 = bins.view(c, h, w)
-    sb = torch.stack([b3[:, r:r + th, a:a + STRIP_W] for r in rst for a in cst]).contiguous()
+    ro, rl, co, cl, rst_d, cst_d = _tile_index(h, w, cfg.patch_size, bins.device, rst, rown,
+                                               rloc, cst, cown, cloc)
+    sb = empty((nt, c, th, STRIP_W), torch.uint8)
+    if w % 4 == 0:
+        N.call("qfca_gather_tiles", bins.data_ptr(), c, h, w, rst_d.data_ptr(), len(rst),
+               cst_d.data_ptr(), len(cst), th, STRIP_W, sb.data_ptr(), s)
+    else:
+        b3 = bins.view(c, h, w)
+        sb.copy_(torch.stack([b3[:, r:r + th, a:a + STRIP_W] for r in rst for a in cst]))
     lo_r = lo.repeat(nt).contiguous()
     hi_r = hi.repeat(nt).contiguous()
     ref_r = ref.repeat(nt, 1).contiguous()
@@ -184,7 +191,6 @@ def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
     acc = empty((nt, hw), torch.float64)
     N.call("qfca_reduce_partials", partial.data_ptr(), nt, groups, hw, ones.data_ptr(),
            acc.data_ptr(), s)
-    ro, rl, co, cl = _tile_index(h, w, cfg.patch_size, bins.device, rown, rloc, cown, cloc)
     a4 = acc.view(len(rst), len(cst), th, STRIP_W)
     return a4[ro, co, rl, cl].contiguous()  # (h, w)
 
@@ -192,14 +198,17 @@ def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
 _TILE_IDX: dict = {}
 
 
-def _tile_index(h, w, t, dev, rown, rloc, cown, cloc):
-    """Owner / local index tensors of the tile decomposition, cached on the device."""
+def _tile_index(h, w, t, dev, rst, rown, rloc, cst, cown, cloc):
+    """Owner / local index tensors and tile starts of the decomposition, cached
+    on the device."""
     key = (h, w, t, str(dev))
     if key not in _TILE_IDX:
         _TILE_IDX[key] = (torch.as_tensor(rown, device=dev)[:, None],
                           torch.as_tensor(rloc, device=dev)[:, None],
                           torch.as_tensor(cown, device=dev)[None, :],
-                          torch.as_tensor(cloc, device=dev)[None, :])
+                          torch.as_tensor(cloc, device=dev)[None, :],
+                          torch.as_tensor(rst, dtype=torch.int32, device=dev),
+                          torch.as_tensor(cst, dtype=torch.int32, device=dev))
     return _TILE_IDX[key]
 
 
