@@ -282,8 +282,8 @@ def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
     for i in range(b):
         acc, used, flag = _channel_partial(x[i], cfg)
         out.nonfinite.bitwise_or_(flag)
-        out.used[i] = used
-        agg = acc / used if used > 0 else acc
+        out.used[i:i + 1] = used
+        agg = acc / used.clamp(min=1).to(torch.float64)  # all degenerate: zeros
         final = sep_convolve_dev(agg[None].contiguous(), taps, cfg.pad)[0] \
             if taps is not None else agg
         out.scores[i] = final

@@ -79,14 +79,20 @@ def shard_batch(batch: torch.Tensor, world: int, rank: int) -> torch.Tensor:
 def combine_partials(acc: torch.Tensor, used: int | torch.Tensor, group=None):
     """All-reduce(sum) of a rank's channel-sum map and used-channel count.
 
-    One collective on an (h*w + 1) fp64 buffer.  Returns (sum map, total used).
+    One collective on an (h*w + 1) fp64 buffer.  Returns (sum map, total used):
+    an int when ``used`` is an int, a 0-d device tensor (no host sync) when it
+    is a tensor.
     """
     import torch.distributed as dist
-    flat = torch.cat([acc.reshape(-1).to(torch.float64),
-                      torch.as_tensor([float(used)], dtype=torch.float64,
-                                      device=acc.device)])
+    if isinstance(used, torch.Tensor):
+        u = used.reshape(1).to(device=acc.device, dtype=torch.float64)
+    else:
+        u = torch.as_tensor([float(used)], dtype=torch.float64, device=acc.device)
+    flat = torch.cat([acc.reshape(-1).to(torch.float64), u])
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    if isinstance(used, torch.Tensor):
+        return flat[:-1].reshape(acc.shape), flat[-1]
     return flat[:-1].reshape(acc.shape), int(round(float(flat[-1])))
 
 
@@ -95,7 +101,7 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     channel slice (C_local, h, w), fused path (scoring.py:286-309 without the
     division)."""
     acc, used, _ = _channel_partial(values, cfg)
-    return acc, used
+    return acc, int(used[0])
 
 
 def wide_supported(cfg, h: int, w: int, c: int) -> bool:
@@ -142,13 +148,14 @@ def _channel_partial(values: torch.Tensor, cfg):
     acc = empty((1, hw), torch.float64)
     N.call("qfca_reduce_partials", partial.data_ptr(), 1, groups, hw, ones.data_ptr(),
            acc.data_ptr(), s)
-    return acc.reshape(h, w), int(used[0]), flag
+    return acc.reshape(h, w), used, flag
 
 
-def _used(lo, hi, c) -> int:
+def _used(lo, hi, c) -> torch.Tensor:
+    """(1,) int32 device count of non-degenerate channels (no host sync)."""
     used = empty((1,), torch.int32)
     N.call("qfca_count_used", lo.data_ptr(), hi.data_ptr(), 1, c, used.data_ptr(), N.stream())
-    return int(used[0])
+    return used
 
 
 def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
@@ -216,17 +223,18 @@ def detect_channel_sharded(values_local: torch.Tensor, cfg=None, group=None):
     """Score one image whose channels are split across the ranks.
 
     ``values_local`` is this rank's (C_local, h, w) slice on its GPU.  Returns
-    (scores (h, w) fp64, image_score, degenerate) on every rank.
+    (scores (h, w) fp64, image_score, degenerate) on every rank; the last two
+    are 0-d device tensors (float() / bool() them), so a step has no host sync.
     """
     from .scoring import PipelineConfig
     cfg = cfg or PipelineConfig()
-    acc, used = channel_partial(values_local, cfg)
+    acc, used, _ = _channel_partial(values_local, cfg)
     total, used_all = combine_partials(acc, used, group)
     h, w = total.shape
-    agg = total / used_all if used_all > 0 else total
+    agg = total / used_all.clamp(min=1.0)  # all degenerate: the sum map is all zeros
     final = sep_convolve_dev(agg[None].contiguous(), _gauss_kernel(cfg.sigma_s), cfg.pad)[0] \
         if cfg.sigma_s > 0 else agg
     img = empty((1,), torch.float64)
     N.call("qfca_image_score", final.contiguous().data_ptr(), 1, h, w, cfg.border,
            img.data_ptr(), N.stream())
-    return final, float(img[0]), used_all == 0
+    return final, img[0], used_all == 0
