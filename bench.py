@@ -66,12 +66,15 @@ class ClockSampler:
                 self.samples.append([p.strip() for p in line.split(",")])
 
     def __enter__(self):
-        # one long-running nvidia-smi sampling every 50 ms (a fresh process
-        # per sample is too slow for sub-second timed regions)
+        # one long-running nvidia-smi sampling every 200 ms (a fresh process
+        # per sample is too slow for sub-second timed regions; 50 ms polling was
+        # measured to perturb the timed GPU work: configs[4] steps 23.7 ms
+        # unsampled vs 23.8-33.8 ms at 50 ms)
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms",
+                 os.environ.get("QFCA_BENCH_SMI_MS", "200")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._thr = threading.Thread(target=self._run, daemon=True)
             self._thr.start()
