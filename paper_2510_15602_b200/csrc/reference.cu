@@ -112,11 +112,20 @@ k_reference(const BT* __restrict__ bins, const float* __restrict__ lo,
                     if (j == 0 || g.stride >= g.t) {
 #pragma unroll
                         for (int k = 0; k < REF_NW; ++k) st[k] = 0u;
-                        for (int dy = 0; dy < g.t; ++dy) {
-                            uint32_t a[REF_NW];
-                            onehot_words<LANE>(row_bin(ys + dy), i0, a);
+                        // the window's rows in batches of 8 independent loads (one
+                        // memory latency per batch instead of one per row)
+                        for (int d0 = 0; d0 < g.t; d0 += 8) {
+                            int bv[8];
 #pragma unroll
-                            for (int k = 0; k < REF_NW; ++k) st[k] += a[k];
+                            for (int q = 0; q < 8; ++q) bv[q] = d0 + q < g.t ? row_bin(ys + d0 + q) : -1;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                if (bv[q] < 0) continue;
+                                uint32_t a[REF_NW];
+                                onehot_words<LANE>(bv[q], i0, a);
+#pragma unroll
+                                for (int k = 0; k < REF_NW; ++k) st[k] += a[k];
+                            }
                         }
                     } else {
                         for (int d = 0; d < g.stride; ++d) {
