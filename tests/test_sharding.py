@@ -96,3 +96,28 @@ def test_channel_partials_gpu():
     ref, img_ref, _ = O.detect(x)
     assert np.abs(final.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
     assert not degen
+
+
+def test_strip_geometry():
+    """sharding.strips: every column owned by exactly one segment, owned outputs
+    at least 2R columns from a segment's inner edges (so the segment's own border
+    padding never reaches them), true borders at segment borders."""
+    from paper_2510_15602_b200.sharding import strips
+    for w in (129, 200, 257, 300, 1000, 1024, 4096):
+        for t in (1, 3, 5, 9, 15):
+            for sw in (128, 256):
+                if w <= sw:
+                    st, own, loc = strips(w, t, sw)
+                    assert st == [0] and (own == 0).all() and (loc == np.arange(w)).all()
+                    continue
+                st, own, loc = strips(w, t, sw)
+                halo = 2 * (t // 2)
+                assert st[0] == 0 and st[-1] + sw == w
+                assert (np.diff(own) >= 0).all()
+                for x in range(w):
+                    a = st[own[x]]
+                    assert 0 <= x - a < sw and loc[x] == x - a
+                    if own[x] > 0:
+                        assert x - a >= halo              # far from the left inner edge
+                    if own[x] < len(st) - 1:
+                        assert a + sw - 1 - x >= halo     # far from the right inner edge
