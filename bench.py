@@ -299,19 +299,25 @@ def main():
         peak_src = "measured"
     alg = alg_bytes_per_image(size, pca_k > 0) * per_gpu
     achieved = alg / (score_ms / 1e3) / 1e9
-    traffic = None
+    traffic, issue = None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("dram_bytes_per_launch")
+            # K4 is issue-bound, not HBM-bound: its instruction-issue
+            # utilisation from the same ncu capture is the kernel-quality figure
+            issue = {"issue_active_frac": tj.get("issue_active_frac"), "ipc": tj.get("ipc"),
+                     "ipc_peak": 4.0, "source": tj.get("source")}
         except Exception:
-            traffic = None
+            traffic, issue = None, None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "kernel": "k_score (fused histogram/transport/association/channel-sum)",
             "kernel_ms_per_launch": score_ms, "step_ms": ms_per_step,
             "kernel_share_of_step": score_ms / ms_per_step,
-            "step_alg_bytes_frac": (alg / (ms_per_step / 1e3) / 1e9) / peak}
+            "step_alg_bytes_frac": (alg / (ms_per_step / 1e3) / 1e9) / peak,
+            "issue": issue}
 
     # ---- CPU baseline (rank 0, N = 1 only): the oracle on host cores
     cpu = None
