@@ -212,6 +212,7 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
     __shared__ int8_t sched[EIG_MAXP - 1][EIG_MAXP];  // round -> player per position
     __shared__ int srank[EIG_MAXP];
     __shared__ int any_rot[2];  // per sweep parity: set by rotations, reset a sweep ahead
+    __shared__ double s_tol;
     const int tid = threadIdx.x;
     const int64_t m = blockIdx.x;
     const int n = p + (p & 1);  // players incl. a dummy when p is odd
@@ -223,6 +224,15 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
         V[r][c] = r == c ? 1.0 : 0.0;
     }
     if (tid == 0) any_rot[0] = 0;
+    __syncthreads();
+    if (tid == 0) {
+        // rotations stop once an off-diagonal entry is below 1e-16 of the largest
+        // |diagonal| (~lambda_1): what is left perturbs eigenvalues by < 1e-16
+        // lambda_1 and the well-separated top eigenvectors by ~1e-16 lambda_1 / gap
+        double md = 0.0;
+        for (int i = 0; i < p; ++i) md = fmax(md, fabs(A[i][i]));
+        s_tol = 1e-16 * md;
+    }
     // circle method: position 0 fixed, the others rotate by one per round
     for (int i = tid; i < (n - 1) * n; i += JAC_THREADS) {
         const int rnd = i / n, pos = i % n;
@@ -241,7 +251,7 @@ k_sym_eig(const double* __restrict__ h, int64_t batch, int p, double* __restrict
                     app = A[a][a];
                     aqq = A[b][b];
                     // skip entries already negligible against their diagonal pair
-                    if (apq != 0.0 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+                    if (fabs(apq) > s_tol && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
                         // t = tan(theta) = sgn(d) 2 apq / u with d = aqq - app,
                         // u = |d| + sqrt(d^2 + 4 apq^2); c = u / sqrt(u^2 + 4 apq^2),
                         // s = t c: one sqrt, then rsqrt and 1/u side by side
