@@ -467,9 +467,8 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     const uint32_t wlo = g1 ? v.y : v.x, whi = g1 ? v.w : v.z;
                     const uint32_t plo = g1 ? v.x : 0u, phi = g1 ? v.z : v.y;
                     const uint32_t word = g2 ? whi : wlo, prev = g2 ? phi : plo;
-                    const bool mass = (word >> 24) != (prev >> 24);
-                    float E[4] = {0.f, 0.f, 0.f, 0.f};  // warp without mass in the group: E = 0
-                    if (__any_sync(0xffffffffu, mass)) {
+                    float E[4] = {0.f, 0.f, 0.f, 0.f};
+                    {
                         uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
                         uint32_t aa = gaddr + 4u * ma;
 #define S4_E(J)                                                                 \
