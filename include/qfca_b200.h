@@ -195,12 +195,16 @@ int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, doubl
 /* Block Lanczos (8-column blocks, full reorthogonalisation) on a batch of
  * symmetric C x C fp64 matrices (C % 64 == 0, C <= 512), the Krylov stage of the
  * top-k eigensolver replacing np.linalg.eigh of pca_fit (features.py:173):
- * q0 (C, 8) seeded start block R (the kernel starts from qr(cov R)); basis (batch, 8*passes, C) receives the
- * Krylov basis (vector-contiguous), h (batch, n, n) row-major the upper block
- * triangle of H = basis^T cov basis (n = 8*passes <= C, passes <= 32);
- * passes + 1 sweeps over cov in all. */
+ * q0 (C, 8) seeded start block R (the kernel starts from qr(cov R)); basis
+ * (batch, 8*passes, C) receives the Krylov basis (vector-contiguous), h
+ * (batch, n, n) row-major the upper block triangle of H = basis^T cov basis
+ * (n = 8*passes <= C, passes <= 32); passes + 1 sweeps over cov in all.
+ * With twin_basis (same shape as basis), exchange (batch * 4 * C * 8 doubles)
+ * and flags (batch int32, zeroed) non-NULL, each matrix runs on a cluster of
+ * two CTAs that split the passes over cov; NULL: one CTA per matrix. */
 int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, const double* q0,
-                 double* basis, double* h, void* stream);
+                 double* basis, double* h, double* twin_basis, double* exchange,
+                 int32_t* flags, void* stream);
 
 /* Top-32 subspace of the Lanczos projection (batch, n, n), n <= 128, n % 8 == 0,
  * as qfca_lanczos writes it (upper block triangle): x <- qr(H (H x)) for `iters`

@@ -62,7 +62,7 @@ _SIGNATURES = {
     "qfca_cholqr": ([_P, _I64, _I32, _I32, _P], _I32),
     "qfca_chol_rinv": ([_P, _I64, _I32, _P, _P], _I32),
     "qfca_sym_eig": ([_P, _I64, _I32, _P, _P, _P], _I32),
-    "qfca_lanczos": ([_P, _I64, _I32, _I32, _P, _P, _P, _P], _I32),
+    "qfca_lanczos": ([_P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "qfca_ritz": ([_P, _I64, _I32, _P, _I32, _P, _P, _P], _I32),
     "qfca_gather_tiles": ([_P, _I32, _I32, _I32, _P, _I32, _P, _I32, _I32, _I32, _P, _P], _I32),
     "qfca_covariance_workspace_bytes": ([_I64, _I32, _I32], _I64),

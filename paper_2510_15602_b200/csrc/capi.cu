@@ -44,7 +44,8 @@ int launch_cholqr(double*, int64_t, int, int, cudaStream_t);
 int64_t cov_i8_workspace(int64_t, int, int);
 int launch_chol_rinv(const double*, int64_t, int, double*, cudaStream_t);
 int launch_sym_eig(const double*, int64_t, int, double*, double*, cudaStream_t);
-int launch_lanczos(const double*, int64_t, int, int, const double*, double*, double*, cudaStream_t);
+int launch_lanczos(const double*, int64_t, int, int, const double*, double*, double*, double*,
+                   double*, int*, cudaStream_t);
 int launch_ritz(const double*, int64_t, int, const double*, int, double*, double*, cudaStream_t);
 int launch_gather_tiles(const void*, int, int, int, const int*, int, const int*, int, int, int, void*,
                         cudaStream_t);
@@ -336,8 +337,10 @@ int qfca_sym_eig(const double* h, int64_t batch, int32_t p, double* evals, doubl
 }
 
 int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, const double* q0,
-                 double* basis, double* h, void* stream) {
-    return counted(launch_lanczos(cov, batch, C, passes, q0, basis, h, S(stream)), 1);
+                 double* basis, double* h, double* twin_basis, double* exchange,
+                 int32_t* flags, void* stream) {
+    return counted(launch_lanczos(cov, batch, C, passes, q0, basis, h, twin_basis, exchange,
+                                  flags, S(stream)), 1);
 }
 
 int qfca_ritz(const double* h, int64_t batch, int32_t n, const double* x0, int32_t iters,

@@ -121,16 +121,17 @@ __host__ __device__ inline LzSmem lz_layout(int C, int n) {
 // projection 2 (j+1 blocks each).  A dedicated producer warp walks the same
 // program: it refills a slot as soon as all 8 consumer warps have released it
 // (empty mbarrier), so the consumers never meet at a CTA barrier per chunk.
-__host__ __device__ inline int lz_pass_chunks(int C, int P, int j) {
+__host__ __device__ inline int lz_pass_chunks(int nS, int P, int j) {
     const int nb = j + 1;
     const int nsweep = j < 0 ? 0 : (j == P - 1 ? 1 : 4);
-    return C / LZ_KC + nsweep * nb;
+    return nS + nsweep * nb;  // nS: this CTA's S chunks
 }
 
 template <int NT>  // 8-row tiles per warp: C = 64 NT
 __global__ void __launch_bounds__(LZ_CTA, 1)
 k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__ Q0,
-          double* __restrict__ Bm, double* __restrict__ H) {
+          double* __restrict__ Bm, double* __restrict__ H, double* __restrict__ Bm2,
+          double* __restrict__ Wx, int* __restrict__ flags, int split) {
     extern __shared__ __align__(128) uint8_t lz_sm[];
     __shared__ __align__(8) uint64_t full[LZ_NST], empty[LZ_NST];
     const int n = P * LZ_BW;
@@ -143,11 +144,19 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
     double* const G = reinterpret_cast<double*>(lz_sm + L.o_g);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int lr = lane >> 2, lc = lane & 3;
-    const int img = blockIdx.x;
+    // split == 2: a cluster of two CTAs per image.  Each CTA streams half of the
+    // rows of S (half the S-pass MMAs and bytes), the two partial W = S Q_j are
+    // exchanged through global memory (one flag handshake per pass; the cluster
+    // launch guarantees both CTAs are resident), and everything after the S
+    // pass runs redundantly in both (bit-identical inputs, each CTA streams its
+    // own copy of the basis); CTA 0 writes H and the output basis.
+    const int img = blockIdx.x / split, half = blockIdx.x % split;
     const double* const Si = S + (size_t)img * C * C;
-    double* const Bi = Bm + (size_t)img * n * C;
+    double* const Bi = (half ? Bm2 : Bm) + (size_t)img * n * C;
     double* const Hi = H + (size_t)img * n * n;
-    const int nS = C / LZ_KC;
+    const int nS_all = C / LZ_KC;
+    const int c_lo = half * (nS_all / split);
+    const int nS = split == 2 ? (half ? nS_all - nS_all / 2 : nS_all / 2) : nS_all;
 
     if (tid == 0) {
         for (int s = 0; s < LZ_NST; ++s) {
@@ -157,7 +166,8 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < C * LZ_BW; i += LZ_CTA) Ws[i] = Q0[i];
-    for (int i = tid; i < n * n; i += LZ_CTA) Hi[i] = 0.0;
+    if (half == 0)
+        for (int i = tid; i < n * n; i += LZ_CTA) Hi[i] = 0.0;
     __syncthreads();
 
     if (warp == LZ_NW) {
@@ -165,13 +175,13 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
         if (lane == 0) {
             uint32_t k = 0;  // kernel-wide chunk counter
             for (int j = -1; j < P; ++j) {
-                const int nb = j + 1, nch = lz_pass_chunks(C, P, j);
+                const int nb = j + 1, nch = lz_pass_chunks(nS, P, j);
                 for (int c = 0; c < nch; ++c, ++k) {
                     const int s = k % LZ_NST;
                     if (k >= LZ_NST) lz_mbar_wait(lz_smem(&empty[s]), ((k / LZ_NST) - 1) & 1u);
                     // basis chunks are written by the consumers one pass earlier; the
                     // empty-barrier wait orders their (proxy-fenced) stores before this copy
-                    const double* src = c < nS ? Si + (size_t)c * LZ_KC * C
+                    const double* src = c < nS ? Si + (size_t)(c_lo + c) * LZ_KC * C
                                                : Bi + (size_t)((c - nS) % nb) * LZ_KC * C;
                     const uint32_t bar = lz_smem(&full[s]);
                     lz_mbar_expect_tx(bar, (uint32_t)LZ_KC * C * 8);
@@ -180,7 +190,7 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
                         lz_bulk_load(lz_smem(dst + rr * CP), src + (size_t)rr * C, (uint32_t)C * 8,
                                      bar);
                     if (c + LZ_PF < nS)  // S rows further ahead: into L2
-                        lz_prefetch_l2(Si + (size_t)(c + LZ_PF) * LZ_KC * C,
+                        lz_prefetch_l2(Si + (size_t)(c_lo + c + LZ_PF) * LZ_KC * C,
                                        (uint32_t)LZ_KC * C * 8);
                 }
             }
@@ -225,13 +235,41 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
             const double* st = acquire();
 #pragma unroll
             for (int ks = 0; ks < LZ_KC / 4; ++ks) {
-                const double b = Ws[(c * LZ_KC + 4 * ks + lc) * LZ_BW + lr];  // Q[k][q]
+                const double b = Ws[((c_lo + c) * LZ_KC + 4 * ks + lc) * LZ_BW + lr];  // Q[k][q]
                 const double* arow = st + (4 * ks + lc) * CP + wr0 + lr;      // S[k][r]
 #pragma unroll
                 for (int t = 0; t < NT; ++t)
                     lz_dmma(acc[t][0], acc[t][1], arow[8 * t], b);
             }
             release();
+        }
+        if (split == 2) {
+            // ---- exchange the partial W with the other CTA of the pair (buffers
+            // alternate by pass parity: a buffer is rewritten only after the
+            // partner has signalled the following pass, i.e. finished reading it)
+            const int par = (j + 1) & 1;
+            double* mine = Wx + (((size_t)img * 2 + par) * 2 + half) * C * LZ_BW;
+            const double* other = Wx + (((size_t)img * 2 + par) * 2 + (1 - half)) * C * LZ_BW;
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                __stcg(reinterpret_cast<double2*>(mine + (wr0 + 8 * t + lr) * LZ_BW + 2 * lc),
+                       make_double2(acc[t][0], acc[t][1]));
+            __threadfence();
+            lz_csync();
+            if (tid == 0) {
+                atomicAdd(flags + img, 1);
+                const int target = 2 * (j + 2);
+                while (atomicAdd(flags + img, 0) < target) __nanosleep(64);
+                __threadfence();
+            }
+            lz_csync();
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const double2 o =
+                    __ldcg(reinterpret_cast<const double2*>(other + (wr0 + 8 * t + lr) * LZ_BW + 2 * lc));
+                acc[t][0] += o.x;  // a + b == b + a: both CTAs hold the same W
+                acc[t][1] += o.y;
+            }
         }
 
         // coefficient sweep: cf[8 i + c][q] = B_i[c] . W[:, q]; warp = row slice,
@@ -283,8 +321,9 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
         const int cols = nb * LZ_BW;
         if (j >= 0) {
             coef_sweep();  // block column j of H
-            for (int i = tid; i < cols * LZ_BW; i += LZ_THREADS)
-                Hi[(size_t)(i / LZ_BW) * n + j * LZ_BW + (i % LZ_BW)] = cf[i];
+            if (half == 0)
+                for (int i = tid; i < cols * LZ_BW; i += LZ_THREADS)
+                    Hi[(size_t)(i / LZ_BW) * n + j * LZ_BW + (i % LZ_BW)] = cf[i];
             if (j == P - 1) break;
             proj_sweep();
             coef_sweep();
@@ -395,12 +434,14 @@ k_lanczos(const double* __restrict__ S, int C, int P, const double* __restrict__
 size_t lanczos_smem(int C, int P) { return (size_t)lz_layout(C, P * LZ_BW).total; }
 
 int launch_lanczos(const double* S, int64_t batch, int C, int P, const double* Q0, double* Bm,
-                   double* H, cudaStream_t st) {
+                   double* H, double* Bm2, double* Wx, int* flags, cudaStream_t st) {
     if (batch <= 0 || C <= 0 || P <= 0) return QFCA_ERR_ARG;
     if (C > LZ_MAXC || C % 64 || P > LZ_MAXP || P * LZ_BW > C) return QFCA_ERR_UNSUPPORTED;
+    if (C % (2 * LZ_KC)) return QFCA_ERR_UNSUPPORTED;
     const size_t smem = lanczos_smem(C, P);
     if (smem > 227 * 1024) return QFCA_ERR_UNSUPPORTED;
-    void (*kern)(const double*, int, int, const double*, double*, double*) = nullptr;
+    void (*kern)(const double*, int, int, const double*, double*, double*, double*, double*, int*,
+                 int) = nullptr;
     switch (C / 64) {
         case 1: kern = k_lanczos<1>; break;
         case 2: kern = k_lanczos<2>; break;
@@ -414,7 +455,26 @@ int launch_lanczos(const double* S, int64_t batch, int C, int P, const double* Q
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return QFCA_ERR_CUDA;
-    kern<<<(unsigned)batch, LZ_CTA, smem, st>>>(S, C, P, Q0, Bm, H);
+    const int split = (Bm2 && Wx && flags) ? 2 : 1;
+    if (split == 1) {
+        kern<<<(unsigned)batch, LZ_CTA, smem, st>>>(S, C, P, Q0, Bm, H, Bm2, Wx, flags, 1);
+        return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+    }
+    // two-CTA clusters: the pair is co-scheduled, so the flag handshake cannot deadlock
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * batch));
+    cfg.blockDim = dim3(LZ_CTA);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, S, C, P, Q0, Bm, H, Bm2, Wx, flags, 2) != cudaSuccess)
+        return QFCA_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 

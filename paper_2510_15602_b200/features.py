@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._dev import empty, is_torch, to_dev, to_host
+from ._dev import empty, is_torch, to_dev, to_host, zeros
 
 __all__ = ["FeatureMap", "PcaModel", "pca_fit", "pca_residual", "pca_fit_batch",
            "pca_residual_batch", "gaussian_blur", "FormatError"]
@@ -237,6 +237,7 @@ def sym_eig(h: torch.Tensor):
 
 LANCZOS_BW, LANCZOS_PASSES = 8, 16  # csrc/lanczos.cu block width; passes over cov
 LANCZOS_DIM = LANCZOS_BW * LANCZOS_PASSES
+LANCZOS_SPLIT = True  # two-CTA clusters per covariance (csrc/lanczos.cu)
 
 
 def _topk_eigh_lanczos(cov: torch.Tensor, k: int, block: int, iters: int):
@@ -253,8 +254,16 @@ def _topk_eigh_lanczos(cov: torch.Tensor, k: int, block: int, iters: int):
     q0 = _start_block(c, LANCZOS_BW, cov.device).contiguous()
     basis = empty((b, n, c), torch.float64)
     h = empty((b, n, n), torch.float64)
-    N.call("qfca_lanczos", cov.data_ptr(), b, c, LANCZOS_PASSES, q0.data_ptr(),
-           basis.data_ptr(), h.data_ptr(), N.stream())
+    if LANCZOS_SPLIT:  # two CTAs per matrix (cluster), partial S Q exchanged per pass
+        twin = empty((b, n, c), torch.float64)
+        xch = empty((b, 4, c, LANCZOS_BW), torch.float64)
+        flags = zeros((b,), torch.int32)
+        N.call("qfca_lanczos", cov.data_ptr(), b, c, LANCZOS_PASSES, q0.data_ptr(),
+               basis.data_ptr(), h.data_ptr(), twin.data_ptr(), xch.data_ptr(),
+               flags.data_ptr(), N.stream())
+    else:
+        N.call("qfca_lanczos", cov.data_ptr(), b, c, LANCZOS_PASSES, q0.data_ptr(),
+               basis.data_ptr(), h.data_ptr(), None, None, None, N.stream())
     p = 32
     x0 = _start_block(n, p, cov.device).contiguous()
     x = empty((b, n, p), torch.float64)

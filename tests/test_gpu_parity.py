@@ -369,9 +369,10 @@ def test_detect_pipeline_matches_detect_batch(Q, pinned):
         assert torch.equal(up, Q.upsample_batch(ref.scores, 64, 64).cpu())
 
 
-@pytest.mark.parametrize("c", [512, 384, 256])
-def test_lanczos_basis_and_projection(Q, c):
-    """csrc/lanczos.cu: the Krylov basis is orthonormal and H = B^T S B."""
+@pytest.mark.parametrize("c,split", [(512, True), (512, False), (384, True), (256, False)])
+def test_lanczos_basis_and_projection(Q, c, split):
+    """csrc/lanczos.cu: the Krylov basis is orthonormal and H = B^T S B, with one
+    CTA per matrix and with two-CTA clusters (which must agree bit for bit)."""
     from paper_2510_15602_b200 import features as F
     from paper_2510_15602_b200 import _native as N
     g = torch.Generator().manual_seed(c)
@@ -380,10 +381,24 @@ def test_lanczos_basis_and_projection(Q, c):
     s = (a @ a.mT / (2 * c)).cuda()
     n = F.LANCZOS_DIM
     q0 = F._start_block(c, F.LANCZOS_BW, s.device).contiguous()
-    basis = torch.empty((3, n, c), dtype=torch.float64, device="cuda")
-    h = torch.empty((3, n, n), dtype=torch.float64, device="cuda")
-    N.call("qfca_lanczos", s.data_ptr(), 3, c, F.LANCZOS_PASSES, q0.data_ptr(),
-           basis.data_ptr(), h.data_ptr(), N.stream())
+
+    def run(two):
+        basis = torch.empty((3, n, c), dtype=torch.float64, device="cuda")
+        h = torch.empty((3, n, n), dtype=torch.float64, device="cuda")
+        if two:
+            twin = torch.empty_like(basis)
+            xch = torch.empty((3, 4, c, F.LANCZOS_BW), dtype=torch.float64, device="cuda")
+            flags = torch.zeros((3,), dtype=torch.int32, device="cuda")
+            N.call("qfca_lanczos", s.data_ptr(), 3, c, F.LANCZOS_PASSES, q0.data_ptr(),
+                   basis.data_ptr(), h.data_ptr(), twin.data_ptr(), xch.data_ptr(),
+                   flags.data_ptr(), N.stream())
+            assert torch.equal(twin, basis)  # both CTAs ran the same arithmetic
+        else:
+            N.call("qfca_lanczos", s.data_ptr(), 3, c, F.LANCZOS_PASSES, q0.data_ptr(),
+                   basis.data_ptr(), h.data_ptr(), None, None, None, N.stream())
+        return basis, h
+
+    basis, h = run(split)
     eye = torch.eye(n, dtype=torch.float64, device="cuda")
     assert float((basis @ basis.mT - eye).abs().max()) < 1e-12
     hs = torch.triu(h) + torch.triu(h, 1).mT

@@ -21,7 +21,7 @@ q0 = F._start_block(c, F.LANCZOS_BW, cov.device).contiguous()
 basis = torch.empty((b, n, c), dtype=torch.float64, device="cuda")
 h = torch.empty((b, n, n), dtype=torch.float64, device="cuda")
 lz = lambda: N.call("qfca_lanczos", cov.data_ptr(), b, c, F.LANCZOS_PASSES, q0.data_ptr(),
-                    basis.data_ptr(), h.data_ptr(), N.stream())
+                    basis.data_ptr(), h.data_ptr(), None, None, None, N.stream())
 lz()
 hs = torch.triu(h) + torch.triu(h, 1).mT
 p = 32

@@ -14,5 +14,5 @@ basis = torch.empty((b, n, c), dtype=torch.float64, device="cuda")
 h = torch.empty((b, n, n), dtype=torch.float64, device="cuda")
 for _ in range(3):
     N.call("qfca_lanczos", cov.data_ptr(), b, c, F.LANCZOS_PASSES, q0.data_ptr(),
-           basis.data_ptr(), h.data_ptr(), N.stream())
+           basis.data_ptr(), h.data_ptr(), None, None, None, N.stream())
 torch.cuda.synchronize()
