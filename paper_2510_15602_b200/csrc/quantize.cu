@@ -239,7 +239,7 @@ k_quantize_plane(const float* __restrict__ x, int plane_len, int n_bins, float* 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float4* p4 = reinterpret_cast<const float4*>(x + plane * plane_len);
     float mn = INFINITY, mx = -INFINITY;
-    bool bad = false;
+    float nf = 0.f;  // v * 0 is NaN exactly for inf / NaN v: one FMA per value
     if (tid == 0) sbad = 0;
 #pragma unroll 4
     for (int i = tid; i < plane_len / 4; i += FQ_THREADS) {
@@ -247,11 +247,11 @@ k_quantize_plane(const float* __restrict__ x, int plane_len, int n_bins, float* 
         reinterpret_cast<float4*>(fq_x)[i] = v;
         mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
         mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+        nf = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, nf))));
     }
     mn = warp_min(mn);
     mx = warp_max(mx);
-    bad = __any_sync(0xffffffffu, bad);
+    const bool bad = __any_sync(0xffffffffu, nf != nf);
     __syncthreads();
     if (lane == 0) {
         smn[warp] = mn;
