@@ -25,6 +25,7 @@ from .scoring import (AnomalyMap, DetectResult, PipelineConfig, aggregate_channe
 from .transport import (IllConditionedError, MassError, mismatch_batch,
                         quantized_mismatch)
 from .pipeline import DetectPipeline, HostResult
+from . import exporter, tensor_io  # feature backbone on the GPU, QTF1 feature files
 
 __all__ = [
     "FeatureMap", "FormatError", "PcaModel", "gaussian_blur", "pca_fit", "pca_residual",
@@ -34,5 +35,5 @@ __all__ = [
     "associate_errors", "bin_error_maps", "channel_error_maps", "detect", "detect_batch",
     "fused_supported", "image_score_of", "smooth_scores", "upsample_batch",
     "upsample_scores", "IllConditionedError", "MassError", "mismatch_batch",
-    "quantized_mismatch", "DetectPipeline", "HostResult",
+    "quantized_mismatch", "DetectPipeline", "HostResult", "exporter", "tensor_io",
 ]

@@ -485,3 +485,40 @@ def test_wide_plane_detect_batch(Q):
         assert rel_err(res.scores[i].cpu().numpy(), ref) <= TOL
         assert abs(float(res.image_scores[i]) - img) <= TOL * np.abs(ref).max()
         assert int(res.used[i]) == 5
+
+
+def test_read_features_to_device(Q, tmp_path):
+    """QTF1 feature files -> pinned host buffer -> device batch, then detect."""
+    rng = np.random.default_rng(8)
+    xs = [np.maximum(rng.standard_normal((12, 32, 32)), 0).astype(np.float32) for _ in range(3)]
+    paths = []
+    for i, a in enumerate(xs):
+        p = tmp_path / f"f{i}.qtf"
+        Q.tensor_io.write_tensor(a, p)
+        paths.append(str(p))
+    dev = Q.tensor_io.read_features(paths)
+    torch.cuda.synchronize()
+    assert dev.is_cuda and tuple(dev.shape) == (3, 12, 32, 32)
+    np.testing.assert_array_equal(dev.cpu().numpy(), np.stack(xs))
+    res = Q.detect_batch(dev, Q.PipelineConfig())
+    ref = Q.detect_batch(torch.from_numpy(np.stack(xs)).cuda(), Q.PipelineConfig())
+    assert torch.equal(res.scores, ref.scores)
+
+
+def test_exporter_matches_cpu_trunk(Q):
+    """exporter.extract_features (WRN50-2 conv1..layer2 on the GPU, fp32) vs the
+    same random-init trunk on the CPU (the reference exporter's arithmetic,
+    export.py:71-143) on a small image batch."""
+    from paper_2510_15602_b200 import exporter as E
+    g = torch.Generator().manual_seed(3)
+    imgs = torch.randint(0, 256, (2, 3, 64, 64), dtype=torch.uint8, generator=g)
+    trunk = E.build_backbone("random")
+    got = E.extract_features(trunk, imgs.cuda())
+    assert tuple(got.shape) == (2, 512, 8, 8)
+    cpu = E.build_backbone("random", device=torch.device("cpu"))
+    with torch.no_grad():
+        ref = cpu(E.normalize(imgs))
+    err = float((got.cpu() - ref).abs().max() / ref.abs().max())
+    assert err < 1e-4, err
+    with pytest.raises(E.WeightsError):
+        E.build_backbone("/nonexistent/weights.pth")
