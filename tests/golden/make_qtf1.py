@@ -14,5 +14,6 @@ feats = np.maximum(rng.standard_normal((6, 5, 7)), 0).astype(np.float32)
 T.write_tensor(T.Tensor.from_array(feats), os.path.join(OUT, "qtf1_features_6x5x7.qtf"))
 img = rng.integers(0, 256, (3, 4, 2), dtype=np.uint8)
 T.write_tensor(T.Tensor.from_array(img), os.path.join(OUT, "qtf1_uint8_3x4x2.qtf"))
-np.savez_compressed(os.path.join(OUT, "qtf1_arrays.npz"), feats=feats, img=img)
+np.save(os.path.join(OUT, "qtf1_feats.npy"), feats)
+np.save(os.path.join(OUT, "qtf1_img.npy"), img)
 print("wrote QTF1 fixtures")

@@ -11,7 +11,8 @@ G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def test_reads_reference_files():
-    ref = np.load(os.path.join(G, "qtf1_arrays.npz"))
+    ref = {"feats": np.load(os.path.join(G, "qtf1_feats.npy")),
+           "img": np.load(os.path.join(G, "qtf1_img.npy"))}
     a = T.read_tensor(os.path.join(G, "qtf1_features_6x5x7.qtf"))
     assert a.dtype == np.float32 and a.shape == (6, 5, 7)
     np.testing.assert_array_equal(a, ref["feats"])
@@ -21,7 +22,8 @@ def test_reads_reference_files():
 
 
 def test_writes_reference_bytes(tmp_path):
-    ref = np.load(os.path.join(G, "qtf1_arrays.npz"))
+    ref = {"feats": np.load(os.path.join(G, "qtf1_feats.npy")),
+           "img": np.load(os.path.join(G, "qtf1_img.npy"))}
     for name, arr in (("qtf1_features_6x5x7.qtf", ref["feats"]), ("qtf1_uint8_3x4x2.qtf", ref["img"])):
         p = tmp_path / name
         T.write_tensor(arr, p)
