@@ -15,3 +15,5 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_sc
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_lanczos --launch-skip 2 -c 1 -o $O/prof_k_lanczos python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_score3 --launch-skip 2 -c 1 -o $O/prof_k_score3 python bench.py --workload qfca1024 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ls -la $O
+timeout 900 python bench.py --workload qfca8192 --steps 5 --warmup 3 > $O/bench_8192.json 2> $O/bench_8192.err; tail -c 300 $O/bench_8192.json
+timeout 900 ncu --nvtx --nvtx-include "qfca_step/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_step_plus512.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
