@@ -39,7 +39,6 @@ constexpr int LZ_THREADS = 256;  // consumers: 8 warps x 64 rows: C <= 512, C % 
 constexpr int LZ_NW = LZ_THREADS / 32;
 constexpr int LZ_CTA = LZ_THREADS + 32;  // + one producer warp (ring refills)
 constexpr int LZ_MAXC = 64 * LZ_NW;
-constexpr int LZ_RT = 8;         // max 8-row tiles per warp
 constexpr int LZ_KC = 8;         // rows per ring chunk
 constexpr int LZ_NST = 5;        // ring stages
 constexpr int LZ_MAXP = 32;      // passes (n = 8 P <= 256)

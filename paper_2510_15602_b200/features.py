@@ -1,10 +1,11 @@
 """Feature maps and PCA-residual preprocessing on the GPU.
 
 Mirrors qfca.features (reference features.py:26-41, 49-77, 150-193): same
-names, same dataclasses, same validation and error types.  The covariance is
-an fp32 tensor-core-free GEMM split into K-chunks whose partial products are
-summed in fp64; the eigensolver is fp64; the residual kernel is ours
-(csrc/pca.cu).
+names, same dataclasses, same validation and error types.  pca_fit: plane
+means and the exact covariance on the int8 tensor cores (csrc/cov_i8.cu),
+top-k eigenpairs by block Lanczos on the fp64 tensor cores (csrc/lanczos.cu)
+plus the Ritz step on the small projection (csrc/eig.cu); pca_residual: fp64
+MMA kernel (csrc/residual.cu).
 """
 
 from __future__ import annotations
@@ -279,15 +280,16 @@ def topk_eigh(cov: torch.Tensor, k: int, block: int = 32, iters: int = 30,
     """Top-k eigenpairs of a batch of symmetric PSD matrices (B, C, C), fp64.
 
     Replaces the full ``np.linalg.eigh`` of features.py:173 (only the top-k
-    pairs are used, features.py:174-176): block subspace iteration (block p =
-    max(block, k) columns) on cov^2, re-orthonormalised by Cholesky QR (fp64
-    batched GEMMs for Y = S X and the Gram, csrc/eig.cu for R^-1), then a
-    Rayleigh-Ritz step on cov with a parallel-Jacobi eigensolver.  The error
-    of the k-th vector decays as (lambda_{p+1} / lambda_k)^iters; on
-    random-init WRN50-2 block-2 features (lambda_33 / lambda_10 ~ 0.2-0.33)
-    30 iterations reach the fp64 eigh to ~1e-15.  C <= p degenerates to an
-    exact eigen-decomposition of the whole matrix.  Returns (eigenvalues
-    (B, k) descending, vectors (B, C, k)).
+    pairs are used, features.py:174-176).  For 256 <= C <= 512 (C % 64 == 0)
+    block Lanczos over cov (``_topk_eigh_lanczos``), whose 128 x 128
+    projection goes through the path below.  Otherwise (and for that small
+    matrix): block subspace iteration (block p = max(block, k) columns) on
+    cov^2, re-orthonormalised by Cholesky QR, then a Rayleigh-Ritz step on cov
+    with a parallel-Jacobi eigensolver.  The error of the k-th vector decays as
+    (lambda_{p+1} / lambda_k)^iters; on random-init WRN50-2 block-2 features
+    (lambda_33 / lambda_10 ~ 0.2-0.33) 30 iterations reach the fp64 eigh to
+    ~1e-15.  C <= p degenerates to an exact eigen-decomposition of the whole
+    matrix.  Returns (eigenvalues (B, k) descending, vectors (B, C, k)).
     """
     b, c, _ = cov.shape
     p = min(c, max(block, k))
