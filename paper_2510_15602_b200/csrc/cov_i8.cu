@@ -307,6 +307,7 @@ k_cov_i8(const __grid_constant__ CUtensorMap tmap, int C, int Cp, int Kp, int hw
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int er = r < C ? expo[(int64_t)img * C + r] : 0;
         double* cimg = cov + (int64_t)img * C * C;
+        const double inv_hw = 1.0 / (double)hw;  // one division per thread, not per element
         for (int cc = 0; cc < CV_BN / 16; ++cc) {
             int32_t v[CV_CLS][16];
 #pragma unroll
@@ -324,7 +325,10 @@ k_cov_i8(const __grid_constant__ CUtensorMap tmap, int C, int Cp, int Kp, int hw
                 s += (double)v[1][j] * 16777216.0;                         // 256^3
                 s += (double)v[0][j] * 65536.0;                            // 256^2
                 const int ec = expo[(int64_t)img * C + col];
-                const double val = ldexp(s, er + ec - 64) / (double)hw;
+                // exact power-of-two scale (exponent field; er + ec - 64 stays in the
+                // normal range for fp32 inputs), then * 1/hw
+                const double p2 = __longlong_as_double((long long)(1023 + er + ec - 64) << 52);
+                const double val = (s * p2) * inv_hw;
                 cimg[(int64_t)r * C + col] = val;
                 cimg[(int64_t)col * C + r] = val;
             }
