@@ -185,22 +185,25 @@ k_cov_digits(const float* __restrict__ x, int C, int hw, int Cp, int Kp,
         uint32_t w[CV_DIG][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint32_t b[CV_DIG] = {0u, 0u, 0u, 0u};
+            // balanced digits n = d0 + 256 (d1 + 256 (d2 + 256 d3)), d0..d2 in
+            // [-128, 127]: the bytes of u = n + 0x808080 are d_k + 128 (k < 3, no
+            // carries) and d3, so the two's-complement digit bytes of one pixel
+            // are u ^ 0x808080; a 4 x 4 byte transpose then gives one word per digit
+            uint32_t u[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int p = p0 + 4 * q + j;
-                int n = 0;
-                if (p < hw) n = (int)rint(((double)xs[p] - mu) * sc);
-                // balanced digits: n = d0 + 256 (d1 + 256 (d2 + 256 d3)), d_k in [-128, 127]
-#pragma unroll
-                for (int k = 0; k < CV_DIG; ++k) {
-                    const int dk = k < CV_DIG - 1 ? (int)(int8_t)(n & 0xFF) : n;
-                    b[k] |= ((uint32_t)dk & 0xFFu) << (8 * j);
-                    n = (n - dk) >> 8;
-                }
+                const int n = p < hw ? (int)rint(((double)xs[p] - mu) * sc) : 0;
+                u[j] = ((uint32_t)n + 0x00808080u) ^ 0x00808080u;
             }
-#pragma unroll
-            for (int k = 0; k < CV_DIG; ++k) w[k][q] = b[k];
+            const uint32_t t01 = __byte_perm(u[0], u[1], 0x5140);  // d0: p0 p1, d1: p0 p1
+            const uint32_t t23 = __byte_perm(u[2], u[3], 0x5140);
+            const uint32_t h01 = __byte_perm(u[0], u[1], 0x7362);  // d2, d3 of p0 p1
+            const uint32_t h23 = __byte_perm(u[2], u[3], 0x7362);
+            w[0][q] = __byte_perm(t01, t23, 0x5410);
+            w[1][q] = __byte_perm(t01, t23, 0x7632);
+            w[2][q] = __byte_perm(h01, h23, 0x5410);
+            w[3][q] = __byte_perm(h01, h23, 0x7632);
         }
 #pragma unroll
         for (int k = 0; k < CV_DIG; ++k)
