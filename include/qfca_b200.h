@@ -237,6 +237,49 @@ int qfca_covariance(const float* x, int64_t images, int32_t C, int32_t hw, const
 int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, double* mean,
                          void* workspace, int64_t workspace_bytes, double* cov, void* stream);
 
+/* ---- evaluation metrics (metrics.py) ---- */
+
+/* Pooled interiors of a batch of maps (metrics.py:36-41 EvalSample.interior,
+ * 61-68 _pooled): scores (images, H, W) fp64 (scores_bytes 8) or fp32 (4),
+ * mask (images, H, W) uint8 -> out (images, H-2b, W-2b) fp64 and, if labels is
+ * not NULL, labels (same shape) uint8 0/1. */
+int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
+                       int32_t images, int32_t H, int32_t W, int32_t border, double* out,
+                       uint8_t* labels, void* stream);
+
+/* Rank statistics of pooled scores (metrics.py:44-58 _rank_auroc,
+ * 157-172 f1_optimal): one stable sort, then stats[0] = positives,
+ * stats[1] = 2 x the rank sum of the positives (average ranks for ties; exact),
+ * stats[2] = the bits of the best F1 over all thresholds (fp64).  sorted_out
+ * (n fp64, may be NULL) receives the ascending scores (for the PRO quantiles,
+ * metrics.py:87-92).  n < 2^31; workspace from qfca_rank_stats_workspace_bytes. */
+int64_t qfca_rank_stats_workspace_bytes(int64_t n);
+int qfca_rank_stats(const double* scores, const uint8_t* labels, int64_t n, void* workspace,
+                    int64_t workspace_bytes, double* sorted_out, uint64_t* stats, void* stream);
+
+/* 8-connected components of a batch of masks (metrics.py:80-84, scipy
+ * ndimage.label with a 3x3 structure), images x h x w uint8 -> comp (same
+ * shape) int32: -1 outside the masks, else the component number in raster
+ * order of first pixels, numbered across the batch (image 0 first);
+ * *n_comp (device int32) = number of components.  labels (may be NULL) gets
+ * the raster index of each pixel's component root.  images*h*w < 2^31. */
+int64_t qfca_components_workspace_bytes(int64_t n);
+int qfca_components(const uint8_t* mask, int32_t images, int32_t h, int32_t w, void* workspace,
+                    int64_t workspace_bytes, int32_t* labels, int32_t* comp, int32_t* n_comp,
+                    void* stream);
+
+/* PRO histograms (metrics.py:95-122): thr_asc (m <= 2048 ascending distinct
+ * thresholds); each pixel goes to slot #{thr <= score}.  comp_hist
+ * ((comp_hi - comp_lo), m + 1) int32 counts the pixels of components
+ * [comp_lo, comp_hi) (zeroed by the caller), normal_hist (m + 1) uint64 the
+ * pixels with comp < 0 (may be NULL). */
+int qfca_pro_histograms(const double* scores, const int32_t* comp, int64_t n,
+                        const double* thr_asc, int32_t m, int32_t comp_lo, int32_t comp_hi,
+                        int32_t* comp_hist, uint64_t* normal_hist, void* stream);
+/* pro[j] += (pixels >= thr_asc[j]) / size over the ncomp histograms in order
+ * (metrics.py:116-118); comp_hist is turned into suffix sums in place. */
+int qfca_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* pro, void* stream);
+
 /* ---- one-call detect (scoring.py:263-327) for the fused configuration ---- */
 typedef struct qfca_config {
     int32_t n_bins;        /* PipelineConfig.n_bins (16) */

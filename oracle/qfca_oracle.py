@@ -426,3 +426,109 @@ def detect(values, n_bins=16, patch_size=9, sigma_p=math.inf, sigma_s=1.0,
                       agg=agg, used=used)
         return final, score, degenerate, stages
     return final, score, degenerate
+
+
+# ---------------------------------------------------------------------------
+# Evaluation metrics (reference pkg/src/qfca/metrics.py), restated with
+# independent NumPy / SciPy formulations: the checker for metrics.cu.
+# ---------------------------------------------------------------------------
+
+def metrics_pooled(samples):
+    """metrics.py:36-41, 61-68 -- interiors pooled in sample order.
+    samples: list of (scores, mask, image_label, border)."""
+    sc, lb = [], []
+    for s, m, _, b in samples:
+        if b:
+            s, m = s[b:-b, b:-b], m[b:-b, b:-b]
+        sc.append(np.asarray(s).ravel())
+        lb.append(np.asarray(m, bool).ravel())
+    return np.concatenate(sc), np.concatenate(lb)
+
+
+def rank_auroc(scores, labels):
+    """metrics.py:44-58 -- Mann-Whitney U with average ranks (scipy rankdata)."""
+    from scipy.stats import rankdata
+    pos = int(labels.sum())
+    neg = labels.size - pos
+    if pos == 0 or neg == 0:
+        return None
+    r = rankdata(np.asarray(scores, np.float64), method="average")
+    return float((r[labels].sum() - pos * (pos + 1) / 2) / (pos * neg))
+
+
+def f1_optimal(scores, labels):
+    """metrics.py:157-172 -- best 2 tp / (predicted + positives) over the
+    thresholds "score >= t" for every distinct score t."""
+    n_pos = int(labels.sum())
+    if n_pos == 0:
+        return None
+    u, inv = np.unique(scores, return_inverse=True)
+    tot = np.bincount(inv, minlength=u.size)
+    pos = np.bincount(inv, weights=labels.astype(np.float64), minlength=u.size).astype(np.int64)
+    k = np.cumsum(tot[::-1])[::-1]
+    tp = np.cumsum(pos[::-1])[::-1]
+    return float((2.0 * tp / (k + n_pos)).max())
+
+
+def connected_components(mask):
+    """metrics.py:76-80 -- scipy.ndimage.label with the 3x3 structure."""
+    from scipy import ndimage
+    lab, n = ndimage.label(np.asarray(mask, bool), structure=np.ones((3, 3), int))
+    return lab, int(n)
+
+
+def pro_curve(samples, thresholds):
+    """metrics.py:95-122 -- per-threshold mean component overlap and FPR,
+    counting "score >= t" directly for every component."""
+    comps, normal = [], []
+    for s, m, _, b in samples:
+        if b:
+            s, m = s[b:-b, b:-b], m[b:-b, b:-b]
+        m = np.asarray(m, bool)
+        normal.append(s[~m])
+        lab, n = connected_components(m)
+        comps += [s[lab == k] for k in range(1, n + 1)]
+    if not comps:
+        return None
+    normal = np.concatenate(normal)
+    t = np.asarray(thresholds, np.float64)
+    pro = np.zeros(t.size)
+    for c in comps:
+        pro += (c[None, :].astype(np.float64) >= t[:, None]).sum(1) / c.size
+    pro /= len(comps)
+    fpr = (np.zeros(t.size) if normal.size == 0 else
+           (normal[None, :].astype(np.float64) >= t[:, None]).sum(1) / normal.size)
+    return fpr, pro
+
+
+def pro_at_fpr(samples, limit=0.3, thresholds=None):
+    """metrics.py:87-92, 125-154 -- quantile thresholds, trapezoid to the limit."""
+    if thresholds is None:
+        scores, _ = metrics_pooled(samples)
+        thresholds = np.unique(np.quantile(scores, np.linspace(0.0, 1.0, 500)))[::-1]
+    r = pro_curve(samples, thresholds)
+    if r is None:
+        return None
+    f = np.r_[0.0, r[0], 1.0]
+    p = np.r_[0.0, r[1], 1.0]
+    area = 0.0
+    for i in range(1, f.size):
+        if f[i] <= f[i - 1]:
+            continue
+        hi = min(f[i], limit)
+        if hi <= f[i - 1]:
+            break
+        ph = p[i - 1] + (p[i] - p[i - 1]) * (hi - f[i - 1]) / (f[i] - f[i - 1])
+        area += 0.5 * (p[i - 1] + ph) * (hi - f[i - 1])
+        if f[i] >= limit:
+            break
+    return area / limit
+
+
+def auroc_image(samples):
+    """metrics.py:175-179 -- AUROC of per-image interior maxima."""
+    mx, lab = [], []
+    for s, m, l, b in samples:
+        mx.append((s[b:-b, b:-b] if b else s).max())
+        lab.append(bool(l))
+    return rank_auroc(np.array(mx), np.array(lab))

@@ -7,6 +7,17 @@
 #include "common.cuh"
 
 namespace qfca {
+int launch_pool_interior(const void*, int32_t, const uint8_t*, int32_t, int32_t, int32_t, int32_t,
+                         double*, uint8_t*, cudaStream_t);
+int64_t rank_stats_workspace_bytes(int64_t);
+int launch_rank_stats(const double*, const uint8_t*, int64_t, void*, int64_t, double*,
+                      unsigned long long*, cudaStream_t);
+int64_t components_workspace_bytes(int64_t);
+int launch_components(const uint8_t*, int32_t, int32_t, int32_t, void*, int64_t, int32_t*, int32_t*,
+                      int32_t*, cudaStream_t);
+int launch_pro_histograms(const double*, const int32_t*, int64_t, const double*, int32_t, int32_t,
+                          int32_t, int32_t*, unsigned long long*, cudaStream_t);
+int launch_pro_accumulate(int32_t*, int32_t, int32_t, double*, cudaStream_t);
 int launch_minmax(const float*, int64_t, int64_t, float*, float*, int*, cudaStream_t);
 int launch_quantize_fused(const float*, int64_t, int64_t, int, float*, float*, int*, void*, int,
                           cudaStream_t);
@@ -509,6 +520,42 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
         final_map = scores;
     }
     return counted(launch_image_score(final_map, images, h, w, cfg->border, image_scores, st), 1);
+}
+
+int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
+                       int32_t images, int32_t H, int32_t W, int32_t border, double* out,
+                       uint8_t* labels, void* stream) {
+    return counted(launch_pool_interior(scores, scores_bytes, mask, images, H, W, border, out,
+                                        labels, S(stream)), 1);
+}
+
+int64_t qfca_rank_stats_workspace_bytes(int64_t n) { return rank_stats_workspace_bytes(n); }
+
+int qfca_rank_stats(const double* scores, const uint8_t* labels, int64_t n, void* workspace,
+                    int64_t workspace_bytes, double* sorted_out, uint64_t* stats, void* stream) {
+    // radix sort (CUB, ~4 passes) + 3 rank kernels
+    return counted(launch_rank_stats(scores, labels, n, workspace, workspace_bytes, sorted_out,
+                                     (unsigned long long*)stats, S(stream)), 3);
+}
+
+int64_t qfca_components_workspace_bytes(int64_t n) { return components_workspace_bytes(n); }
+
+int qfca_components(const uint8_t* mask, int32_t images, int32_t h, int32_t w, void* workspace,
+                    int64_t workspace_bytes, int32_t* labels, int32_t* comp, int32_t* n_comp,
+                    void* stream) {
+    return counted(launch_components(mask, images, h, w, workspace, workspace_bytes, labels, comp,
+                                     n_comp, S(stream)), 4);
+}
+
+int qfca_pro_histograms(const double* scores, const int32_t* comp, int64_t n,
+                        const double* thr_asc, int32_t m, int32_t comp_lo, int32_t comp_hi,
+                        int32_t* comp_hist, uint64_t* normal_hist, void* stream) {
+    return counted(launch_pro_histograms(scores, comp, n, thr_asc, m, comp_lo, comp_hi, comp_hist,
+                                         (unsigned long long*)normal_hist, S(stream)), 1);
+}
+
+int qfca_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* pro, void* stream) {
+    return counted(launch_pro_accumulate(comp_hist, ncomp, m, pro, S(stream)), ncomp > 0 ? 2 : 0);
 }
 
 }  // extern "C"

@@ -1,0 +1,507 @@
+// metrics.cu -- the evaluation metrics of the reference's metrics.py on the GPU.
+//
+// Rank statistics (metrics.py:44-58 _rank_auroc, 157-172 f1_optimal) run over
+// the pooled scores sorted once (CUB radix sort, stable, fp64 keys with the
+// labels as values).  The average rank of a tie run is (start + end + 1) / 2
+// (0-based start, exclusive end), so twice the positive rank sum is the
+// integer sum over positive elements of (start + last + 2): it is accumulated
+// exactly in 64-bit integers (the reference's fp64 sum of half-integers is
+// exact too, so the AUROC is bit-identical).  Run starts come from a forward
+// max-scan of the start flags and run ends from a backward min-scan, both
+// three-phase over 4096-element tiles (tile aggregates -> one-block scan of
+// the aggregates -> per-tile block scans seeded with the tile prefix).
+// F1 candidates sit at run starts of the ascending order: all elements of
+// score >= s are predicted positive, tp = pos - (positives before the run).
+//
+// Connected components (metrics.py:80-84, scipy.ndimage.label with the 3x3
+// structure): union-find over the interior masks, 8-connectivity, the root of
+// every tree is the smallest raster index of its component (union links the
+// larger root under the smaller with atomicMin), so numbering the roots in
+// index order reproduces ndimage's labels (first-pixel raster order).
+//
+// PRO (metrics.py:95-122): every pixel falls into threshold slot
+// c = #{thresholds <= score}; per-component and normal-pixel histograms over
+// the slots, then per-component suffix sums give "pixels >= threshold", and
+// the per-threshold sum over components runs in component order in fp64 --
+// the same additions in the same order as the reference's loop.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace qfca {
+namespace {
+
+constexpr int MT = 256;
+constexpr int MI = 16;
+constexpr int TILE = MT * MI;
+constexpr long long NO_END = 0x7fffffffffffffffLL;
+
+struct MaxOp {
+    __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; }
+};
+struct MaxD {
+    __device__ double operator()(double a, double b) const { return a > b ? a : b; }
+};
+struct MinOp {
+    __device__ long long operator()(long long a, long long b) const { return a < b ? a : b; }
+};
+
+__device__ __forceinline__ bool run_start(const double* s, long long i) {
+    return i == 0 || s[i] != s[i - 1];
+}
+__device__ __forceinline__ bool run_last(const double* s, long long i, long long n) {
+    return i == n - 1 || s[i] != s[i + 1];
+}
+
+// phase A: per tile positives, last run start, first run end
+__global__ void __launch_bounds__(MT) k_rank_tiles(const double* __restrict__ s,
+                                                   const uint8_t* __restrict__ lab, long long n,
+                                                   long long* tpos, long long* tstart,
+                                                   long long* tend) {
+    using BR = cub::BlockReduce<long long, MT>;
+    __shared__ typename BR::TempStorage tmp;
+    const long long base = (long long)blockIdx.x * TILE;
+    long long pos = 0, st = -1, en = NO_END;
+    for (int k = 0; k < MI; ++k) {
+        const long long i = base + (long long)k * MT + threadIdx.x;
+        if (i < n) {
+            pos += lab[i] != 0;
+            if (run_start(s, i)) st = i > st ? i : st;
+            if (run_last(s, i, n)) en = i < en ? i : en;
+        }
+    }
+    long long a = BR(tmp).Sum(pos);
+    __syncthreads();
+    long long b = BR(tmp).Reduce(st, MaxOp());
+    __syncthreads();
+    long long c = BR(tmp).Reduce(en, MinOp());
+    if (threadIdx.x == 0) {
+        tpos[blockIdx.x] = a;
+        tstart[blockIdx.x] = b;
+        tend[blockIdx.x] = c;
+    }
+}
+
+// phase B: exclusive prefix (sum, max) and exclusive suffix (min) over tiles;
+// stats[0] = total positives
+constexpr int SB = 1024;
+__global__ void __launch_bounds__(SB) k_rank_scan(long long* tpos, long long* tstart,
+                                                  long long* tend, long long ntiles,
+                                                  unsigned long long* stats) {
+    using BS = cub::BlockScan<long long, SB>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ long long carry[3];
+    if (threadIdx.x == 0) { carry[0] = 0; carry[1] = -1; carry[2] = NO_END; }
+    __syncthreads();
+    for (long long c0 = 0; c0 < ntiles; c0 += SB) {
+        const long long t = c0 + threadIdx.x;
+        long long p = t < ntiles ? tpos[t] : 0, st = t < ntiles ? tstart[t] : -1, agg_p, agg_s;
+        BS(tmp).ExclusiveSum(p, p, agg_p);
+        __syncthreads();
+        BS(tmp).ExclusiveScan(st, st, (long long)-1, MaxOp(), agg_s);
+        __syncthreads();
+        if (t < ntiles) {
+            tpos[t] = p + carry[0];
+            tstart[t] = st > carry[1] ? st : carry[1];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry[0] += agg_p;
+            carry[1] = agg_s > carry[1] ? agg_s : carry[1];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) stats[0] = (unsigned long long)carry[0];
+    for (long long c1 = ntiles; c1 > 0; c1 -= SB) {
+        // chunk [c1 - SB, c1) scanned from the right: thread k takes tile c1 - 1 - k
+        const long long t = c1 - 1 - threadIdx.x;
+        long long e = t >= 0 ? tend[t] : NO_END, agg_e;
+        BS(tmp).ExclusiveScan(e, e, NO_END, MinOp(), agg_e);
+        __syncthreads();
+        if (t >= 0) tend[t] = e < carry[2] ? e : carry[2];
+        __syncthreads();
+        if (threadIdx.x == 0) carry[2] = agg_e < carry[2] ? agg_e : carry[2];
+        __syncthreads();
+    }
+}
+
+// phase C: per element run start / run last; accumulate 2 * rank sum of the
+// positives (stats[1]) and the best F1 (stats[2], bits of a non-negative double)
+__global__ void __launch_bounds__(MT) k_rank_emit(const double* __restrict__ s,
+                                                  const uint8_t* __restrict__ lab, long long n,
+                                                  const long long* tpos, const long long* tstart,
+                                                  const long long* tend,
+                                                  unsigned long long* stats) {
+    using BS = cub::BlockScan<long long, MT>;
+    using BRu = cub::BlockReduce<unsigned long long, MT>;
+    using BRd = cub::BlockReduce<double, MT>;
+    __shared__ union {
+        typename BS::TempStorage scan;
+        typename BRu::TempStorage ru;
+        typename BRd::TempStorage rd;
+    } tmp;
+    const long long base = (long long)blockIdx.x * TILE + (long long)threadIdx.x * MI;
+    uint8_t l[MI];
+    bool fs[MI], fl[MI];
+    long long p_loc = 0, st_loc = -1, en_loc = NO_END;
+#pragma unroll
+    for (int k = 0; k < MI; ++k) {
+        const long long i = base + k;
+        if (i < n) {
+            l[k] = lab[i];
+            fs[k] = run_start(s, i);
+            fl[k] = run_last(s, i, n);
+            p_loc += l[k] != 0;
+            if (fs[k]) st_loc = i;
+            if (fl[k] && en_loc == NO_END) en_loc = i;
+        } else {
+            l[k] = 0;
+            fs[k] = fl[k] = false;
+        }
+    }
+    // forward: exclusive positives and last run start before this thread
+    long long p_ex, st_ex;
+    BS(tmp.scan).ExclusiveSum(p_loc, p_ex);
+    __syncthreads();
+    BS(tmp.scan).ExclusiveScan(st_loc, st_ex, (long long)-1, MaxOp());
+    __syncthreads();
+    // backward: first run end after this thread (threads reversed through shared memory)
+    __shared__ long long rev[MT];
+    rev[MT - 1 - threadIdx.x] = en_loc;
+    __syncthreads();
+    long long en_rev = rev[threadIdx.x], en_ex_rev;
+    __syncthreads();
+    BS(tmp.scan).ExclusiveScan(en_rev, en_ex_rev, NO_END, MinOp());
+    __syncthreads();
+    rev[MT - 1 - threadIdx.x] = en_ex_rev;
+    __syncthreads();
+    long long en_ex = rev[threadIdx.x];
+    const long long tp0 = tpos[blockIdx.x], ts0 = tstart[blockIdx.x], te0 = tend[blockIdx.x];
+    long long pcount = p_ex + tp0;
+    long long start = st_ex > ts0 ? st_ex : ts0;
+    long long nxt_end = en_ex < te0 ? en_ex : te0;
+    const long long total_pos = (long long)stats[0];
+    // run last index for each item: scan the thread's items from the right
+    long long last[MI];
+    {
+        long long e = nxt_end;
+#pragma unroll
+        for (int k = MI - 1; k >= 0; --k) {
+            if (fl[k]) e = base + k;
+            last[k] = e;
+        }
+    }
+    unsigned long long r2 = 0;
+    double f1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < MI; ++k) {
+        const long long i = base + k;
+        if (i >= n) break;
+        if (fs[k]) {
+            start = i;
+            // metrics.py:166-171 -- threshold at this run: k = n - i predicted, tp positives
+            const long long tp = total_pos - pcount;
+            const double f = 2.0 * (double)tp / (double)((n - i) + total_pos);
+            f1 = f > f1 ? f : f1;
+        }
+        if (l[k]) r2 += (unsigned long long)(start + last[k] + 2);
+        pcount += l[k] != 0;
+    }
+    unsigned long long r2b = BRu(tmp.ru).Sum(r2);
+    __syncthreads();
+    double f1b = BRd(tmp.rd).Reduce(f1, MaxD());
+    if (threadIdx.x == 0) {
+        atomicAdd(&stats[1], r2b);
+        atomicMax(&stats[2], (unsigned long long)__double_as_longlong(f1b));
+    }
+}
+
+// ---- connected components (8-connectivity union-find) ----
+__device__ __forceinline__ int cc_find(const int* L, int x) {
+    int p = L[x];
+    while (p != x) {
+        x = p;
+        p = L[x];
+    }
+    return x;
+}
+
+__device__ __forceinline__ void cc_union(int* L, int a, int b) {
+    bool done = false;
+    while (!done) {
+        a = cc_find(L, a);
+        b = cc_find(L, b);
+        if (a < b) {
+            int old = atomicMin(&L[b], a);
+            done = (old == b);
+            b = old;
+        } else if (b < a) {
+            int old = atomicMin(&L[a], b);
+            done = (old == a);
+            a = old;
+        } else {
+            done = true;
+        }
+    }
+}
+
+__global__ void k_cc_init(const uint8_t* __restrict__ mask, long long n, int* L) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        L[i] = mask[i] ? (int)i : -1;
+}
+
+__global__ void k_cc_merge(const uint8_t* __restrict__ mask, int images, int h, int w, int* L) {
+    const long long n = (long long)images * h * w;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (!mask[i]) continue;
+        const int x = (int)(i % w), y = (int)((i / w) % h);
+        // the four neighbours already passed in raster order: W, NW, N, NE
+        if (x > 0 && mask[i - 1]) cc_union(L, (int)i, (int)(i - 1));
+        if (y > 0) {
+            const long long up = i - w;
+            if (x > 0 && mask[up - 1]) cc_union(L, (int)i, (int)(up - 1));
+            if (mask[up]) cc_union(L, (int)i, (int)up);
+            if (x + 1 < w && mask[up + 1]) cc_union(L, (int)i, (int)(up + 1));
+        }
+    }
+}
+
+__global__ void k_cc_flatten(long long n, int* L, int* root_flag) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int l = L[i];
+        if (l >= 0) {
+            const int r = cc_find(L, (int)i);
+            L[i] = r;
+            root_flag[i] = (r == (int)i);
+        } else {
+            root_flag[i] = 0;
+        }
+    }
+}
+
+__global__ void k_cc_ids(long long n, const int* __restrict__ L, const int* __restrict__ root_flag,
+                         const int* __restrict__ rank, int* comp, int* n_comp) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int l = L[i];
+        comp[i] = l >= 0 ? rank[l] : -1;
+        if (i == n - 1) *n_comp = rank[i] + root_flag[i];
+    }
+}
+
+// ---- PRO histograms ----
+constexpr int MAX_THR = 2048;
+
+__global__ void __launch_bounds__(256) k_pro_hist(const double* __restrict__ s,
+                                                  const int* __restrict__ comp, long long n,
+                                                  const double* __restrict__ thr_asc, int m,
+                                                  int comp_lo, int comp_hi, int* comp_hist,
+                                                  unsigned long long* normal_hist) {
+    __shared__ double t[MAX_THR];
+    __shared__ unsigned int nh[MAX_THR + 1];
+    for (int j = threadIdx.x; j < m; j += blockDim.x) t[j] = thr_asc[j];
+    for (int j = threadIdx.x; j <= m; j += blockDim.x) nh[j] = 0;
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = comp[i];
+        const bool normal = c < 0;
+        if (!normal && (c < comp_lo || c >= comp_hi)) continue;
+        if (normal && normal_hist == nullptr) continue;
+        const double v = s[i];
+        // slot = #{thresholds <= v} (upper bound over the ascending thresholds)
+        int lo = 0, hi = m;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (t[mid] <= v) lo = mid + 1; else hi = mid;
+        }
+        if (normal) atomicAdd(&nh[lo], 1u);
+        else atomicAdd(&comp_hist[(long long)(c - comp_lo) * (m + 1) + lo], 1);
+    }
+    if (normal_hist == nullptr) return;
+    __syncthreads();
+    for (int j = threadIdx.x; j <= m; j += blockDim.x)
+        if (nh[j]) atomicAdd(&normal_hist[j], (unsigned long long)nh[j]);
+}
+
+// per component: suffix sums in place, S[c] = pixels in slots >= c (S[0] = size)
+__global__ void k_pro_suffix(int* comp_hist, int ncomp, int m) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= ncomp) return;
+    int* h = comp_hist + (long long)q * (m + 1);
+    int acc = 0;
+    for (int c = m; c >= 0; --c) {
+        acc += h[c];
+        h[c] = acc;
+    }
+}
+
+// pro[j] += S_q[j + 1] / S_q[0] over components q in order (metrics.py:116-118)
+__global__ void k_pro_accumulate(const int* __restrict__ comp_hist, int ncomp, int m, double* pro) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double acc = pro[j];
+    for (int q = 0; q < ncomp; ++q) {
+        const int* h = comp_hist + (long long)q * (m + 1);
+        acc += (double)h[j + 1] / (double)h[0];
+    }
+    pro[j] = acc;
+}
+
+// pooled fp64 copy of the interiors: out[b][y][x] = scores[b][y + bd][x + bd]
+template <typename T>
+__global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restrict__ mk,
+                                int images, int H, int W, int bd, double* out, uint8_t* lab) {
+    const int h = H - 2 * bd, w = W - 2 * bd;
+    const long long n = (long long)images * h * w;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % w);
+        const long long r = i / w;
+        const int y = (int)(r % h);
+        const long long b = r / h;
+        const long long src = (b * H + y + bd) * W + x + bd;
+        out[i] = (double)sc[src];
+        if (lab) lab[i] = mk[src] != 0;
+    }
+}
+
+inline int grid_for(long long n, int threads) {
+    long long g = (n + threads - 1) / threads;
+    const long long cap = 148LL * 16;
+    if (g > cap) g = cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t sort_temp_bytes(long long n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const double*)nullptr, (double*)nullptr,
+                                    (const uint8_t*)nullptr, (uint8_t*)nullptr, (int)n);
+    return bytes;
+}
+
+size_t scan_temp_bytes(long long n) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int*)nullptr, (int*)nullptr, (int)n);
+    return bytes;
+}
+
+}  // namespace
+
+// ---- host launchers (C-ABI wrappers in capi.cu) ----
+
+int64_t rank_stats_workspace_bytes(int64_t n) {
+    if (n < 1 || n >= (1LL << 31)) return -1;
+    const long long ntiles = (n + TILE - 1) / TILE;
+    return (int64_t)(align256(n * sizeof(double)) + align256(n) + 3 * align256(ntiles * 8) +
+                     align256(sort_temp_bytes(n)));
+}
+
+int launch_rank_stats(const double* scores, const uint8_t* labels, int64_t n, void* ws,
+                      int64_t ws_bytes, double* sorted_out, unsigned long long* stats,
+                      cudaStream_t st) {
+    const int64_t need = rank_stats_workspace_bytes(n);
+    if (need < 0 || !scores || !labels || !stats || !ws || ws_bytes < need) return QFCA_ERR_ARG;
+    const long long ntiles = (n + TILE - 1) / TILE;
+    char* p = (char*)ws;
+    double* keys = (double*)p;
+    p += align256(n * sizeof(double));
+    uint8_t* lab = (uint8_t*)p;
+    p += align256(n);
+    long long* tpos = (long long*)p;
+    p += align256(ntiles * 8);
+    long long* tstart = (long long*)p;
+    p += align256(ntiles * 8);
+    long long* tend = (long long*)p;
+    p += align256(ntiles * 8);
+    size_t tb = sort_temp_bytes(n);
+    if (cub::DeviceRadixSort::SortPairs(p, tb, scores, keys, labels, lab, (int)n, 0, 64, st) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess)
+        return QFCA_ERR_CUDA;
+    k_rank_tiles<<<(unsigned)ntiles, MT, 0, st>>>(keys, lab, n, tpos, tstart, tend);
+    k_rank_scan<<<1, SB, 0, st>>>(tpos, tstart, tend, ntiles, stats);
+    k_rank_emit<<<(unsigned)ntiles, MT, 0, st>>>(keys, lab, n, tpos, tstart, tend, stats);
+    if (sorted_out && cudaMemcpyAsync(sorted_out, keys, n * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return QFCA_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int64_t components_workspace_bytes(int64_t n) {
+    if (n < 1 || n >= (1LL << 31)) return -1;
+    return (int64_t)(3 * align256(n * sizeof(int)) + align256(scan_temp_bytes(n)));
+}
+
+int launch_components(const uint8_t* mask, int32_t images, int32_t h, int32_t w, void* ws,
+                      int64_t ws_bytes, int32_t* labels, int32_t* comp, int32_t* n_comp,
+                      cudaStream_t st) {
+    const long long n = (long long)images * h * w;
+    const int64_t need = components_workspace_bytes(n);
+    if (images < 1 || h < 1 || w < 1 || need < 0 || !mask || !comp || !n_comp || !ws ||
+        ws_bytes < need)
+        return QFCA_ERR_ARG;
+    char* p = (char*)ws;
+    int* L = labels ? labels : (int*)p;
+    p += align256(n * sizeof(int));
+    int* flag = (int*)p;
+    p += align256(n * sizeof(int));
+    int* rank = (int*)p;
+    p += align256(n * sizeof(int));
+    size_t tb = scan_temp_bytes(n);
+    const int g = grid_for(n, 256);
+    k_cc_init<<<g, 256, 0, st>>>(mask, n, L);
+    k_cc_merge<<<g, 256, 0, st>>>(mask, images, h, w, L);
+    k_cc_flatten<<<g, 256, 0, st>>>(n, L, flag);
+    if (cub::DeviceScan::ExclusiveSum(p, tb, flag, rank, (int)n, st) != cudaSuccess)
+        return QFCA_ERR_CUDA;
+    k_cc_ids<<<g, 256, 0, st>>>(n, L, flag, rank, comp, n_comp);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int launch_pro_histograms(const double* scores, const int32_t* comp, int64_t n,
+                          const double* thr_asc, int32_t m, int32_t comp_lo, int32_t comp_hi,
+                          int32_t* comp_hist, unsigned long long* normal_hist, cudaStream_t st) {
+    if (n < 1 || m < 1 || m > MAX_THR || comp_lo < 0 || comp_hi < comp_lo || !scores || !comp ||
+        !thr_asc || (comp_hi > comp_lo && !comp_hist))
+        return QFCA_ERR_ARG;
+    k_pro_hist<<<grid_for(n, 256), 256, 0, st>>>(scores, comp, n, thr_asc, m, comp_lo, comp_hi,
+                                                 comp_hist, normal_hist);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int launch_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* pro,
+                          cudaStream_t st) {
+    if (ncomp < 0 || m < 1 || m > MAX_THR || !pro || (ncomp > 0 && !comp_hist)) return QFCA_ERR_ARG;
+    if (ncomp == 0) return QFCA_OK;
+    k_pro_suffix<<<(ncomp + 255) / 256, 256, 0, st>>>(comp_hist, ncomp, m);
+    k_pro_accumulate<<<(m + 127) / 128, 128, 0, st>>>(comp_hist, ncomp, m, pro);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int launch_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
+                         int32_t images, int32_t H, int32_t W, int32_t border, double* out,
+                         uint8_t* labels, cudaStream_t st) {
+    if (images < 1 || border < 0 || 2 * border >= H || 2 * border >= W || !scores || !out ||
+        (labels && !mask))
+        return QFCA_ERR_ARG;
+    const long long n = (long long)images * (H - 2 * border) * (W - 2 * border);
+    const int g = grid_for(n, 256);
+    if (scores_bytes == 8)
+        k_pool_interior<double><<<g, 256, 0, st>>>((const double*)scores, mask, images, H, W,
+                                                   border, out, labels);
+    else if (scores_bytes == 4)
+        k_pool_interior<float><<<g, 256, 0, st>>>((const float*)scores, mask, images, H, W,
+                                                  border, out, labels);
+    else
+        return QFCA_ERR_ARG;
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+}  // namespace qfca

@@ -31,8 +31,10 @@ def load_golden(name):
 
 
 def golden_names(prefix=""):
+    # metrics_*.npz belong to tests/test_metrics.py (different layout)
     return sorted(f[:-4] for f in os.listdir(GOLDEN)
-                  if f.endswith(".npz") and f.startswith(prefix))
+                  if f.endswith(".npz") and f.startswith(prefix)
+                  and not f.startswith("metrics_"))
 
 
 def cfg_of(d):
