@@ -26,6 +26,8 @@ from .transport import (IllConditionedError, MassError, mismatch_batch,
                         quantized_mismatch)
 from .pipeline import DetectPipeline, HostResult
 from . import exporter, tensor_io  # feature backbone on the GPU, QTF1 feature files
+from . import metrics  # PRO / AUROC / F1 / components on the GPU (metrics.py)
+from .metrics import EvalSample, MetricReport
 
 __all__ = [
     "FeatureMap", "FormatError", "PcaModel", "gaussian_blur", "pca_fit", "pca_residual",
@@ -36,4 +38,5 @@ __all__ = [
     "fused_supported", "image_score_of", "smooth_scores", "upsample_batch",
     "upsample_scores", "IllConditionedError", "MassError", "mismatch_batch",
     "quantized_mismatch", "DetectPipeline", "HostResult", "exporter", "tensor_io",
+    "metrics", "EvalSample", "MetricReport",
 ]

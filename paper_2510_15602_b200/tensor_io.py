@@ -25,7 +25,9 @@ _DTYPE_CODES = {np.dtype(np.float32): 1, np.dtype(np.uint8): 2}
 _CODE_DTYPES = {1: np.dtype(np.float32), 2: np.dtype(np.uint8)}
 
 __all__ = ["MAGIC", "TensorFormatError", "BadMagicError", "TruncatedError",
-           "UnsupportedDtypeError", "write_tensor", "read_tensor", "read_features"]
+           "UnsupportedDtypeError", "write_tensor", "read_tensor", "read_features",
+           "DecodeError", "DatasetIndexError", "DatasetSample", "load_dataset", "load_mask",
+           "feature_scale"]
 
 
 class TensorFormatError(Exception):
@@ -118,3 +120,91 @@ def read_features(paths, device=None) -> torch.Tensor:
                                                        count=int(np.prod(shape)))
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     return host.to(dev, non_blocking=True)
+
+
+# ---- dataset tree, masks and external feature files (the CLI's inputs) ----
+
+class DecodeError(Exception):
+    """tensor_io.py:43-44 -- an image file could not be decoded."""
+
+
+class DatasetIndexError(Exception):
+    """tensor_io.py:47-48 -- the dataset tree is malformed."""
+
+
+def _nearest_index(n_in: int, n_out: int) -> np.ndarray:
+    """tensor_io.py:133-138 -- half-pixel centres, rounded, clamped."""
+    c = (np.arange(n_out) + 0.5) * n_in / n_out - 0.5
+    return np.clip(np.round(c), 0, n_in - 1).astype(int)
+
+
+def load_mask(path, size=None) -> np.ndarray:
+    """tensor_io.py:186-191 -- binary H x W mask (any value > 0), optionally
+    resized with nearest sampling.  Pixel decode through Pillow like the
+    reference's load_image (tensor_io.py:161-183)."""
+    from PIL import Image
+    try:
+        with Image.open(path) as im:
+            im = im.convert("RGB") if im.mode not in ("L", "RGB") else im
+            arr = np.asarray(im)
+    except Exception as e:  # noqa: BLE001 -- the reference wraps every decoder error
+        raise DecodeError(f"cannot decode {path}: {e}") from e
+    plane = arr if arr.ndim == 2 else arr[..., 0]
+    m = plane > 0
+    if size is not None:
+        if isinstance(size, int):
+            size = (size, size)
+        if tuple(size) != m.shape:
+            m = m[np.ix_(_nearest_index(m.shape[0], size[0]),
+                         _nearest_index(m.shape[1], size[1]))]
+    return m
+
+
+class DatasetSample:
+    """tensor_io.py:194-199."""
+
+    __slots__ = ("image_path", "mask_path", "is_anomalous", "defect_type")
+
+    def __init__(self, image_path, mask_path, is_anomalous, defect_type):
+        self.image_path, self.mask_path = image_path, mask_path
+        self.is_anomalous, self.defect_type = is_anomalous, defect_type
+
+
+def load_dataset(root, class_name: str, layout: str = "mvtec") -> list:
+    """tensor_io.py:207-240 -- index root/class/test/<defect>/*.png|ppm with
+    masks at root/class/ground_truth/<defect>/<stem>_mask.png ("good" has
+    none), lexicographic by defect then file name."""
+    if layout != "mvtec":
+        raise ValueError(f"unknown layout {layout!r}")
+    test_dir = os.path.join(root, class_name, "test")
+    gt_dir = os.path.join(root, class_name, "ground_truth")
+    if not os.path.isdir(test_dir):
+        raise DatasetIndexError(f"missing test directory {test_dir}")
+    out = []
+    for defect in sorted(os.listdir(test_dir)):
+        ddir = os.path.join(test_dir, defect)
+        if not os.path.isdir(ddir):
+            continue
+        bad = defect != "good"
+        for fname in sorted(os.listdir(ddir)):
+            if not fname.lower().endswith((".png", ".ppm")):
+                continue
+            mask = None
+            if bad:
+                mask = os.path.join(gt_dir, defect, os.path.splitext(fname)[0] + "_mask.png")
+                if not os.path.isfile(mask):
+                    raise DatasetIndexError(f"anomalous sample {os.path.join(ddir, fname)} "
+                                            f"has no mask at {mask}")
+            out.append(DatasetSample(os.path.join(ddir, fname), mask, bad, defect))
+    return out
+
+
+def feature_scale(path) -> int:
+    """features.py:135-146 -- downsampling factor from the <path>.json sidecar
+    ({"scale": s}), 8 when absent."""
+    import json
+    side = str(path) + ".json"
+    if os.path.isfile(side):
+        with open(side) as f:
+            return int(json.load(f)["scale"])
+    return 8
