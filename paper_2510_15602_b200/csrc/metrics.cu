@@ -140,17 +140,42 @@ __global__ void __launch_bounds__(MT) k_rank_emit(const double* __restrict__ s,
         typename BRu::TempStorage ru;
         typename BRd::TempStorage rd;
     } tmp;
-    const long long base = (long long)blockIdx.x * TILE + (long long)threadIdx.x * MI;
+    // stage the tile: coalesced global loads into shared memory (one padding
+    // double per 16 so each thread's 16 consecutive items hit distinct banks)
+    __shared__ double sv[TILE + TILE / MI];
+    __shared__ __align__(16) uint8_t sl[TILE];
+    __shared__ double halo[2];
+    const long long t0 = (long long)blockIdx.x * TILE;
+    for (int j = threadIdx.x; j < TILE; j += MT) {
+        const long long i = t0 + j;
+        sv[j + j / MI] = i < n ? s[i] : 0.0;
+        sl[j] = i < n ? lab[i] : 0;
+    }
+    if (threadIdx.x == 0) halo[0] = t0 > 0 ? s[t0 - 1] : 0.0;
+    if (threadIdx.x == 1) halo[1] = t0 + TILE < n ? s[t0 + TILE] : 0.0;
+    __syncthreads();
+    const int j0 = threadIdx.x * MI;
+    const long long base = t0 + j0;
     uint8_t l[MI];
     bool fs[MI], fl[MI];
+    {
+        const uint4 lv = *reinterpret_cast<const uint4*>(&sl[j0]);
+        const uint8_t* lb = reinterpret_cast<const uint8_t*>(&lv);
+#pragma unroll
+        for (int k = 0; k < MI; ++k) l[k] = lb[k];
+    }
+    double v[MI + 2];
+    v[0] = j0 > 0 ? sv[(j0 - 1) + (j0 - 1) / MI] : halo[0];
+#pragma unroll
+    for (int k = 0; k < MI; ++k) v[k + 1] = sv[j0 + k + threadIdx.x];  // (j0 + k) / MI == threadIdx.x
+    v[MI + 1] = j0 + MI < TILE ? sv[(j0 + MI) + (j0 + MI) / MI] : halo[1];
     long long p_loc = 0, st_loc = -1, en_loc = NO_END;
 #pragma unroll
     for (int k = 0; k < MI; ++k) {
         const long long i = base + k;
         if (i < n) {
-            l[k] = lab[i];
-            fs[k] = run_start(s, i);
-            fl[k] = run_last(s, i, n);
+            fs[k] = i == 0 || v[k + 1] != v[k];
+            fl[k] = i == n - 1 || v[k + 1] != v[k + 2];
             p_loc += l[k] != 0;
             if (fs[k]) st_loc = i;
             if (fl[k] && en_loc == NO_END) en_loc = i;
@@ -257,13 +282,17 @@ __global__ void k_cc_merge(const uint8_t* __restrict__ mask, int images, int h, 
          i += (long long)gridDim.x * blockDim.x) {
         if (!mask[i]) continue;
         const int x = (int)(i % w), y = (int)((i / w) % h);
-        // the four neighbours already passed in raster order: W, NW, N, NE
-        if (x > 0 && mask[i - 1]) cc_union(L, (int)i, (int)(i - 1));
-        if (y > 0) {
-            const long long up = i - w;
-            if (x > 0 && mask[up - 1]) cc_union(L, (int)i, (int)(up - 1));
-            if (mask[up]) cc_union(L, (int)i, (int)up);
-            if (x + 1 < w && mask[up + 1]) cc_union(L, (int)i, (int)(up + 1));
+        // neighbours already passed in raster order: W, NW, N, NE.  N alone
+        // suffices when set (NW and NE are N's row neighbours, W is N's
+        // diagonal neighbour: those edges are unioned from the other side);
+        // otherwise W covers NW (W's own N), and NE needs its own union.
+        const bool n_ = y > 0 && mask[i - w];
+        if (n_) {
+            cc_union(L, (int)i, (int)(i - w));
+        } else {
+            if (x > 0 && mask[i - 1]) cc_union(L, (int)i, (int)(i - 1));
+            else if (y > 0 && x > 0 && mask[i - w - 1]) cc_union(L, (int)i, (int)(i - w - 1));
+            if (y > 0 && x + 1 < w && mask[i - w + 1]) cc_union(L, (int)i, (int)(i - w + 1));
         }
     }
 }
