@@ -31,7 +31,7 @@ from .features import _gauss_kernel, sep_convolve_dev
 from .quantize import bins_dev, minmax_dev
 
 __all__ = ["shard_range", "shard_batch", "combine_partials", "channel_partial",
-           "detect_channel_sharded", "strips"]
+           "detect_channel_sharded", "strips", "pca_fit_sharded", "detect_pca_sharded"]
 
 STRIP_W = 128  # widest plane of the fused kernels
 STRIP_H = 256  # tile height: the whole-tile bins + row tables stay in shared memory
@@ -238,3 +238,109 @@ def detect_channel_sharded(values_local: torch.Tensor, cfg=None, group=None):
     N.call("qfca_image_score", final.contiguous().data_ptr(), 1, h, w, cfg.border,
            img.data_ptr(), N.stream())
     return final, img[0], used_all == 0
+
+
+# ---- QFCA+ on one huge image (option (a)) ----
+#
+# The covariance needs every channel of a pixel, so channel sharding alone
+# cannot form it.  Features are replicated on every rank; the pixels are
+# sharded for the two reductions of pca_fit (features.py:167-172): the channel
+# sums (-> mean) and the centred Gram matrix, each combined with one
+# all-reduce (C and C x C fp64).  The top-k eigenpairs are then formed
+# identically on every rank, each rank takes the residual of its channel
+# slice, and scoring continues as detect_channel_sharded (one more
+# all-reduce of the channel-sum map).
+
+COV_CHUNK = 16384  # pixels per exact int8-digit covariance block (cov_i8.cu bound)
+
+
+def _world(group=None) -> tuple[int, int]:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def _all_reduce(t: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def local_pixels(values: torch.Tensor, world: int, rank: int) -> torch.Tensor:
+    """This rank's contiguous pixel range of a (C, h, w) plane stack -> (C, n)."""
+    c = values.shape[0]
+    x = values.reshape(c, -1)
+    p0, p1 = shard_range(x.shape[1], world, rank)
+    return x[:, p0:p1].contiguous()
+
+
+def channel_sums(xs: torch.Tensor) -> torch.Tensor:
+    """(C, n) fp32 -> (C,) fp64 channel sums over the local pixels."""
+    c, n = xs.shape
+    m = empty((c,), torch.float64)
+    N.call("qfca_plane_mean", xs.data_ptr(), c, n, m.data_ptr(), N.stream())
+    return m * float(n)
+
+
+def centred_gram(xs: torch.Tensor, mean: torch.Tensor) -> torch.Tensor:
+    """sum over the local pixels of (x - mean)(x - mean)^T, (C, C) fp64.
+
+    Blocks of COV_CHUNK pixels go through the exact int8-digit covariance
+    (covariance_exact, batched over blocks, the global mean for every block);
+    a ragged tail takes the same call on its own size."""
+    from .features import covariance_exact
+    c, n = xs.shape
+    g = zeros((c, c), torch.float64)
+    nf = n // COV_CHUNK
+    if nf:
+        blk = xs[:, :nf * COV_CHUNK].reshape(c, nf, COV_CHUNK).permute(1, 0, 2).contiguous()
+        cov = covariance_exact(blk.view(nf, c, COV_CHUNK, 1),
+                               mean.reshape(1, c).expand(nf, c).contiguous())
+        g += cov.sum(0) * float(COV_CHUNK)
+    r = n - nf * COV_CHUNK
+    if r:
+        tail = xs[:, nf * COV_CHUNK:].contiguous()
+        g += covariance_exact(tail.view(1, c, r, 1), mean.reshape(1, c).contiguous())[0] * float(r)
+    return g
+
+
+def pca_fit_sharded(values: torch.Tensor, k: int, group=None):
+    """pca_fit (features.py:157-180) of one (C, h, w) image replicated on every
+    rank, pixel-sharded: -> (mean (C,), components (k, C), eigenvalues (k,))."""
+    from .features import topk_eigh
+    world, rank = _world(group)
+    c = values.shape[0]
+    hw = values[0].numel()
+    if not 1 <= k <= c:
+        raise ValueError(f"k must be in [1, {c}], got {k}")
+    xs = local_pixels(values, world, rank)
+    mean = _all_reduce(channel_sums(xs), group) / float(hw)
+    cov = _all_reduce(centred_gram(xs, mean), group) / float(hw)
+    evals, vecs = topk_eigh(cov[None], k)
+    comps = vecs[0].transpose(0, 1).contiguous()  # (k, C)
+    arg = comps.abs().argmax(dim=1, keepdim=True)
+    sign = torch.where(torch.gather(comps, 1, arg) < 0, -1.0, 1.0).to(comps.dtype)
+    return mean, comps * sign, evals[0].clamp(min=0.0)
+
+
+def detect_pca_sharded(values: torch.Tensor, cfg=None, group=None):
+    """QFCA+ (cfg.pca_components > 0) on one huge image: ``values`` is the full
+    (C, h, w) stack on every rank.  Returns what detect_channel_sharded does."""
+    import dataclasses
+
+    from .features import pca_residual_batch
+    from .scoring import PipelineConfig
+    cfg = cfg or PipelineConfig()
+    world, rank = _world(group)
+    c = values.shape[0]
+    if cfg.pca_components > 0:
+        mean, comps, _ = pca_fit_sharded(values, min(cfg.pca_components, c), group)
+        c0, c1 = shard_range(c, world, rank)
+        resid = pca_residual_batch(values[None].contiguous(), mean[None], comps[None])[0]
+        local = resid[c0:c1].contiguous()
+    else:
+        c0, c1 = shard_range(c, world, rank)
+        local = values[c0:c1].contiguous()
+    return detect_channel_sharded(local, dataclasses.replace(cfg, pca_components=0), group)

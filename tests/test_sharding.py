@@ -121,3 +121,83 @@ def test_strip_geometry():
                         assert x - a >= halo              # far from the left inner edge
                     if own[x] < len(st) - 1:
                         assert a + sw - 1 - x >= halo     # far from the right inner edge
+
+
+def _pca_worker(rank, world, port, x, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2510_15602_b200.sharding import _all_reduce, _world, local_pixels
+    w, r = _world()
+    xs = local_pixels(torch.from_numpy(x), w, r).double()  # (C, n_local)
+    s = _all_reduce(xs.sum(1))
+    mean = s / float(x[0].size)
+    xc = xs - mean[:, None]
+    g = _all_reduce(xc @ xc.T)
+    if rank == 0:
+        out.put((mean.numpy(), (g / float(x[0].size)).numpy()))
+    dist.destroy_process_group()
+
+
+def test_pixel_sharded_pca_reductions_gloo():
+    """QFCA+ on one huge image: the pixel partition and the two all-reduces
+    (channel sums, centred Gram) reproduce pca_fit's mean and covariance
+    (features.py:169-172).  The per-rank partial is plain torch fp64 here."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((6, 13, 11)).astype(np.float32)  # 143 pixels: ragged split
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pca_worker, args=(r, 2, port, x, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    mean, cov = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    v = x.reshape(6, -1).T.astype(np.float64)
+    np.testing.assert_allclose(mean, v.mean(0), rtol=1e-13, atol=1e-15)
+    xc = v - v.mean(0)
+    np.testing.assert_allclose(cov, xc.T @ xc / v.shape[0], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_pca_sharded_gpu():
+    """Pixel-sharded pca_fit partials (two simulated ranks summed) equal the
+    whole-plane ones; detect_pca_sharded (world size 1) matches the oracle's
+    QFCA+ detect.  150 x 140 = 21000 pixels: one exact 16384-pixel block plus
+    a ragged tail per covariance."""
+    import paper_2510_15602_b200 as Q
+    from paper_2510_15602_b200.sharding import (centred_gram, channel_sums, detect_pca_sharded,
+                                                local_pixels, pca_fit_sharded)
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(6)
+    x = np.maximum(rng.standard_normal((48, 150, 140)) + 0.2, 0).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    hw = 150 * 140
+    full = local_pixels(xt, 1, 0)
+    mean = channel_sums(full) / hw
+    halves = [local_pixels(xt, 2, r) for r in range(2)]
+    mean2 = (channel_sums(halves[0]) + channel_sums(halves[1])) / hw
+    torch.testing.assert_close(mean2, mean, rtol=1e-12, atol=1e-14)
+    g = centred_gram(full, mean)
+    g2 = centred_gram(halves[0], mean) + centred_gram(halves[1], mean)
+    v = x.reshape(48, -1).astype(np.float64)
+    vc = v - v.mean(1, keepdims=True)
+    ref_cov = vc @ vc.T / hw
+    scale = np.abs(ref_cov).max()
+    assert np.abs(g.cpu().numpy() / hw - ref_cov).max() <= 1e-9 * scale
+    assert np.abs(g2.cpu().numpy() / hw - ref_cov).max() <= 1e-9 * scale
+    m, comps, ev = pca_fit_sharded(xt, 5)
+    om, oc, oev = O.pca_fit(x, 5)
+    np.testing.assert_allclose(ev.cpu().numpy(), oev, rtol=1e-8)
+    proj = comps.T.cpu().numpy() @ comps.cpu().numpy()
+    assert np.abs(proj - oc.T @ oc).max() <= 1e-7
+    cfg = Q.PipelineConfig(pca_components=5)
+    final, img, degen = detect_pca_sharded(xt, cfg)
+    ref, img_ref, _ = O.detect(x, pca_components=5)
+    assert np.abs(final.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
+    assert abs(float(img) - img_ref) <= 1e-4 * np.abs(ref).max()
+    assert not bool(degen)
