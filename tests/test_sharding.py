@@ -174,7 +174,11 @@ def test_pca_sharded_gpu():
                                                 local_pixels, pca_fit_sharded)
     from oracle import qfca_oracle as O
     rng = np.random.default_rng(6)
-    x = np.maximum(rng.standard_normal((48, 150, 140)) + 0.2, 0).astype(np.float32)
+    c = 256  # the block-Lanczos eigensolver's range; a decaying spectrum (5 strong directions)
+    u = np.linalg.qr(rng.standard_normal((c, 5)))[0]
+    z = rng.standard_normal((5, 150 * 140)) * np.array([6.0, 5.0, 4.0, 3.0, 2.5])[:, None]
+    x = (u @ z + 0.5 * rng.standard_normal((c, 150 * 140))).reshape(c, 150, 140)
+    x = np.maximum(x + 0.5, 0).astype(np.float32)
     xt = torch.from_numpy(x).cuda()
     hw = 150 * 140
     full = local_pixels(xt, 1, 0)
@@ -184,7 +188,7 @@ def test_pca_sharded_gpu():
     torch.testing.assert_close(mean2, mean, rtol=1e-12, atol=1e-14)
     g = centred_gram(full, mean)
     g2 = centred_gram(halves[0], mean) + centred_gram(halves[1], mean)
-    v = x.reshape(48, -1).astype(np.float64)
+    v = x.reshape(c, -1).astype(np.float64)
     vc = v - v.mean(1, keepdims=True)
     ref_cov = vc @ vc.T / hw
     scale = np.abs(ref_cov).max()
