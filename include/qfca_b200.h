@@ -242,20 +242,25 @@ int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, 
 /* Pooled interiors of a batch of maps (metrics.py:36-41 EvalSample.interior,
  * 61-68 _pooled): scores (images, H, W) fp64 (scores_bytes 8) or fp32 (4),
  * mask (images, H, W) uint8 -> out (images, H-2b, W-2b) fp64 and, if labels is
- * not NULL, labels (same shape) uint8 0/1. */
+ * not NULL, labels (same shape) uint8 0/1.  If out32 is not NULL it also gets
+ * the values as float32, and *inexact (device int32, zeroed by the caller) is
+ * set when some value is not a float32 value (then out32 must not be ranked). */
 int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
                        int32_t images, int32_t H, int32_t W, int32_t border, double* out,
-                       uint8_t* labels, void* stream);
+                       uint8_t* labels, float* out32, int32_t* inexact, void* stream);
 
 /* Rank statistics of pooled scores (metrics.py:44-58 _rank_auroc,
  * 157-172 f1_optimal): one stable sort, then stats[0] = positives,
  * stats[1] = 2 x the rank sum of the positives (average ranks for ties; exact),
- * stats[2] = the bits of the best F1 over all thresholds (fp64).  sorted_out
- * (n fp64, may be NULL) receives the ascending scores (for the PRO quantiles,
- * metrics.py:87-92).  n < 2^31; workspace from qfca_rank_stats_workspace_bytes. */
-int64_t qfca_rank_stats_workspace_bytes(int64_t n);
-int qfca_rank_stats(const double* scores, const uint8_t* labels, int64_t n, void* workspace,
-                    int64_t workspace_bytes, double* sorted_out, uint64_t* stats, void* stream);
+ * stats[2] = the bits of the best F1 over all thresholds (fp64).  Keys are
+ * fp64 (key_bytes 8) or float32 (4: same order and ties when every score is a
+ * float32 value, half the radix passes).  sorted_out (n keys, may be NULL)
+ * receives the ascending scores (for the PRO quantiles, metrics.py:87-92).
+ * n < 2^31; workspace from qfca_rank_stats_workspace_bytes. */
+int64_t qfca_rank_stats_workspace_bytes(int64_t n, int32_t key_bytes);
+int qfca_rank_stats(const void* scores, int32_t key_bytes, const uint8_t* labels, int64_t n,
+                    void* workspace, int64_t workspace_bytes, void* sorted_out, uint64_t* stats,
+                    void* stream);
 
 /* 8-connected components of a batch of masks (metrics.py:80-84, scipy
  * ndimage.label with a 3x3 structure), images x h x w uint8 -> comp (same

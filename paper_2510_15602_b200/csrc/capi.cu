@@ -8,9 +8,9 @@
 
 namespace qfca {
 int launch_pool_interior(const void*, int32_t, const uint8_t*, int32_t, int32_t, int32_t, int32_t,
-                         double*, uint8_t*, cudaStream_t);
-int64_t rank_stats_workspace_bytes(int64_t);
-int launch_rank_stats(const double*, const uint8_t*, int64_t, void*, int64_t, double*,
+                         double*, uint8_t*, float*, int32_t*, cudaStream_t);
+int64_t rank_stats_workspace_bytes(int64_t, int32_t);
+int launch_rank_stats(const void*, int32_t, const uint8_t*, int64_t, void*, int64_t, void*,
                       unsigned long long*, cudaStream_t);
 int64_t components_workspace_bytes(int64_t);
 int launch_components(const uint8_t*, int32_t, int32_t, int32_t, void*, int64_t, int32_t*, int32_t*,
@@ -524,18 +524,21 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
 
 int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
                        int32_t images, int32_t H, int32_t W, int32_t border, double* out,
-                       uint8_t* labels, void* stream) {
+                       uint8_t* labels, float* out32, int32_t* inexact, void* stream) {
     return counted(launch_pool_interior(scores, scores_bytes, mask, images, H, W, border, out,
-                                        labels, S(stream)), 1);
+                                        labels, out32, inexact, S(stream)), 1);
 }
 
-int64_t qfca_rank_stats_workspace_bytes(int64_t n) { return rank_stats_workspace_bytes(n); }
+int64_t qfca_rank_stats_workspace_bytes(int64_t n, int32_t key_bytes) {
+    return rank_stats_workspace_bytes(n, key_bytes);
+}
 
-int qfca_rank_stats(const double* scores, const uint8_t* labels, int64_t n, void* workspace,
-                    int64_t workspace_bytes, double* sorted_out, uint64_t* stats, void* stream) {
-    // radix sort (CUB, ~4 passes) + 3 rank kernels
-    return counted(launch_rank_stats(scores, labels, n, workspace, workspace_bytes, sorted_out,
-                                     (unsigned long long*)stats, S(stream)), 3);
+int qfca_rank_stats(const void* scores, int32_t key_bytes, const uint8_t* labels, int64_t n,
+                    void* workspace, int64_t workspace_bytes, void* sorted_out, uint64_t* stats,
+                    void* stream) {
+    // radix sort (CUB onesweep passes) + 3 rank kernels
+    return counted(launch_rank_stats(scores, key_bytes, labels, n, workspace, workspace_bytes,
+                                     sorted_out, (unsigned long long*)stats, S(stream)), 3);
 }
 
 int64_t qfca_components_workspace_bytes(int64_t n) { return components_workspace_bytes(n); }

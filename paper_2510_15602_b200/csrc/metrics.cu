@@ -46,15 +46,18 @@ struct MinOp {
     __device__ long long operator()(long long a, long long b) const { return a < b ? a : b; }
 };
 
-__device__ __forceinline__ bool run_start(const double* s, long long i) {
+template <typename K>
+__device__ __forceinline__ bool run_start(const K* s, long long i) {
     return i == 0 || s[i] != s[i - 1];
 }
-__device__ __forceinline__ bool run_last(const double* s, long long i, long long n) {
+template <typename K>
+__device__ __forceinline__ bool run_last(const K* s, long long i, long long n) {
     return i == n - 1 || s[i] != s[i + 1];
 }
 
 // phase A: per tile positives, last run start, first run end
-__global__ void __launch_bounds__(MT) k_rank_tiles(const double* __restrict__ s,
+template <typename K>
+__global__ void __launch_bounds__(MT) k_rank_tiles(const K* __restrict__ s,
                                                    const uint8_t* __restrict__ lab, long long n,
                                                    long long* tpos, long long* tstart,
                                                    long long* tend) {
@@ -127,7 +130,8 @@ __global__ void __launch_bounds__(SB) k_rank_scan(long long* tpos, long long* ts
 
 // phase C: per element run start / run last; accumulate 2 * rank sum of the
 // positives (stats[1]) and the best F1 (stats[2], bits of a non-negative double)
-__global__ void __launch_bounds__(MT) k_rank_emit(const double* __restrict__ s,
+template <typename K>
+__global__ void __launch_bounds__(MT) k_rank_emit(const K* __restrict__ s,
                                                   const uint8_t* __restrict__ lab, long long n,
                                                   const long long* tpos, const long long* tstart,
                                                   const long long* tend,
@@ -142,17 +146,17 @@ __global__ void __launch_bounds__(MT) k_rank_emit(const double* __restrict__ s,
     } tmp;
     // stage the tile: coalesced global loads into shared memory (one padding
     // double per 16 so each thread's 16 consecutive items hit distinct banks)
-    __shared__ double sv[TILE + TILE / MI];
+    __shared__ K sv[TILE + TILE / MI];
     __shared__ __align__(16) uint8_t sl[TILE];
-    __shared__ double halo[2];
+    __shared__ K halo[2];
     const long long t0 = (long long)blockIdx.x * TILE;
     for (int j = threadIdx.x; j < TILE; j += MT) {
         const long long i = t0 + j;
-        sv[j + j / MI] = i < n ? s[i] : 0.0;
+        sv[j + j / MI] = i < n ? s[i] : K(0);
         sl[j] = i < n ? lab[i] : 0;
     }
-    if (threadIdx.x == 0) halo[0] = t0 > 0 ? s[t0 - 1] : 0.0;
-    if (threadIdx.x == 1) halo[1] = t0 + TILE < n ? s[t0 + TILE] : 0.0;
+    if (threadIdx.x == 0) halo[0] = t0 > 0 ? s[t0 - 1] : K(0);
+    if (threadIdx.x == 1) halo[1] = t0 + TILE < n ? s[t0 + TILE] : K(0);
     __syncthreads();
     const int j0 = threadIdx.x * MI;
     const long long base = t0 + j0;
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(MT) k_rank_emit(const double* __restrict__ s,
 #pragma unroll
         for (int k = 0; k < MI; ++k) l[k] = lb[k];
     }
-    double v[MI + 2];
+    K v[MI + 2];
     v[0] = j0 > 0 ? sv[(j0 - 1) + (j0 - 1) / MI] : halo[0];
 #pragma unroll
     for (int k = 0; k < MI; ++k) v[k + 1] = sv[j0 + k + threadIdx.x];  // (j0 + k) / MI == threadIdx.x
@@ -383,7 +387,8 @@ __global__ void k_pro_accumulate(const int* __restrict__ comp_hist, int ncomp, i
 // pooled fp64 copy of the interiors: out[b][y][x] = scores[b][y + bd][x + bd]
 template <typename T>
 __global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restrict__ mk,
-                                int images, int H, int W, int bd, double* out, uint8_t* lab) {
+                                int images, int H, int W, int bd, double* out, uint8_t* lab,
+                                float* out32, int* inexact) {
     const int h = H - 2 * bd, w = W - 2 * bd;
     const long long n = (long long)images * h * w;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -393,8 +398,14 @@ __global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restr
         const int y = (int)(r % h);
         const long long b = r / h;
         const long long src = (b * H + y + bd) * W + x + bd;
-        out[i] = (double)sc[src];
+        const double v = (double)sc[src];
+        out[i] = v;
         if (lab) lab[i] = mk[src] != 0;
+        if (out32) {
+            const float f = (float)v;
+            out32[i] = f;
+            if ((double)f != v) *inexact = 1;  // racy benign write of the same value
+        }
     }
 }
 
@@ -407,9 +418,10 @@ inline int grid_for(long long n, int threads) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+template <typename K>
 size_t sort_temp_bytes(long long n) {
     size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const double*)nullptr, (double*)nullptr,
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const K*)nullptr, (K*)nullptr,
                                     (const uint8_t*)nullptr, (uint8_t*)nullptr, (int)n);
     return bytes;
 }
@@ -424,22 +436,21 @@ size_t scan_temp_bytes(long long n) {
 
 // ---- host launchers (C-ABI wrappers in capi.cu) ----
 
-int64_t rank_stats_workspace_bytes(int64_t n) {
-    if (n < 1 || n >= (1LL << 31)) return -1;
+int64_t rank_stats_workspace_bytes(int64_t n, int32_t key_bytes) {
+    if (n < 1 || n >= (1LL << 31) || (key_bytes != 4 && key_bytes != 8)) return -1;
     const long long ntiles = (n + TILE - 1) / TILE;
-    return (int64_t)(align256(n * sizeof(double)) + align256(n) + 3 * align256(ntiles * 8) +
-                     align256(sort_temp_bytes(n)));
+    const size_t tb = key_bytes == 8 ? sort_temp_bytes<double>(n) : sort_temp_bytes<float>(n);
+    return (int64_t)(align256(n * key_bytes) + align256(n) + 3 * align256(ntiles * 8) +
+                     align256(tb));
 }
 
-int launch_rank_stats(const double* scores, const uint8_t* labels, int64_t n, void* ws,
-                      int64_t ws_bytes, double* sorted_out, unsigned long long* stats,
-                      cudaStream_t st) {
-    const int64_t need = rank_stats_workspace_bytes(n);
-    if (need < 0 || !scores || !labels || !stats || !ws || ws_bytes < need) return QFCA_ERR_ARG;
+template <typename K>
+static int rank_stats_impl(const K* scores, const uint8_t* labels, int64_t n, void* ws,
+                           K* sorted_out, unsigned long long* stats, cudaStream_t st) {
     const long long ntiles = (n + TILE - 1) / TILE;
     char* p = (char*)ws;
-    double* keys = (double*)p;
-    p += align256(n * sizeof(double));
+    K* keys = (K*)p;
+    p += align256(n * sizeof(K));
     uint8_t* lab = (uint8_t*)p;
     p += align256(n);
     long long* tpos = (long long*)p;
@@ -448,19 +459,29 @@ int launch_rank_stats(const double* scores, const uint8_t* labels, int64_t n, vo
     p += align256(ntiles * 8);
     long long* tend = (long long*)p;
     p += align256(ntiles * 8);
-    size_t tb = sort_temp_bytes(n);
-    if (cub::DeviceRadixSort::SortPairs(p, tb, scores, keys, labels, lab, (int)n, 0, 64, st) !=
-        cudaSuccess)
+    size_t tb = sort_temp_bytes<K>(n);
+    if (cub::DeviceRadixSort::SortPairs(p, tb, scores, keys, labels, lab, (int)n, 0,
+                                        (int)(8 * sizeof(K)), st) != cudaSuccess)
         return QFCA_ERR_CUDA;
     if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess)
         return QFCA_ERR_CUDA;
-    k_rank_tiles<<<(unsigned)ntiles, MT, 0, st>>>(keys, lab, n, tpos, tstart, tend);
+    k_rank_tiles<K><<<(unsigned)ntiles, MT, 0, st>>>(keys, lab, n, tpos, tstart, tend);
     k_rank_scan<<<1, SB, 0, st>>>(tpos, tstart, tend, ntiles, stats);
-    k_rank_emit<<<(unsigned)ntiles, MT, 0, st>>>(keys, lab, n, tpos, tstart, tend, stats);
-    if (sorted_out && cudaMemcpyAsync(sorted_out, keys, n * sizeof(double),
-                                      cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    k_rank_emit<K><<<(unsigned)ntiles, MT, 0, st>>>(keys, lab, n, tpos, tstart, tend, stats);
+    if (sorted_out && cudaMemcpyAsync(sorted_out, keys, n * sizeof(K), cudaMemcpyDeviceToDevice,
+                                      st) != cudaSuccess)
         return QFCA_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+int launch_rank_stats(const void* scores, int32_t key_bytes, const uint8_t* labels, int64_t n,
+                      void* ws, int64_t ws_bytes, void* sorted_out, unsigned long long* stats,
+                      cudaStream_t st) {
+    const int64_t need = rank_stats_workspace_bytes(n, key_bytes);
+    if (need < 0 || !scores || !labels || !stats || !ws || ws_bytes < need) return QFCA_ERR_ARG;
+    if (key_bytes == 8)
+        return rank_stats_impl((const double*)scores, labels, n, ws, (double*)sorted_out, stats, st);
+    return rank_stats_impl((const float*)scores, labels, n, ws, (float*)sorted_out, stats, st);
 }
 
 int64_t components_workspace_bytes(int64_t n) {
@@ -516,18 +537,18 @@ int launch_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* 
 
 int launch_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
                          int32_t images, int32_t H, int32_t W, int32_t border, double* out,
-                         uint8_t* labels, cudaStream_t st) {
+                         uint8_t* labels, float* out32, int32_t* inexact, cudaStream_t st) {
     if (images < 1 || border < 0 || 2 * border >= H || 2 * border >= W || !scores || !out ||
-        (labels && !mask))
+        (labels && !mask) || (out32 && !inexact))
         return QFCA_ERR_ARG;
     const long long n = (long long)images * (H - 2 * border) * (W - 2 * border);
     const int g = grid_for(n, 256);
     if (scores_bytes == 8)
         k_pool_interior<double><<<g, 256, 0, st>>>((const double*)scores, mask, images, H, W,
-                                                   border, out, labels);
+                                                   border, out, labels, out32, inexact);
     else if (scores_bytes == 4)
         k_pool_interior<float><<<g, 256, 0, st>>>((const float*)scores, mask, images, H, W,
-                                                  border, out, labels);
+                                                  border, out, labels, out32, inexact);
     else
         return QFCA_ERR_ARG;
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;

@@ -99,6 +99,8 @@ class _Pool:
         self.n = int(sum(sizes))
         self.dtype = np.result_type(*[_np_dtype(s.scores) for s in samples])
         self.scores = empty((self.n,), torch.float64)
+        self.scores32 = empty((self.n,), torch.float32)  # ranked instead when exact
+        self.inexact = zeros((1,), torch.int32)
         self.labels = empty((self.n,), torch.uint8)
         self.image_max = empty((len(samples),), torch.float64)
         off = img = 0
@@ -115,7 +117,8 @@ class _Pool:
                 mk[i].copy_(m.to(device=dev, dtype=torch.uint8))
             h, w = H - 2 * b, W - 2 * b
             N.call("qfca_pool_interior", sc.data_ptr(), 8, mk.data_ptr(), k, H, W, b,
-                   self.scores[off:].data_ptr(), self.labels[off:].data_ptr(), stream)
+                   self.scores[off:].data_ptr(), self.labels[off:].data_ptr(),
+                   self.scores32[off:].data_ptr(), self.inexact.data_ptr(), stream)
             # metrics.py:185-187 -- interior maximum per image
             N.call("qfca_image_score", self.scores[off:].data_ptr(), k, h, w, 0,
                    self.image_max[img:].data_ptr(), stream)
@@ -126,21 +129,25 @@ class _Pool:
         self._rank = None
 
     def rank(self):
-        """(positives, 2 x positive rank sum, best F1, ascending scores)."""
+        """(positives, 2 x positive rank sum, best F1, ascending scores).  When
+        every pooled score is a float32 value (upsampled maps are) the sort
+        runs on 32-bit keys: same order, same ties, half the radix passes."""
         if self._rank is None:
-            self._rank = _rank_stats(self.scores, self.labels, want_sorted=True)
+            keys = self.scores32 if int(self.inexact.item()) == 0 else self.scores
+            self._rank = _rank_stats(keys, self.labels, want_sorted=True)
         return self._rank
 
 
 def _rank_stats(scores: torch.Tensor, labels: torch.Tensor, want_sorted: bool):
     n = scores.numel()
-    wsb = int(N.lib().qfca_rank_stats_workspace_bytes(n))
+    kb = scores.element_size()
+    wsb = int(N.lib().qfca_rank_stats_workspace_bytes(n, kb))
     if wsb < 0:
         raise ValueError(f"{n} pooled pixels: the rank kernels take 1 .. 2^31 - 1")
     ws = empty((wsb,), torch.uint8)
     stats = zeros((3,), torch.int64)
-    srt = empty((n,), torch.float64) if want_sorted else None
-    N.call("qfca_rank_stats", scores.data_ptr(), labels.data_ptr(), n, ws.data_ptr(), wsb,
+    srt = empty((n,), scores.dtype) if want_sorted else None
+    N.call("qfca_rank_stats", scores.data_ptr(), kb, labels.data_ptr(), n, ws.data_ptr(), wsb,
            N.ptr(srt), stats.data_ptr(), N.stream())
     pos, r2, f1bits = (int(v) & 0xFFFFFFFFFFFFFFFF for v in stats.cpu().tolist())
     f1 = struct.unpack("<d", struct.pack("<Q", f1bits))[0]
@@ -243,7 +250,7 @@ def _quantiles(sorted_dev: torch.Tensor, dtype, qs: np.ndarray) -> np.ndarray:
     prev_i = prev.astype(np.intp) % n
     next_i = nxt.astype(np.intp) % n
     idx = torch.from_numpy(np.concatenate([prev_i, next_i]).astype(np.int64)).to(sorted_dev.device)
-    vals = sorted_dev.index_select(0, idx).cpu().numpy().astype(dtype)
+    vals = sorted_dev.index_select(0, idx).double().cpu().numpy().astype(dtype)
     a, b = vals[:qs.size], vals[qs.size:]
     gamma = np.asanyarray(vi - prev.astype(np.intp).astype(np.float64))
     return _lerp(a, b, gamma)

@@ -35,6 +35,8 @@ def make(b, h, w, seed=0):
             ry, rx = rng.integers(4, h // 10), rng.integers(4, w // 10)
             mk[i, max(0, y - ry):y + ry, max(0, x - rx):x + rx] = True
     sc += mk * 0.3
+    # anomaly maps reach evaluation upsampled: float32 values held in fp64
+    sc = sc.float().double()
     return sc, mk
 
 
