@@ -388,9 +388,11 @@ __global__ void k_pro_accumulate(const int* __restrict__ comp_hist, int ncomp, i
 template <typename T>
 __global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restrict__ mk,
                                 int images, int H, int W, int bd, double* out, uint8_t* lab,
-                                float* out32, int* inexact) {
+                                float* out32, int* inexact, unsigned long long* img_max) {
     const int h = H - 2 * bd, w = W - 2 * bd;
     const long long n = (long long)images * h * w;
+    long long cur_b = -1;
+    unsigned long long cur_m = 0;  // order-preserving encoding of the running max
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const int x = (int)(i % w);
@@ -406,7 +408,20 @@ __global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restr
             out32[i] = f;
             if ((double)f != v) *inexact = 1;  // racy benign write of the same value
         }
+        if (img_max) {
+            // metrics.py:175-179 interior maximum per image, folded into the pass
+            const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+            const unsigned long long o = (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+            if (b != cur_b) {
+                if (cur_b >= 0) atomicMax(&img_max[cur_b], cur_m);
+                cur_b = b;
+                cur_m = o;
+            } else if (o > cur_m) {
+                cur_m = o;
+            }
+        }
     }
+    if (img_max && cur_b >= 0) atomicMax(&img_max[cur_b], cur_m);
 }
 
 inline int grid_for(long long n, int threads) {
@@ -537,7 +552,8 @@ int launch_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* 
 
 int launch_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
                          int32_t images, int32_t H, int32_t W, int32_t border, double* out,
-                         uint8_t* labels, float* out32, int32_t* inexact, cudaStream_t st) {
+                         uint8_t* labels, float* out32, int32_t* inexact,
+                         unsigned long long* img_max, cudaStream_t st) {
     if (images < 1 || border < 0 || 2 * border >= H || 2 * border >= W || !scores || !out ||
         (labels && !mask) || (out32 && !inexact))
         return QFCA_ERR_ARG;
@@ -545,10 +561,10 @@ int launch_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t
     const int g = grid_for(n, 256);
     if (scores_bytes == 8)
         k_pool_interior<double><<<g, 256, 0, st>>>((const double*)scores, mask, images, H, W,
-                                                   border, out, labels, out32, inexact);
+                                                   border, out, labels, out32, inexact, img_max);
     else if (scores_bytes == 4)
         k_pool_interior<float><<<g, 256, 0, st>>>((const float*)scores, mask, images, H, W,
-                                                  border, out, labels, out32, inexact);
+                                                  border, out, labels, out32, inexact, img_max);
     else
         return QFCA_ERR_ARG;
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;

@@ -102,7 +102,7 @@ class _Pool:
         self.scores32 = empty((self.n,), torch.float32)  # ranked instead when exact
         self.inexact = zeros((1,), torch.int32)
         self.labels = empty((self.n,), torch.uint8)
-        self.image_max = empty((len(samples),), torch.float64)
+        enc = zeros((len(samples),), torch.int64)  # order-preserving max encoding
         off = img = 0
         for g, size in zip(groups, sizes):
             (H, W), b = g[0][0]
@@ -118,14 +118,17 @@ class _Pool:
             h, w = H - 2 * b, W - 2 * b
             N.call("qfca_pool_interior", sc.data_ptr(), 8, mk.data_ptr(), k, H, W, b,
                    self.scores[off:].data_ptr(), self.labels[off:].data_ptr(),
-                   self.scores32[off:].data_ptr(), self.inexact.data_ptr(), stream)
-            # metrics.py:185-187 -- interior maximum per image
-            N.call("qfca_image_score", self.scores[off:].data_ptr(), k, h, w, 0,
-                   self.image_max[img:].data_ptr(), stream)
+                   self.scores32[off:].data_ptr(), self.inexact.data_ptr(),
+                   enc[img:].data_ptr(), stream)
             self.groups.append((off, k, h, w))
             off += size
             img += k
         self.image_labels = np.array([bool(s.image_label) for s in samples], dtype=bool)
+        # metrics.py:175-179 -- interior maxima, decoded from the pool kernel's encoding
+        u = enc.cpu().numpy().view(np.uint64)
+        top = (u >> np.uint64(63)).astype(bool)
+        bits = np.where(top, u & np.uint64(0x7FFFFFFFFFFFFFFF), ~u)
+        self.image_max = torch.from_numpy(bits.view(np.float64).copy()).to(dev)
         self._rank = None
 
     def rank(self):
