@@ -244,10 +244,14 @@ int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, 
  * mask (images, H, W) uint8 -> out (images, H-2b, W-2b) fp64 and, if labels is
  * not NULL, labels (same shape) uint8 0/1.  If out32 is not NULL it also gets
  * the values as float32, and *inexact (device int32, zeroed by the caller) is
- * set when some value is not a float32 value (then out32 must not be ranked). */
+ * set when some value is not a float32 value (then out32 must not be ranked).
+ * If image_max is not NULL (images uint64, zeroed by the caller) it receives
+ * each image's interior maximum (metrics.py:175-179) in an order-preserving
+ * encoding: u = bits(v) | 2^63 for v >= 0, else u = ~bits(v). */
 int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
                        int32_t images, int32_t H, int32_t W, int32_t border, double* out,
-                       uint8_t* labels, float* out32, int32_t* inexact, void* stream);
+                       uint8_t* labels, float* out32, int32_t* inexact, uint64_t* image_max,
+                       void* stream);
 
 /* Rank statistics of pooled scores (metrics.py:44-58 _rank_auroc,
  * 157-172 f1_optimal): one stable sort, then stats[0] = positives,
