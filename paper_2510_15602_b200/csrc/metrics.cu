@@ -393,8 +393,12 @@ __global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restr
     const long long n = (long long)images * h * w;
     long long cur_b = -1;
     unsigned long long cur_m = 0;  // order-preserving encoding of the running max
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
+    // block-contiguous chunks (coalesced within the block): a thread meets at
+    // most a couple of images, so the per-image max costs one atomic per
+    // thread and image instead of one per element
+    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const long long end = min(n, (long long)(blockIdx.x + 1) * chunk);
+    for (long long i = (long long)blockIdx.x * chunk + threadIdx.x; i < end; i += blockDim.x) {
         const int x = (int)(i % w);
         const long long r = i / w;
         const int y = (int)(r % h);
