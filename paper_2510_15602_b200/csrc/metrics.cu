@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(SB) k_rank_scan(long long* tpos, long long* ts
 // phase C: per element run start / run last; accumulate 2 * rank sum of the
 // positives (stats[1]) and the best F1 (stats[2], bits of a non-negative double)
 template <typename K>
-__global__ void __launch_bounds__(MT) k_rank_emit(const K* __restrict__ s,
+__global__ void __launch_bounds__(MT, 4) k_rank_emit(const K* __restrict__ s,
                                                   const uint8_t* __restrict__ lab, long long n,
                                                   const long long* tpos, const long long* tstart,
                                                   const long long* tend,
@@ -160,34 +160,36 @@ __global__ void __launch_bounds__(MT) k_rank_emit(const K* __restrict__ s,
     __syncthreads();
     const int j0 = threadIdx.x * MI;
     const long long base = t0 + j0;
-    uint8_t l[MI];
-    bool fs[MI], fl[MI];
+    // per-item bits: label, run start, run last (registers instead of arrays)
+    unsigned lbits = 0, fsb = 0, flb = 0;
     {
         const uint4 lv = *reinterpret_cast<const uint4*>(&sl[j0]);
         const uint8_t* lb = reinterpret_cast<const uint8_t*>(&lv);
 #pragma unroll
-        for (int k = 0; k < MI; ++k) l[k] = lb[k];
+        for (int k = 0; k < MI; ++k) lbits |= (lb[k] != 0 ? 1u : 0u) << k;
     }
-    K v[MI + 2];
-    v[0] = j0 > 0 ? sv[(j0 - 1) + (j0 - 1) / MI] : halo[0];
-#pragma unroll
-    for (int k = 0; k < MI; ++k) v[k + 1] = sv[j0 + k + threadIdx.x];  // (j0 + k) / MI == threadIdx.x
-    v[MI + 1] = j0 + MI < TILE ? sv[(j0 + MI) + (j0 + MI) / MI] : halo[1];
     long long p_loc = 0, st_loc = -1, en_loc = NO_END;
+    {
+        K prev = j0 > 0 ? sv[(j0 - 1) + (j0 - 1) / MI] : halo[0];
+        K cur = sv[j0 + threadIdx.x];  // (j0 + k) / MI == threadIdx.x
 #pragma unroll
-    for (int k = 0; k < MI; ++k) {
-        const long long i = base + k;
-        if (i < n) {
-            fs[k] = i == 0 || v[k + 1] != v[k];
-            fl[k] = i == n - 1 || v[k + 1] != v[k + 2];
-            p_loc += l[k] != 0;
-            if (fs[k]) st_loc = i;
-            if (fl[k] && en_loc == NO_END) en_loc = i;
-        } else {
-            l[k] = 0;
-            fs[k] = fl[k] = false;
+        for (int k = 0; k < MI; ++k) {
+            const K nxt = k + 1 < MI ? sv[j0 + k + 1 + threadIdx.x]
+                                     : (j0 + MI < TILE ? sv[(j0 + MI) + (j0 + MI) / MI] : halo[1]);
+            const long long i = base + k;
+            if (i < n) {
+                if (i == 0 || cur != prev) fsb |= 1u << k;
+                if (i == n - 1 || cur != nxt) flb |= 1u << k;
+            } else {
+                lbits &= ~(1u << k);
+            }
+            prev = cur;
+            cur = nxt;
         }
     }
+    p_loc = __popc(lbits);
+    if (fsb) st_loc = base + 31 - __clz(fsb);
+    if (flb) en_loc = base + __ffs(flb) - 1;
     // forward: exclusive positives and last run start before this thread
     long long p_ex, st_ex;
     BS(tmp.scan).ExclusiveSum(p_loc, p_ex);
@@ -210,31 +212,31 @@ __global__ void __launch_bounds__(MT) k_rank_emit(const K* __restrict__ s,
     long long start = st_ex > ts0 ? st_ex : ts0;
     long long nxt_end = en_ex < te0 ? en_ex : te0;
     const long long total_pos = (long long)stats[0];
-    // run last index for each item: scan the thread's items from the right
-    long long last[MI];
+    unsigned long long r2 = 0;
+    // backward over the items: the run's last index for every positive
     {
         long long e = nxt_end;
 #pragma unroll
         for (int k = MI - 1; k >= 0; --k) {
-            if (fl[k]) e = base + k;
-            last[k] = e;
+            if ((flb >> k) & 1u) e = base + k;
+            if ((lbits >> k) & 1u) r2 += (unsigned long long)e;
         }
     }
-    unsigned long long r2 = 0;
     double f1 = 0.0;
 #pragma unroll
     for (int k = 0; k < MI; ++k) {
         const long long i = base + k;
-        if (i >= n) break;
-        if (fs[k]) {
+        if ((fsb >> k) & 1u) {
             start = i;
             // metrics.py:166-171 -- threshold at this run: k = n - i predicted, tp positives
             const long long tp = total_pos - pcount;
             const double f = 2.0 * (double)tp / (double)((n - i) + total_pos);
             f1 = f > f1 ? f : f1;
         }
-        if (l[k]) r2 += (unsigned long long)(start + last[k] + 2);
-        pcount += l[k] != 0;
+        if ((lbits >> k) & 1u) {
+            r2 += (unsigned long long)(start + 2);
+            ++pcount;
+        }
     }
     unsigned long long r2b = BRu(tmp.ru).Sum(r2);
     __syncthreads();
