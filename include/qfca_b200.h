@@ -253,6 +253,16 @@ int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* 
                        uint8_t* labels, float* out32, int32_t* inexact, uint64_t* image_max,
                        void* stream);
 
+/* qfca_pool_interior over separately allocated maps (metrics.py:61-68, the
+ * same _pooled order): score_images and mask_images are DEVICE arrays of
+ * `images` device pointers, each to one contiguous H x W map (scores_bytes 8
+ * or 4; masks one byte per pixel, nonzero = anomalous, e.g. torch.bool).
+ * Saves stacking a class's maps into one buffer before pooling. */
+int qfca_pool_interior_table(const void* const* score_images, int32_t scores_bytes,
+                             const uint8_t* const* mask_images, int32_t images, int32_t H,
+                             int32_t W, int32_t border, double* out, uint8_t* labels, float* out32,
+                             int32_t* inexact, uint64_t* image_max, void* stream);
+
 /* Rank statistics of pooled scores (metrics.py:44-58 _rank_auroc,
  * 157-172 f1_optimal): one stable sort, then stats[0] = positives,
  * stats[1] = 2 x the rank sum of the positives (average ranks for ties; exact),

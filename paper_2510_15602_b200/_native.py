@@ -75,6 +75,8 @@ _SIGNATURES = {
     "qfca_detect_ex": ([_P, _I64, _I32, _I32, _I32, ctypes.POINTER(QfcaConfig), _P, _I64, _P,
                         _P, _P, _P, _P, _P], _I32),
     "qfca_pool_interior": ([_P, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "qfca_pool_interior_table": ([_P, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P],
+                                 _I32),
     "qfca_rank_stats_workspace_bytes": ([_I64, _I32], _I64),
     "qfca_rank_stats": ([_P, _I32, _P, _I64, _P, _I64, _P, _P, _P], _I32),
     "qfca_components_workspace_bytes": ([_I64], _I64),

@@ -7,8 +7,9 @@
 #include "common.cuh"
 
 namespace qfca {
-int launch_pool_interior(const void*, int32_t, const uint8_t*, int32_t, int32_t, int32_t, int32_t,
-                         double*, uint8_t*, float*, int32_t*, unsigned long long*, cudaStream_t);
+int launch_pool_interior(const void*, const void* const*, int32_t, const uint8_t*,
+                         const uint8_t* const*, int32_t, int32_t, int32_t, int32_t, double*,
+                         uint8_t*, float*, int32_t*, unsigned long long*, cudaStream_t);
 int64_t rank_stats_workspace_bytes(int64_t, int32_t);
 int launch_rank_stats(const void*, int32_t, const uint8_t*, int64_t, void*, int64_t, void*,
                       unsigned long long*, cudaStream_t);
@@ -526,9 +527,19 @@ int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* 
                        int32_t images, int32_t H, int32_t W, int32_t border, double* out,
                        uint8_t* labels, float* out32, int32_t* inexact, uint64_t* image_max,
                        void* stream) {
-    return counted(launch_pool_interior(scores, scores_bytes, mask, images, H, W, border, out,
-                                        labels, out32, inexact, (unsigned long long*)image_max,
-                                        S(stream)), 1);
+    return counted(launch_pool_interior(scores, nullptr, scores_bytes, mask, nullptr, images, H,
+                                        W, border, out, labels, out32, inexact,
+                                        (unsigned long long*)image_max, S(stream)), 1);
+}
+
+int qfca_pool_interior_table(const void* const* score_images, int32_t scores_bytes,
+                             const uint8_t* const* mask_images, int32_t images, int32_t H,
+                             int32_t W, int32_t border, double* out, uint8_t* labels, float* out32,
+                             int32_t* inexact, uint64_t* image_max, void* stream) {
+    if (!score_images) return QFCA_ERR_ARG;
+    return counted(launch_pool_interior(nullptr, score_images, scores_bytes, nullptr, mask_images,
+                                        images, H, W, border, out, labels, out32, inexact,
+                                        (unsigned long long*)image_max, S(stream)), 1);
 }
 
 int64_t qfca_rank_stats_workspace_bytes(int64_t n, int32_t key_bytes) {

@@ -387,43 +387,69 @@ __global__ void k_pro_accumulate(const int* __restrict__ comp_hist, int ncomp, i
 }
 
 // pooled fp64 copy of the interiors: out[b][y][x] = scores[b][y + bd][x + bd]
+// (sc_tbl / mk_tbl non-null: image b is read from sc_tbl[b] / mk_tbl[b], each
+// a contiguous H x W map, instead of from the stacked sc / mk)
 template <typename T>
 __global__ void k_pool_interior(const T* __restrict__ sc, const uint8_t* __restrict__ mk,
-                                int images, int H, int W, int bd, double* out, uint8_t* lab,
-                                float* out32, int* inexact, unsigned long long* img_max) {
+                                const T* const* __restrict__ sc_tbl,
+                                const uint8_t* const* __restrict__ mk_tbl,
+                                int images, int H, int W, int bd, double* __restrict__ out,
+                                uint8_t* __restrict__ lab, float* __restrict__ out32,
+                                int* inexact, unsigned long long* img_max) {
     const int h = H - 2 * bd, w = W - 2 * bd;
-    const long long n = (long long)images * h * w;
+    const long long rows = (long long)images * h;
     long long cur_b = -1;
     unsigned long long cur_m = 0;  // order-preserving encoding of the running max
-    // block-contiguous chunks (coalesced within the block): a thread meets at
-    // most a couple of images, so the per-image max costs one atomic per
-    // thread and image instead of one per element
-    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
-    const long long end = min(n, (long long)(blockIdx.x + 1) * chunk);
-    for (long long i = (long long)blockIdx.x * chunk + threadIdx.x; i < end; i += blockDim.x) {
-        const int x = (int)(i % w);
-        const long long r = i / w;
-        const int y = (int)(r % h);
+    // block-contiguous runs of interior rows (coalesced along each row): the
+    // row's image and source pointers are computed once per row, and a
+    // thread meets at most a couple of images, so the per-image max costs one
+    // atomic per thread and image instead of one per element
+    const long long chunk = (rows + gridDim.x - 1) / gridDim.x;
+    const long long r_end = min(rows, (long long)(blockIdx.x + 1) * chunk);
+    for (long long r = (long long)blockIdx.x * chunk; r < r_end; ++r) {
         const long long b = r / h;
-        const long long src = (b * H + y + bd) * W + x + bd;
-        const double v = (double)sc[src];
-        out[i] = v;
-        if (lab) lab[i] = mk[src] != 0;
-        if (out32) {
-            const float f = (float)v;
-            out32[i] = f;
-            if ((double)f != v) *inexact = 1;  // racy benign write of the same value
+        const int y = (int)(r - b * h);
+        const long long pix = (long long)(y + bd) * W + bd;
+        const T* srow = (sc_tbl ? sc_tbl[b] : sc + b * H * W) + pix;
+        const uint8_t* mrow = lab ? (mk_tbl ? mk_tbl[b] : mk + b * H * W) + pix : nullptr;
+        const long long o0 = r * w;
+        unsigned long long row_m = 0;
+        bool any = false;
+        constexpr int U = 4;  // loads of U row elements in flight per thread
+        for (int x0 = threadIdx.x; x0 < w; x0 += U * blockDim.x) {
+            double v[U];
+            uint8_t m[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int x = x0 + u * blockDim.x;
+                v[u] = x < w ? (double)srow[x] : 0.0;
+                m[u] = (lab && x < w) ? mrow[x] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int x = x0 + u * blockDim.x;
+                if (x >= w) break;
+                out[o0 + x] = v[u];
+                if (lab) lab[o0 + x] = m[u] != 0;
+                if (out32) {
+                    const float f = (float)v[u];
+                    out32[o0 + x] = f;
+                    if ((double)f != v[u]) *inexact = 1;  // racy benign write of the same value
+                }
+                // metrics.py:175-179 interior maximum per image, folded into the pass
+                const unsigned long long b64 = (unsigned long long)__double_as_longlong(v[u]);
+                const unsigned long long o = (b64 >> 63) ? ~b64 : (b64 | 0x8000000000000000ULL);
+                row_m = (!any || o > row_m) ? o : row_m;
+                any = true;
+            }
         }
-        if (img_max) {
-            // metrics.py:175-179 interior maximum per image, folded into the pass
-            const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-            const unsigned long long o = (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+        if (img_max && any) {
             if (b != cur_b) {
                 if (cur_b >= 0) atomicMax(&img_max[cur_b], cur_m);
                 cur_b = b;
-                cur_m = o;
-            } else if (o > cur_m) {
-                cur_m = o;
+                cur_m = row_m;
+            } else if (row_m > cur_m) {
+                cur_m = row_m;
             }
         }
     }
@@ -556,21 +582,25 @@ int launch_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* 
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
-int launch_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* mask,
-                         int32_t images, int32_t H, int32_t W, int32_t border, double* out,
-                         uint8_t* labels, float* out32, int32_t* inexact,
-                         unsigned long long* img_max, cudaStream_t st) {
-    if (images < 1 || border < 0 || 2 * border >= H || 2 * border >= W || !scores || !out ||
-        (labels && !mask) || (out32 && !inexact))
+int launch_pool_interior(const void* scores, const void* const* score_tbl, int32_t scores_bytes,
+                         const uint8_t* mask, const uint8_t* const* mask_tbl, int32_t images,
+                         int32_t H, int32_t W, int32_t border, double* out, uint8_t* labels,
+                         float* out32, int32_t* inexact, unsigned long long* img_max,
+                         cudaStream_t st) {
+    if (images < 1 || border < 0 || 2 * border >= H || 2 * border >= W ||
+        (!scores && !score_tbl) || !out || (labels && !mask && !mask_tbl) ||
+        (out32 && !inexact))
         return QFCA_ERR_ARG;
     const long long n = (long long)images * (H - 2 * border) * (W - 2 * border);
     const int g = grid_for(n, 256);
     if (scores_bytes == 8)
-        k_pool_interior<double><<<g, 256, 0, st>>>((const double*)scores, mask, images, H, W,
-                                                   border, out, labels, out32, inexact, img_max);
+        k_pool_interior<double><<<g, 256, 0, st>>>(
+            (const double*)scores, mask, (const double* const*)score_tbl, mask_tbl, images, H, W,
+            border, out, labels, out32, inexact, img_max);
     else if (scores_bytes == 4)
-        k_pool_interior<float><<<g, 256, 0, st>>>((const float*)scores, mask, images, H, W,
-                                                  border, out, labels, out32, inexact, img_max);
+        k_pool_interior<float><<<g, 256, 0, st>>>(
+            (const float*)scores, mask, (const float* const*)score_tbl, mask_tbl, images, H, W,
+            border, out, labels, out32, inexact, img_max);
     else
         return QFCA_ERR_ARG;
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;

@@ -71,6 +71,30 @@ def _np_dtype(a):
     return np.asarray(a).dtype
 
 
+def _device_tables(group, dev):
+    """(score bytes, score pointer table, mask pointer table) on ``dev`` when
+    every map of the group is already a contiguous device tensor (scores all
+    float64 or all float32, masks bool / uint8), else None."""
+    sd = None
+    sp, mp = [], []
+    for _, s in group:
+        sc, m = s.scores, s.mask
+        if not (is_torch(sc) and is_torch(m)) or sc.device != dev or m.device != dev:
+            return None
+        if sc.dtype not in (torch.float64, torch.float32) or (sd is not None and sc.dtype != sd):
+            return None
+        if m.dtype not in (torch.bool, torch.uint8) or tuple(m.shape) != tuple(sc.shape):
+            return None
+        if not (sc.is_contiguous() and m.is_contiguous()):
+            return None
+        sd = sc.dtype
+        sp.append(sc.data_ptr())
+        mp.append(m.data_ptr())
+    tab = torch.tensor(sp + mp, dtype=torch.int64).pin_memory().to(dev, non_blocking=True)
+    k = len(sp)
+    return (8 if sd == torch.float64 else 4), tab[:k], tab[k:]
+
+
 class _Pool:
     """Device copy of the pooled interiors (metrics.py:61-68 _pooled order).
 
@@ -84,6 +108,7 @@ class _Pool:
         dev = N.require_cuda()
         stream = N.stream()
         self.groups = []  # (offset, images, h, w)
+        self._tables = []
         groups, cur = [], []
         for s in samples:
             key = (_shape(s.scores), s.border)
@@ -107,19 +132,27 @@ class _Pool:
         for g, size in zip(groups, sizes):
             (H, W), b = g[0][0]
             k = len(g)
-            sc = empty((k, H, W), torch.float64)
-            mk = empty((k, H, W), torch.uint8)
-            for i, (_, s) in enumerate(g):
-                sc[i].copy_(torch.as_tensor(np.asarray(s.scores, dtype=np.float64))
-                            if not is_torch(s.scores) else s.scores.to(torch.float64))
-                m = s.mask if is_torch(s.mask) else torch.from_numpy(
-                    np.ascontiguousarray(np.asarray(s.mask, dtype=bool)))
-                mk[i].copy_(m.to(device=dev, dtype=torch.uint8))
             h, w = H - 2 * b, W - 2 * b
-            N.call("qfca_pool_interior", sc.data_ptr(), 8, mk.data_ptr(), k, H, W, b,
-                   self.scores[off:].data_ptr(), self.labels[off:].data_ptr(),
+            out = (self.scores[off:].data_ptr(), self.labels[off:].data_ptr(),
                    self.scores32[off:].data_ptr(), self.inexact.data_ptr(),
                    enc[img:].data_ptr(), stream)
+            tbl = _device_tables(g, dev)
+            if tbl is not None:
+                # maps already resident: read each in place through a pointer table
+                sb, stab, mtab = tbl
+                self._tables.append(stab)  # alive until the pool is dropped
+                N.call("qfca_pool_interior_table", stab.data_ptr(), sb, mtab.data_ptr(), k, H, W,
+                       b, *out)
+            else:
+                sc = empty((k, H, W), torch.float64)
+                mk = empty((k, H, W), torch.uint8)
+                for i, (_, s) in enumerate(g):
+                    sc[i].copy_(torch.as_tensor(np.asarray(s.scores, dtype=np.float64))
+                                if not is_torch(s.scores) else s.scores.to(torch.float64))
+                    m = s.mask if is_torch(s.mask) else torch.from_numpy(
+                        np.ascontiguousarray(np.asarray(s.mask, dtype=bool)))
+                    mk[i].copy_(m.to(device=dev, dtype=torch.uint8))
+                N.call("qfca_pool_interior", sc.data_ptr(), 8, mk.data_ptr(), k, H, W, b, *out)
             self.groups.append((off, k, h, w))
             off += size
             img += k

@@ -115,11 +115,12 @@ def _random_set(rng, n_img, h, w, border, ties=None, dtype=np.float64):
     (12, 6, 97, 131, 7, 2, np.float32),
     (13, 3, 256, 256, 2, 0, np.float64),   # very few distinct scores
 ])
-def test_gpu_metrics_vs_oracle(seed, n_img, h, w, border, ties, dtype):
+@pytest.mark.parametrize("torch_inputs", [False, True])  # True: pointer-table pooling
+def test_gpu_metrics_vs_oracle(seed, n_img, h, w, border, ties, dtype, torch_inputs):
     from paper_2510_15602_b200 import metrics as M
     rng = np.random.default_rng(seed)
     s = _random_set(rng, n_img, h, w, border, ties, dtype)
-    ev = _samples(M, s)
+    ev = _samples(M, s, torch_inputs)
     sc, lb = O.metrics_pooled(s)
     assert M.auroc_pixel(ev) == pytest.approx(O.rank_auroc(sc, lb), abs=1e-15)
     assert M.f1_optimal(ev) == O.f1_optimal(sc, lb)
@@ -152,3 +153,22 @@ def test_gpu_metrics_undefined_and_errors():
     allpos = [M.EvalSample(scores=np.arange(64.0).reshape(8, 8), mask=z == 0, image_label=True)]
     s = [(allpos[0].scores, allpos[0].mask, True, 0)]
     assert M.pro_at_fpr(allpos) == O.pro_at_fpr(s)
+
+
+@pytest.mark.gpu
+def test_gpu_pool_table_and_staged_paths_agree():
+    """Device maps pooled in place (qfca_pool_interior_table) against the same
+    maps staged (a non-contiguous view forces the staging copy)."""
+    import torch
+    from paper_2510_15602_b200 import metrics as M
+    rng = np.random.default_rng(5)
+    s = _random_set(rng, 4, 64, 80, 3, None, np.float32)
+    ev_t = _samples(M, s, True)
+    ev_s = [M.EvalSample(scores=torch.from_numpy(sc.T.copy()).cuda().t(),
+                         mask=torch.from_numpy(m).cuda(), image_label=lab, border=b)
+            for sc, m, lab, b in s]
+    assert not ev_s[0].scores.is_contiguous()
+    pt, ps = M._Pool(ev_t), M._Pool(ev_s)
+    assert len(pt._tables) == 1 and len(ps._tables) == 0
+    assert torch.equal(pt.scores, ps.scores) and torch.equal(pt.labels, ps.labels)
+    assert torch.equal(pt.scores32, ps.scores32) and torch.equal(pt.image_max, ps.image_max)
