@@ -362,15 +362,26 @@ __global__ void __launch_bounds__(256) k_pro_hist(const double* __restrict__ s,
         if (nh[j]) atomicAdd(&normal_hist[j], (unsigned long long)nh[j]);
 }
 
-// per component: suffix sums in place, S[c] = pixels in slots >= c (S[0] = size)
+// per component: suffix sums in place, S[c] = pixels in slots >= c (S[0] = size).
+// One warp per component walks its m + 1 slots from the top in coalesced
+// 32-slot chunks: a warp suffix scan per chunk plus the carry from above.
 __global__ void k_pro_suffix(int* comp_hist, int ncomp, int m) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (q >= ncomp) return;
     int* h = comp_hist + (long long)q * (m + 1);
-    int acc = 0;
-    for (int c = m; c >= 0; --c) {
-        acc += h[c];
-        h[c] = acc;
+    int carry = 0;
+    for (int c0 = (m / 32) * 32; c0 >= 0; c0 -= 32) {
+        const int c = c0 + lane;
+        int v = c <= m ? h[c] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_down_sync(0xffffffffu, v, d);
+            if (lane + d < 32) v += o;
+        }
+        v += carry;
+        if (c <= m) h[c] = v;
+        carry = __shfl_sync(0xffffffffu, v, 0);
     }
 }
 
@@ -577,7 +588,7 @@ int launch_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* 
                           cudaStream_t st) {
     if (ncomp < 0 || m < 1 || m > MAX_THR || !pro || (ncomp > 0 && !comp_hist)) return QFCA_ERR_ARG;
     if (ncomp == 0) return QFCA_OK;
-    k_pro_suffix<<<(ncomp + 255) / 256, 256, 0, st>>>(comp_hist, ncomp, m);
+    k_pro_suffix<<<(int)(((long long)ncomp * 32 + 255) / 256), 256, 0, st>>>(comp_hist, ncomp, m);
     k_pro_accumulate<<<(m + 127) / 128, 128, 0, st>>>(comp_hist, ncomp, m, pro);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
