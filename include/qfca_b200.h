@@ -5,8 +5,8 @@
  * Python; it has no C FFI.  Its closest native surface is the pair of Numba
  * kernels that a binding would replace:
  *   _channel_score_kernel(idx, nbins, t, pad_code, refw, centers, score_out)
- *       scoring.py:205-260           -> qfca_score (+ qfca_select_reference)
- *   mismatch_batch(Pb, R, Q, out)      transport.py:310-325 -> qfca_mismatch_pixels
+ *       scoring.py:177-232           -> qfca_score (+ qfca_select_reference)
+ *   mismatch_batch(Pb, R, Q, out)      transport.py:110-125 -> qfca_mismatch_pixels
  * and the NumPy stages around them, each of which gets an entry point below
  * (file:line of the function it replaces in the comment).  libqfca_b200.so
  * exports exactly these symbols.
@@ -21,7 +21,7 @@
  *   - feature planes are float32, contiguous (images, channels, h, w); a
  *     "plane" is one (image, channel) h x w map; bins are uint8 (n_bins <=
  *     256), uint16 (<= 65536) or int32 (bins_bytes = 1, 2, 4);
- *   - pad codes follow scoring.py:183: 0 zero, 1 reflect, 2 wrap.
+ *   - pad codes follow scoring.py:155: 0 zero, 1 reflect, 2 wrap.
  */
 #ifndef QFCA_B200_H
 #define QFCA_B200_H
@@ -83,19 +83,19 @@ int qfca_window_counts(const void* bins, int32_t bins_bytes, int64_t planes, int
                        int32_t w, int32_t n_bins, int32_t patch_size, int32_t pad,
                        uint16_t* scratch, void* counts, int32_t counts_kind, void* stream);
 
-/* mismatch_batch (transport.py:310-325) over every pixel of every plane:
+/* mismatch_batch (transport.py:110-125) over every pixel of every plane:
  * counts (planes, n_bins, hw) uint16, ref_weights / centers (planes, n_bins)
  * fp64, err (planes, n_bins, hw) fp64.  skip[plane] != 0 -> zero errors. */
 int qfca_mismatch_pixels(const uint16_t* counts, int64_t planes, int64_t hw, int32_t n_bins,
                          const double* ref_weights, const double* centers, const uint8_t* skip,
                          double* err, void* stream);
 
-/* mismatch_batch (transport.py:310-325) verbatim: Pb (rows, n_bins) fp64
+/* mismatch_batch (transport.py:110-125) verbatim: Pb (rows, n_bins) fp64
  * row-major, R / Q (n_bins) fp64, out (rows, n_bins) fp64 */
 int qfca_mismatch_rows(const double* Pb, int64_t rows, int32_t n_bins, const double* R,
                        const double* Q, double* out, void* stream);
 
-/* _smooth_error_planes + own-bin gather (scoring.py:116-140): separable filter
+/* _smooth_error_planes + own-bin gather (scoring.py:88-112): separable filter
  * of the error planes with taps (host array, patch_size taps: ones for the
  * box, the normalised Gaussian for finite sigma_p), times post_scale, read at
  * each pixel's own bin.  scratch: planes*n_bins*h*w fp64; score: planes*h*w. */
@@ -104,12 +104,12 @@ int qfca_smooth_gather(const double* err, const void* bins, int32_t bins_bytes, 
                        const double* taps_host, double post_scale, double* scratch,
                        double* score, void* stream);
 
-/* fixed-order channel sum (scoring.py:292-309) of per-channel scores */
+/* fixed-order channel sum (scoring.py:264-281) of per-channel scores */
 int qfca_channel_sum(const double* score, int64_t images, int32_t channels, int64_t hw,
                      const uint8_t* skip, int32_t accumulate, double* acc, int32_t* used,
                      void* stream);
 
-/* number of non-degenerate channels per image (scoring.py:309 `used`) */
+/* number of non-degenerate channels per image (scoring.py:281 `used`) */
 int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t channels,
                     int32_t* used, void* stream);
 
@@ -135,7 +135,7 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
 int qfca_set_score_kernel(int32_t version);
 
 /* THE HOT PATH: _channel_score_kernel + channel accumulation
- * (scoring.py:205-260, 286-309) fused, for uniform sigma_p, median-quan and
+ * (scoring.py:177-232, 258-281) fused, for uniform sigma_p, median-quan and
  * reflect / wrap padding.  ref_cum = qfca_select_reference mode-0 stats, or
  * NULL to select the reference inside the kernel (select_reference,
  * quantize.py:150-200, from the same window counts; sample_budget applies).
@@ -146,7 +146,7 @@ int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const floa
                int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
                int32_t groups, float* partial, void* stream);
 
-/* agg = (sum over groups, fixed order, fp64) / used   (scoring.py:311-317) */
+/* agg = (sum over groups, fixed order, fp64) / used   (scoring.py:283-289) */
 int qfca_reduce_partials(const float* partial, int64_t images, int32_t groups, int64_t hw,
                          const int32_t* used, double* agg, void* stream);
 int qfca_divide_used(const double* acc, int64_t images, int64_t hw, const int32_t* used,
@@ -156,11 +156,11 @@ int qfca_divide_used(const double* acc, int64_t images, int64_t hw, const int32_
 int qfca_sep_conv(const double* in, int64_t images, int32_t h, int32_t w, int32_t axis,
                   const double* taps_host, int32_t ntaps, int32_t pad, double* out, void* stream);
 
-/* image_score_of (scoring.py:169-174) */
+/* image_score_of (scoring.py:141-146) */
 int qfca_image_score(const double* scores, int64_t images, int32_t h, int32_t w, int32_t border,
                      double* image_score, void* stream);
 
-/* upsample_scores (scoring.py:177-180, tensor_io.py:127-151) -> float32 */
+/* upsample_scores (scoring.py:149-152, tensor_io.py:127-151) -> float32 */
 int qfca_upsample(const double* in, int64_t images, int32_t h, int32_t w, int32_t out_h,
                   int32_t out_w, float* out, void* stream);
 
@@ -239,7 +239,7 @@ int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, 
 
 /* ---- evaluation metrics (metrics.py) ---- */
 
-/* Pooled interiors of a batch of maps (metrics.py:36-41 EvalSample.interior,
+/* Pooled interiors of a batch of maps (metrics.py:37-41 EvalSample.interior,
  * 61-68 _pooled): scores (images, H, W) fp64 (scores_bytes 8) or fp32 (4),
  * mask (images, H, W) uint8 -> out (images, H-2b, W-2b) fp64 and, if labels is
  * not NULL, labels (same shape) uint8 0/1.  If out32 is not NULL it also gets
@@ -253,7 +253,7 @@ int qfca_pool_interior(const void* scores, int32_t scores_bytes, const uint8_t* 
                        uint8_t* labels, float* out32, int32_t* inexact, uint64_t* image_max,
                        void* stream);
 
-/* qfca_pool_interior over separately allocated maps (metrics.py:61-68, the
+/* qfca_pool_interior over separately allocated maps (metrics.py:62-68, the
  * same _pooled order): score_images and mask_images are DEVICE arrays of
  * `images` device pointers, each to one contiguous H x W map (scores_bytes 8
  * or 4; masks one byte per pixel, nonzero = anomalous, e.g. torch.bool).
@@ -269,14 +269,14 @@ int qfca_pool_interior_table(const void* const* score_images, int32_t scores_byt
  * stats[2] = the bits of the best F1 over all thresholds (fp64).  Keys are
  * fp64 (key_bytes 8) or float32 (4: same order and ties when every score is a
  * float32 value, half the radix passes).  sorted_out (n keys, may be NULL)
- * receives the ascending scores (for the PRO quantiles, metrics.py:87-92).
+ * receives the ascending scores (for the PRO quantiles, metrics.py:83-88).
  * n < 2^31; workspace from qfca_rank_stats_workspace_bytes. */
 int64_t qfca_rank_stats_workspace_bytes(int64_t n, int32_t key_bytes);
 int qfca_rank_stats(const void* scores, int32_t key_bytes, const uint8_t* labels, int64_t n,
                     void* workspace, int64_t workspace_bytes, void* sorted_out, uint64_t* stats,
                     void* stream);
 
-/* 8-connected components of a batch of masks (metrics.py:80-84, scipy
+/* 8-connected components of a batch of masks (metrics.py:76-80, scipy
  * ndimage.label with a 3x3 structure), images x h x w uint8 -> comp (same
  * shape) int32: -1 outside the masks, else the component number in raster
  * order of first pixels, numbered across the batch (image 0 first);
@@ -287,7 +287,7 @@ int qfca_components(const uint8_t* mask, int32_t images, int32_t h, int32_t w, v
                     int64_t workspace_bytes, int32_t* labels, int32_t* comp, int32_t* n_comp,
                     void* stream);
 
-/* PRO histograms (metrics.py:95-122): thr_asc (m <= 2048 ascending distinct
+/* PRO histograms (metrics.py:91-120): thr_asc (m <= 2048 ascending distinct
  * thresholds); each pixel goes to slot #{thr <= score}.  comp_hist
  * ((comp_hi - comp_lo), m + 1) int32 counts the pixels of components
  * [comp_lo, comp_hi) (zeroed by the caller), normal_hist (m + 1) uint64 the
@@ -296,10 +296,10 @@ int qfca_pro_histograms(const double* scores, const int32_t* comp, int64_t n,
                         const double* thr_asc, int32_t m, int32_t comp_lo, int32_t comp_hi,
                         int32_t* comp_hist, uint64_t* normal_hist, void* stream);
 /* pro[j] += (pixels >= thr_asc[j]) / size over the ncomp histograms in order
- * (metrics.py:116-118); comp_hist is turned into suffix sums in place. */
+ * (metrics.py:112-115); comp_hist is turned into suffix sums in place. */
 int qfca_pro_accumulate(int32_t* comp_hist, int32_t ncomp, int32_t m, double* pro, void* stream);
 
-/* ---- one-call detect (scoring.py:263-327) for the fused configuration ---- */
+/* ---- one-call detect (scoring.py:235-299) for the fused configuration ---- */
 typedef struct qfca_config {
     int32_t n_bins;        /* PipelineConfig.n_bins (16) */
     int32_t patch_size;    /* PipelineConfig.patch_size (9) */

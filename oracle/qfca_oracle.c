@@ -13,8 +13,8 @@
  * (tests/golden/make_golden.py).  Citations are file:line in the reference.
  *
  * OpenMP is used only across channels (each channel is independent,
- * scoring.py:292-309); the channel sum is then done in fixed channel order in
- * fp64, exactly like the reference's `acc += chan_scores` (scoring.py:301).
+ * scoring.py:264-281); the channel sum is then done in fixed channel order in
+ * fp64, exactly like the reference's `acc += chan_scores` (scoring.py:273).
  */
 #include <math.h>
 #include <stdint.h>
@@ -108,7 +108,7 @@ static int np_pad_index(int c, int n, int pad, int edge_mode) {
     return c;
 }
 
-/* scoring.py:186-202 (_map_coord) */
+/* scoring.py:158-174 (_map_coord) */
 static int map_coord(int c, int n, int pad_code) {
     if (c >= 0 && c < n) return c;
     if (pad_code == PAD_ZERO) return -1;
@@ -185,7 +185,7 @@ void oracle_select_reference_median(const float* v, int64_t C, int h, int w,
     }
 }
 
-/* transport.py:273-307 (_mismatch_row): Alg. 1 with the reference rescaled to
+/* transport.py:73-107 (_mismatch_row): Alg. 1 with the reference rescaled to
  * the patch mass and an eps tie guard. */
 void oracle_mismatch_row(const double* P, const double* R, const double* Q,
                          int n, double eps, double* out) {
@@ -216,7 +216,7 @@ void oracle_mismatch_row(const double* P, const double* R, const double* Q,
     for (int b = 0; b < n; ++b) out[b] = P[b] > 0.0 ? out[b] / P[b] : 0.0;
 }
 
-/* transport.py:310-325 (mismatch_batch) */
+/* transport.py:110-125 (mismatch_batch) */
 void oracle_mismatch_batch(const double* Pb, int64_t M, int n, const double* R,
                            const double* Q, double* out) {
 #pragma omp parallel for schedule(static)
@@ -228,7 +228,7 @@ void oracle_mismatch_batch(const double* Pb, int64_t M, int n, const double* R,
     }
 }
 
-/* scoring.py:205-260 (_channel_score_kernel): per-bin indicator SATs ->
+/* scoring.py:177-232 (_channel_score_kernel): per-bin indicator SATs ->
  * counts, per-pixel Alg. 1, per-bin error SATs -> own-bin gather, x 1/T^2.
  * All fp64, identical loop order. */
 void oracle_channel_score(const int32_t* idx, int h, int w, int nbins, int t,
@@ -293,7 +293,7 @@ void oracle_channel_score(const int32_t* idx, int h, int w, int nbins, int t,
 }
 
 /* Window counts of one bin-index plane: (N, h, w) float64, via the same SAT
- * construction as the scoring kernel (scoring.py:219-239); equals
+ * construction as the scoring kernel (scoring.py:191-211); equals
  * quantize.py:85-89 (box_average_stack of the one-hot planes x T^2). */
 void oracle_channel_histograms(const int32_t* idx, int h, int w, int nbins,
                                int t, int pad_code, double* counts_nhw) {
@@ -338,7 +338,7 @@ void oracle_channel_histograms(const int32_t* idx, int h, int w, int nbins,
     free(xmap);
 }
 
-/* The per-channel loop of detect (scoring.py:286-309) for the uniform-sigma_p
+/* The per-channel loop of detect (scoring.py:258-281) for the uniform-sigma_p
  * path: channel scores for every non-degenerate channel, summed in channel
  * order in fp64.  Channels run in parallel into private buffers; the sum is
  * sequential so the result is independent of the thread count.

@@ -24,7 +24,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
-PAD_CODES = {"zero": 0, "reflect": 1, "wrap": 2}  # scoring.py:183
+PAD_CODES = {"zero": 0, "reflect": 1, "wrap": 2}  # scoring.py:155
 REFERENCE_MODES = ("median-quan", "mean-quan", "quan-median", "quan-mean")
 _lib = None
 
@@ -224,7 +224,7 @@ def patch_histograms(bins, n_bins, t, pad="reflect") -> np.ndarray:
 
 # ---------------------------------------------------------------- transport
 def mismatch_batch(pb, r, q) -> np.ndarray:
-    """transport.py:310-325."""
+    """transport.py:110-125."""
     pb = np.ascontiguousarray(pb, np.float64)
     out = np.empty_like(pb)
     lib().oracle_mismatch_batch(_p(pb), pb.shape[0], pb.shape[1],
@@ -272,14 +272,14 @@ def gaussian_blur(plane, sigma, pad="reflect"):
 
 
 def smooth_scores(m, sigma_s, pad="reflect"):
-    """scoring.py:161-166."""
+    """scoring.py:133-138."""
     if sigma_s == 0:
         return np.asarray(m, dtype=np.float64)
     return gaussian_blur(m, sigma_s, pad)
 
 
 def image_score_of(scores, border):
-    """scoring.py:169-174."""
+    """scoring.py:141-146."""
     h, w = scores.shape
     b = min(border, (h - 1) // 2, (w - 1) // 2)
     interior = scores[b:h - b, b:w - b] if b > 0 else scores
@@ -306,7 +306,7 @@ def resize_plane(plane, out_h, out_w):
 
 
 def upsample_scores(scores, out_h, out_w):
-    """scoring.py:177-180."""
+    """scoring.py:149-152."""
     return resize_plane(np.asarray(scores, np.float64), out_h, out_w).astype(np.float64)
 
 
@@ -341,7 +341,7 @@ def pca_residual(values, mean, comps):
 
 # ---------------------------------------------------------------- detect
 def _smooth_error_planes(planes, t, sigma_p, pad):
-    """scoring.py:116-126."""
+    """scoring.py:88-98."""
     if math.isinf(sigma_p):
         r = t // 2
         if pad == "zero":
@@ -377,7 +377,7 @@ def _smooth_error_planes(planes, t, sigma_p, pad):
 def detect(values, n_bins=16, patch_size=9, sigma_p=math.inf, sigma_s=1.0,
            pca_components=0, reference_mode="median-quan", sample_budget=4096,
            border_exclusion=None, pad="reflect", return_stages=False):
-    """scoring.py:263-327 (detect) -> (scores f64 (h,w), image_score, degenerate).
+    """scoring.py:235-299 (detect) -> (scores f64 (h,w), image_score, degenerate).
 
     The uniform-sigma_p path runs the C restatement of _channel_score_kernel
     (parallel over channels, fixed-order fp64 sum).
@@ -434,7 +434,7 @@ def detect(values, n_bins=16, patch_size=9, sigma_p=math.inf, sigma_s=1.0,
 # ---------------------------------------------------------------------------
 
 def metrics_pooled(samples):
-    """metrics.py:36-41, 61-68 -- interiors pooled in sample order.
+    """metrics.py:37-41, 61-68 -- interiors pooled in sample order.
     samples: list of (scores, mask, image_label, border)."""
     sc, lb = [], []
     for s, m, _, b in samples:
@@ -478,7 +478,7 @@ def connected_components(mask):
 
 
 def pro_curve(samples, thresholds):
-    """metrics.py:95-122 -- per-threshold mean component overlap and FPR,
+    """metrics.py:91-120 -- per-threshold mean component overlap and FPR,
     counting "score >= t" directly for every component."""
     comps, normal = [], []
     for s, m, _, b in samples:
@@ -502,7 +502,7 @@ def pro_curve(samples, thresholds):
 
 
 def pro_at_fpr(samples, limit=0.3, thresholds=None):
-    """metrics.py:87-92, 125-154 -- quantile thresholds, trapezoid to the limit."""
+    """metrics.py:83-88, 125-154 -- quantile thresholds, trapezoid to the limit."""
     if thresholds is None:
         scores, _ = metrics_pooled(samples)
         thresholds = np.unique(np.quantile(scores, np.linspace(0.0, 1.0, 500)))[::-1]

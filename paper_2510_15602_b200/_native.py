@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqfca_b200.so")
 
 QFCA_OK, QFCA_ERR_ARG, QFCA_ERR_CUDA, QFCA_ERR_UNSUPPORTED = 0, 1, 2, 3
-PAD_CODES = {"zero": 0, "reflect": 1, "wrap": 2}  # scoring.py:183
+PAD_CODES = {"zero": 0, "reflect": 1, "wrap": 2}  # scoring.py:155
 REF_MODE_CODES = {"median-quan": 0, "quan-median": 2, "quan-mean": 3}
 
 _P, _I32, _I64, _F64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double

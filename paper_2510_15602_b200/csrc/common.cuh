@@ -54,7 +54,7 @@ inline int balanced_groups(int64_t images, int C, int cpb, int per_sm) {
 }
 
 // Padded-plane coordinate -> source index, -1 for zero padding.
-// Restates scoring.py:186-202 (_map_coord): reflect without edge repeat,
+// Restates scoring.py:158-174 (_map_coord): reflect without edge repeat,
 // repeated for large margins; n == 1 -> 0; wrap is toroidal.
 __host__ __device__ __forceinline__ int map_coord(int c, int n, int pad) {
     if (c >= 0 && c < n) return c;

@@ -1,10 +1,10 @@
 // finalize.cu -- K5: channel mean, final Gaussian smoothing, border-excluded
 // image score and bilinear upsampling.
 //
-// Restates scoring.py:311-319 (agg = acc / used, all-degenerate -> zeros),
-// scoring.py:161-166 + features.py:49-77 (normalised Gaussian of radius
-// ceil(3 sigma), rows (axis 0) then columns, np.pad modes), scoring.py:169-174
-// (image_score_of) and scoring.py:177-180 + tensor_io.py:127-151 (bilinear,
+// Restates scoring.py:283-291 (agg = acc / used, all-degenerate -> zeros),
+// scoring.py:133-138 + features.py:49-77 (normalised Gaussian of radius
+// ceil(3 sigma), rows (axis 0) then columns, np.pad modes), scoring.py:141-146
+// (image_score_of) and scoring.py:149-152 + tensor_io.py:127-151 (bilinear,
 // half-pixel centres, computed in fp64, rounded to float32).
 #include "common.cuh"
 

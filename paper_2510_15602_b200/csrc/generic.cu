@@ -2,10 +2,10 @@
 // finite sigma_p), materialising per-bin planes.
 //
 // It restates, plane by plane, the reference's non-fused route
-// (scoring.py:87-140 and 302-308): window counts (quantize.py:85-89), the
+// (scoring.py:59-112 and 274-280): window counts (quantize.py:85-89), the
 // two-pointer Alg. 1 with the reference rescaled to each window's mass
-// (transport.py:273-325) in fp64, and the box / Gaussian smoothing of the
-// error planes followed by the own-bin gather (scoring.py:116-140).  It backs
+// (transport.py:73-125) in fp64, and the box / Gaussian smoothing of the
+// error planes followed by the own-bin gather (scoring.py:88-112).  It backs
 // the public step APIs (patch_histograms, bin_error_maps, associate_errors)
 // and the detect() configurations the fused kernel (score.cu) does not cover
 // (zero padding, non-integer references, finite sigma_p).
@@ -58,8 +58,8 @@ __global__ void k_counts_horizontal(const uint16_t* __restrict__ col, int64_t pl
     out[gid] = (OT)c;
 }
 
-// Alg. 1 per pixel (transport.py:273-307) with R rescaled to the window mass,
-// eps = 1e-9 * mass (transport.py:11, scoring.py:244-245).  E in fp64.
+// Alg. 1 per pixel (transport.py:73-107) with R rescaled to the window mass,
+// eps = 1e-9 * mass (transport.py:11, scoring.py:216-217).  E in fp64.
 __global__ void k_mismatch_pixels(const uint16_t* __restrict__ counts, int64_t planes,
                                   int64_t hw, int n_bins, const double* __restrict__ refw,
                                   const double* __restrict__ centers,
@@ -105,7 +105,7 @@ __global__ void k_mismatch_pixels(const uint16_t* __restrict__ counts, int64_t p
     }
 }
 
-// mismatch_batch (transport.py:310-325) on row-major fp64 rows: Pb (M, N),
+// mismatch_batch (transport.py:110-125) on row-major fp64 rows: Pb (M, N),
 // R / Q (N,), out (M, N).  One thread per row, identical arithmetic.
 __global__ void k_mismatch_rows(const double* __restrict__ Pb, int64_t M, int n,
                                 const double* __restrict__ R, const double* __restrict__ Q,
@@ -118,7 +118,7 @@ __global__ void k_mismatch_rows(const double* __restrict__ Pb, int64_t M, int n,
     for (int b = 0; b < n; ++b) mr += R[b];
     for (int b = 0; b < n; ++b) mp += P[b];
     const double eps = 1e-9 * (mp > 1e-300 ? mp : 1e-300);
-    // _mismatch_row recomputes both masses (transport.py:276-281)
+    // _mismatch_row recomputes both masses (transport.py:76-81)
     mp = 0.0;
     mr = 0.0;
     for (int b = 0; b < n; ++b) {
@@ -188,7 +188,7 @@ __global__ void k_smooth_gather(const double* __restrict__ tmp, const BT* __rest
     score[gid] = s * post;
 }
 
-// fixed-order channel sum (scoring.py:292-309): acc[b][px] = sum_c score[b][c][px]
+// fixed-order channel sum (scoring.py:264-281): acc[b][px] = sum_c score[b][c][px]
 // over non-skipped channels; used[b] = number of those channels.
 __global__ void k_channel_sum(const double* __restrict__ score, int64_t images, int channels,
                               int64_t hw, const uint8_t* __restrict__ skip, int accumulate,

@@ -13,13 +13,13 @@
 // F1 candidates sit at run starts of the ascending order: all elements of
 // score >= s are predicted positive, tp = pos - (positives before the run).
 //
-// Connected components (metrics.py:80-84, scipy.ndimage.label with the 3x3
+// Connected components (metrics.py:76-80, scipy.ndimage.label with the 3x3
 // structure): union-find over the interior masks, 8-connectivity, the root of
 // every tree is the smallest raster index of its component (union links the
 // larger root under the smaller with atomicMin), so numbering the roots in
 // index order reproduces ndimage's labels (first-pixel raster order).
 //
-// PRO (metrics.py:95-122): every pixel falls into threshold slot
+// PRO (metrics.py:91-120): every pixel falls into threshold slot
 // c = #{thresholds <= score}; per-component and normal-pixel histograms over
 // the slots, then per-component suffix sums give "pixels >= threshold", and
 // the per-threshold sum over components runs in component order in fp64 --
@@ -385,7 +385,7 @@ __global__ void k_pro_suffix(int* comp_hist, int ncomp, int m) {
     }
 }
 
-// pro[j] += S_q[j + 1] / S_q[0] over components q in order (metrics.py:116-118)
+// pro[j] += S_q[j + 1] / S_q[0] over components q in order (metrics.py:112-115)
 __global__ void k_pro_accumulate(const int* __restrict__ comp_hist, int ncomp, int m, double* pro) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;

@@ -1,9 +1,9 @@
 // score.cu -- K4: fused per-(image, channel-group) scoring kernel.
 //
-// Replaces the reference hot loop: _channel_score_kernel (scoring.py:205-260,
+// Replaces the reference hot loop: _channel_score_kernel (scoring.py:177-232,
 // per-bin indicator SATs -> window counts -> per-pixel Alg. 1 -> per-bin error
 // SATs -> own-bin gather) and the channel accumulation in detect
-// (scoring.py:286-309), for the default family of configurations: uniform
+// (scoring.py:258-281), for the default family of configurations: uniform
 // sigma_p, median-quan reference, reflect or wrap padding.
 //
 // Everything below is exact integer work except the error values:
@@ -12,7 +12,7 @@
 //     prefix difference along the padded row (exact, lanes never exceed T^2);
 //   * the reference enters as V_i (cumulative reference counts, reference.cu)
 //     and the prefix table PJ[x] = sum_{k<x} J_k; Alg. 1 on integer masses of
-//     equal total (scale = 1, transport.py:284) has the closed form
+//     equal total (scale = 1, transport.py:84) has the closed form
 //         E_i = w * (G_i(A_i) - G_i(A_{i-1})) / P_i,
 //         G_i(x) = x < V_{i-1} ? -(PJ[x] - i x) : (PJ[x] - i x) + D_i,
 //         D_i = 2 (i V_{i-1} - PJ[V_{i-1}])
@@ -98,7 +98,7 @@ k_score(const BT* __restrict__ bins, const float* __restrict__ lo, const float* 
     for (int c = c_begin; c < c_end; ++c) {
         const int64_t plane = (int64_t)img * g.C + c;
         const double lo_c = lo[plane], hi_c = hi[plane];
-        if (!(hi_c > lo_c)) continue;  // degenerate: skipped (scoring.py:293-294)
+        if (!(hi_c > lo_c)) continue;  // degenerate: skipped (scoring.py:265-266)
         const float scale = (float)(((hi_c - lo_c) / (double)g.n_bins) / (double)g.t2);
         const BT* bp = bins + plane * hw;
 

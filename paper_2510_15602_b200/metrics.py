@@ -96,7 +96,7 @@ def _device_tables(group, dev):
 
 
 class _Pool:
-    """Device copy of the pooled interiors (metrics.py:61-68 _pooled order).
+    """Device copy of the pooled interiors (metrics.py:62-68 _pooled order).
 
     Consecutive samples of the same (H, W, border) form one group, gathered by
     one ``qfca_pool_interior`` call into a contiguous (images, h, w) slice.
@@ -293,14 +293,14 @@ def _quantiles(sorted_dev: torch.Tensor, dtype, qs: np.ndarray) -> np.ndarray:
 
 
 def _pro_thresholds(p: _Pool) -> np.ndarray:
-    """metrics.py:87-92 -- distinct quantile scores, descending."""
+    """metrics.py:83-88 -- distinct quantile scores, descending."""
     qs = np.linspace(0.0, 1.0, PRO_MAX_THRESHOLDS)
     thr = np.unique(_quantiles(p.rank()[3], p.dtype, qs))
     return thr[::-1]
 
 
 def _pro_curve(p: _Pool, thresholds: np.ndarray):
-    """metrics.py:95-122 -- (fpr, pro) at the given thresholds (score >= t)."""
+    """metrics.py:91-120 -- (fpr, pro) at the given thresholds (score >= t)."""
     thresholds = np.asarray(thresholds, dtype=np.float64)
     uniq, inv = np.unique(thresholds, return_inverse=True)
     m = uniq.size

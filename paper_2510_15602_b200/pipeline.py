@@ -1,7 +1,7 @@
 """Streaming host -> device -> host driver around ``detect_batch``.
 
 A serving loop feeds batches of features that live in host memory.  The
-reference scores one image at a time on the CPU (scoring.py:263-327); on the
+reference scores one image at a time on the CPU (scoring.py:235-299); on the
 B200 the PCIe copy of a batch (C x H x W float32 per image) takes as long as
 scoring it, so the driver overlaps them: batch i+1 is copied on a dedicated
 copy stream into the second of two device buffers while batch i is scored on
@@ -38,7 +38,7 @@ class DetectPipeline:
     (pinned for asynchronous copies; unpinned ones are staged through a
     pinned buffer) of one fixed shape and yields a ``HostResult`` per batch,
     in order.  ``upsample_to = (H, W)`` also returns the image-resolution maps
-    (upsample_scores, scoring.py:177-180).
+    (upsample_scores, scoring.py:149-152).
     """
 
     def __init__(self, cfg: PipelineConfig | None = None, upsample_to=None, device=None):

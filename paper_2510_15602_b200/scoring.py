@@ -1,6 +1,6 @@
 """End-to-end anomaly map on the GPU (drop-in for qfca.scoring).
 
-Mirrors reference scoring.py:25-327: PipelineConfig / AnomalyMap dataclasses,
+Mirrors reference scoring.py:25-299: PipelineConfig / AnomalyMap dataclasses,
 the step APIs (bin_error_maps, channel_error_maps, associate_errors,
 aggregate_channels, smooth_scores, image_score_of, upsample_scores) and
 detect(), plus the batched device entry point detect_batch().
@@ -40,7 +40,7 @@ __all__ = ["PipelineConfig", "AnomalyMap", "DetectResult", "detect", "detect_bat
 
 @dataclass(frozen=True)
 class PipelineConfig:
-    """scoring.py:53-77 -- same fields, defaults and validation."""
+    """scoring.py:25-49 -- same fields, defaults and validation."""
 
     n_bins: int = 16
     patch_size: int = 9
@@ -272,7 +272,7 @@ def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
     """Feature planes wider than the fused kernels' 128 columns (an 8192^2
     texture: 1024^2 per channel): each image through the tiled fused path of
     sharding.py (one rank holding every channel), then the channel mean,
-    Gaussian and image score as in _fused_detect (scoring.py:286-327)."""
+    Gaussian and image score as in _fused_detect (scoring.py:258-299)."""
     from .sharding import _channel_partial
     b, c, h, w = x.shape
     out = DetectResult(scores=empty((b, h, w), torch.float64),
@@ -294,7 +294,7 @@ def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
 
 def detect(f: FeatureMap, cfg: PipelineConfig | None = None,
            timings: dict | None = None) -> AnomalyMap:
-    """scoring.py:263-327: full anomaly-map pipeline on one feature map."""
+    """scoring.py:235-299: full anomaly-map pipeline on one feature map."""
     cfg = cfg or PipelineConfig()
     _check_cfg(cfg)
     like = is_torch(f.values)
@@ -325,7 +325,7 @@ def detect(f: FeatureMap, cfg: PipelineConfig | None = None,
 
 
 def channel_error_maps(counts, ref_w, centers):
-    """scoring.py:103-113: (N, H, W) errors of one channel's histogram field."""
+    """scoring.py:75-85: (N, H, W) errors of one channel's histogram field."""
     like = is_torch(counts)
     cnt = to_dev(counts, torch.float32)
     n, h, w = cnt.shape
@@ -336,7 +336,7 @@ def channel_error_maps(counts, ref_w, centers):
 
 
 def bin_error_maps(hf: HistogramField, ref: ReferenceHistogram, q: Quantizer):
-    """scoring.py:87-100: (C, N, H, W) per-bin mismatch scores."""
+    """scoring.py:59-72: (C, N, H, W) per-bin mismatch scores."""
     like = is_torch(hf.counts)
     counts = to_dev(hf.counts, torch.float32)
     c, n, h, w = counts.shape
@@ -355,7 +355,7 @@ def bin_error_maps(hf: HistogramField, ref: ReferenceHistogram, q: Quantizer):
 
 
 def associate_errors(err, bins: BinIndexMap, cfg: PipelineConfig):
-    """scoring.py:129-140: smooth each channel's error planes, own-bin gather."""
+    """scoring.py:101-112: smooth each channel's error planes, own-bin gather."""
     like = is_torch(err)
     e = to_dev(err, torch.float64)
     c, n, h, w = e.shape
@@ -370,7 +370,7 @@ def associate_errors(err, bins: BinIndexMap, cfg: PipelineConfig):
 
 
 def aggregate_channels(scores, skip=None):
-    """scoring.py:143-158: mean over non-skipped channels (fixed order)."""
+    """scoring.py:115-130: mean over non-skipped channels (fixed order)."""
     like = is_torch(scores)
     s = to_dev(scores, torch.float64)
     if s.shape[0] < 1:
@@ -395,7 +395,7 @@ def aggregate_channels(scores, skip=None):
 
 
 def smooth_scores(score_map, sigma_s: float, pad: str = "reflect"):
-    """scoring.py:161-166."""
+    """scoring.py:133-138."""
     if sigma_s == 0:
         return score_map.to(torch.float64) if is_torch(score_map) else np.asarray(
             score_map, dtype=np.float64)
@@ -403,7 +403,7 @@ def smooth_scores(score_map, sigma_s: float, pad: str = "reflect"):
 
 
 def image_score_of(scores, border: int) -> float:
-    """scoring.py:169-174: max over pixels at least ``border`` from the edge."""
+    """scoring.py:141-146: max over pixels at least ``border`` from the edge."""
     s = to_dev(scores, torch.float64)
     h, w = s.shape
     out = empty((1,), torch.float64)
@@ -412,7 +412,7 @@ def image_score_of(scores, border: int) -> float:
 
 
 def upsample_scores(scores, out_h: int, out_w: int):
-    """scoring.py:177-180: bilinear (half-pixel) resize, float32-rounded, fp64 out."""
+    """scoring.py:149-152: bilinear (half-pixel) resize, float32-rounded, fp64 out."""
     like = is_torch(scores)
     s = to_dev(scores, torch.float64)
     h, w = s.shape

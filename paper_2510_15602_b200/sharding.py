@@ -4,7 +4,7 @@
   process per GPU, no collective (bench.py under torchrun, ``shard_batch``).
 * One very large image (8192^2 -> 512 x 1024^2 features): every stage up to
   the channel sum is per channel (quantize.py:66-68, 168-199; scoring.py:
-  292-309), so each rank scores a contiguous channel slice and ONE all-reduce
+  264-281), so each rank scores a contiguous channel slice and ONE all-reduce
   (sum) of the (h*w + 1) fp64 partial -- channel-sum map plus the count of
   used channels -- combines them; every rank then finalises (channel mean,
   Gaussian, image score) identically.  NCCL over NVLink in production, gloo
@@ -98,7 +98,7 @@ def combine_partials(acc: torch.Tensor, used: int | torch.Tensor, group=None):
 
 def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
     """Channel-sum map (h, w) fp64 and used-channel count for this rank's
-    channel slice (C_local, h, w), fused path (scoring.py:286-309 without the
+    channel slice (C_local, h, w), fused path (scoring.py:258-281 without the
     division)."""
     acc, used, _ = _channel_partial(values, cfg)
     return acc, int(used[0])

@@ -31,7 +31,7 @@ __all__ = ["MAGIC", "TensorFormatError", "BadMagicError", "TruncatedError",
 
 
 class TensorFormatError(Exception):
-    """Base class for QTF1 format violations (tensor_io.py:30)."""
+    """Base class for QTF1 format violations (tensor_io.py:27-28)."""
 
 
 class BadMagicError(TensorFormatError):
@@ -133,7 +133,7 @@ class DatasetIndexError(Exception):
 
 
 def _nearest_index(n_in: int, n_out: int) -> np.ndarray:
-    """tensor_io.py:133-138 -- half-pixel centres, rounded, clamped."""
+    """tensor_io.py:133-147 -- half-pixel centres, rounded, clamped."""
     c = (np.arange(n_out) + 0.5) * n_in / n_out - 0.5
     return np.clip(np.round(c), 0, n_in - 1).astype(int)
 
@@ -171,7 +171,7 @@ class DatasetSample:
 
 
 def load_dataset(root, class_name: str, layout: str = "mvtec") -> list:
-    """tensor_io.py:207-240 -- index root/class/test/<defect>/*.png|ppm with
+    """tensor_io.py:207-239 -- index root/class/test/<defect>/*.png|ppm with
     masks at root/class/ground_truth/<defect>/<stem>_mask.png ("good" has
     none), lexicographic by defect then file name."""
     if layout != "mvtec":

@@ -49,7 +49,7 @@ def _validate(P, R, Q):
 
 def mismatch_batch_dev(pb: torch.Tensor, r: torch.Tensor, q: torch.Tensor,
                        out: torch.Tensor | None = None) -> torch.Tensor:
-    """(M, N) fp64 device rows -> (M, N) per-bin errors (transport.py:310-325)."""
+    """(M, N) fp64 device rows -> (M, N) per-bin errors (transport.py:110-125)."""
     m, n = pb.shape
     if out is None:
         out = empty((m, n), torch.float64)
@@ -59,7 +59,7 @@ def mismatch_batch_dev(pb: torch.Tensor, r: torch.Tensor, q: torch.Tensor,
 
 
 def mismatch_batch(Pb, R, Q, out) -> None:
-    """transport.py:310-325: fills ``out`` (M, N) in place."""
+    """transport.py:110-125: fills ``out`` (M, N) in place."""
     like = is_torch(Pb)
     pb = to_dev(Pb, torch.float64)
     res = mismatch_batch_dev(pb, to_dev(R, torch.float64), to_dev(Q, torch.float64))

@@ -205,7 +205,7 @@ def test_transport_api(Q):
 
 def test_step_apis_vs_reference_route(Q):
     """bin_error_maps -> associate_errors -> aggregate -> smooth reproduces
-    detect (the reference's unfused route, scoring.py:87-166)."""
+    detect (the reference's unfused route, scoring.py:59-138)."""
     d = load_golden("small_rand_n16_t9_reflect")
     v = d["values"]
     cfg = Q.PipelineConfig(n_bins=16, patch_size=9)
