@@ -24,7 +24,13 @@ __all__ = ["HostResult", "DetectPipeline"]
 
 @dataclass
 class HostResult:
-    """One batch's results in pinned host memory (valid once yielded)."""
+    """One batch's results in pinned host memory.
+
+    Lifetime: the tensors are views of the pipeline's two reusable pinned
+    buffers.  They hold this batch's results until the caller asks the
+    generator for the next result; after that the buffers are refilled by a
+    later batch.  Clone them (or run with ``copy=True``) to keep them.
+    """
     index: int
     scores: torch.Tensor          # (B, h, w) float64
     image_scores: torch.Tensor    # (B,) float64
@@ -36,8 +42,9 @@ class DetectPipeline:
 
     ``run(batches)`` takes an iterable of (B, C, h, w) float32 CPU tensors
     (pinned for asynchronous copies; unpinned ones are staged through a
-    pinned buffer) of one fixed shape and yields a ``HostResult`` per batch,
-    in order.  ``upsample_to = (H, W)`` also returns the image-resolution maps
+    pinned buffer) with one (C, h, w) and B no larger than the first batch's,
+    and yields a ``HostResult`` per batch, in order (see HostResult for how
+    long its tensors stay valid; ``copy=True`` yields owned copies).  ``upsample_to = (H, W)`` also returns the image-resolution maps
     (upsample_scores, scoring.py:149-152).
     """
 
@@ -69,20 +76,27 @@ class DetectPipeline:
         self.done = [torch.cuda.Event() for _ in range(2)]      # results on the host
 
     def _copy_in(self, host: torch.Tensor, slot: int):
+        n = host.shape[0]
         src = host
         if not host.is_pinned():
             if self.stage[slot] is None:
                 self.stage[slot] = torch.empty(self._shape, dtype=torch.float32).pin_memory()
             self.copied[slot].synchronize()  # the staging buffer's last copy has been read
-            self.stage[slot].copy_(host)
-            src = self.stage[slot]
+            self.stage[slot][:n].copy_(host)
+            src = self.stage[slot][:n]
         with torch.cuda.stream(self.copy_stream):
             # the buffer is free once the compute that last read it has run
             self.copy_stream.wait_event(self.freed[slot])
-            self.dev_in[slot].copy_(src, non_blocking=True)
+            self.dev_in[slot][:n].copy_(src, non_blocking=True)
             self.copied[slot].record(self.copy_stream)
 
-    def run(self, batches: Iterable[torch.Tensor]) -> Iterator[HostResult]:
+    def _check(self, batch: torch.Tensor):
+        if (batch.dim() != 4 or tuple(batch.shape[1:]) != self._shape[1:]
+                or batch.shape[0] > self._shape[0] or batch.shape[0] < 1):
+            raise ValueError("every batch needs the first batch's (C, h, w) and at most "
+                             "its number of images")
+
+    def run(self, batches: Iterable[torch.Tensor], copy: bool = False) -> Iterator[HostResult]:
         it = iter(batches)
         try:
             first = next(it)
@@ -94,21 +108,23 @@ class DetectPipeline:
         for ev in self.freed:
             ev.record(compute)
         self._copy_in(first, 0)
-        pending = None  # (index, slot) whose results are in flight
+        pending = None  # (index, slot, images) whose results are in flight
         i, cur = 0, first
         while cur is not None:
             slot = i & 1
+            n = cur.shape[0]
             nxt = next(it, None)
             if nxt is not None:
-                if tuple(nxt.shape) != self._shape:
-                    raise ValueError("all batches of a run must have one shape")
+                self._check(nxt)
                 self._copy_in(nxt, slot ^ 1)
             compute.wait_event(self.copied[slot])
-            res = detect_batch(self.dev_in[slot], self.cfg)
+            res = detect_batch(self.dev_in[slot][:n], self.cfg)
             self.freed[slot].record(compute)
-            outs = [(res.scores, self.h_scores[slot]), (res.image_scores, self.h_img[slot])]
+            outs = [(res.scores, self.h_scores[slot][:n]),
+                    (res.image_scores, self.h_img[slot][:n])]
             if self.h_up is not None:
-                outs.append((upsample_batch(res.scores, *self.upsample_to), self.h_up[slot]))
+                outs.append((upsample_batch(res.scores, *self.upsample_to),
+                             self.h_up[slot][:n]))
             # results travel back on their own stream: the next batch's scoring
             # does not queue behind this batch's device -> host copies
             self.d2h_stream.wait_stream(compute)
@@ -118,14 +134,19 @@ class DetectPipeline:
                     host_t.copy_(dev_t, non_blocking=True)
                 self.done[slot].record(self.d2h_stream)
             if pending is not None:
-                yield self._result(*pending)
-            pending = (i, slot)
+                yield self._result(*pending, copy)
+            pending = (i, slot, n)
             i, cur = i + 1, nxt
         if pending is not None:
-            yield self._result(*pending)
+            yield self._result(*pending, copy)
 
-    def _result(self, index: int, slot: int) -> HostResult:
+    def _result(self, index: int, slot: int, n: int, copy: bool) -> HostResult:
         self.done[slot].synchronize()
-        return HostResult(index=index, scores=self.h_scores[slot],
-                          image_scores=self.h_img[slot],
-                          upsampled=None if self.h_up is None else self.h_up[slot])
+        up = None if self.h_up is None else self.h_up[slot][:n]
+        r = HostResult(index=index, scores=self.h_scores[slot][:n],
+                       image_scores=self.h_img[slot][:n], upsampled=up)
+        if copy:
+            r = HostResult(index=index, scores=r.scores.clone(),
+                           image_scores=r.image_scores.clone(),
+                           upsampled=None if up is None else up.clone())
+        return r

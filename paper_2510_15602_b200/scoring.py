@@ -138,6 +138,9 @@ def _fused_detect(x: torch.Tensor, cfg: PipelineConfig, groups: int = 0,
                            used=empty((b,), torch.int32), nonfinite=zeros((1,), torch.int32))
     ev = None
     if events is not None:
+        for e in events:  # torch creates the cudaEvent handle lazily, on first record
+            if not e.cuda_event:
+                e.record()
         ev = (ctypes.c_void_p * 2)(events[0].cuda_event, events[1].cuda_event)
     N.check(L.qfca_detect_ex(x.data_ptr(), b, c, h, w, ctypes.byref(qc), ws.data_ptr(), nbytes,
                              out.scores.data_ptr(), out.image_scores.data_ptr(),
@@ -166,16 +169,11 @@ def _smooth_taps(cfg: PipelineConfig):
     return k, 1.0
 
 
-def _general_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
+def _reference_weights_dev(x, bins, lo, hi, degen, cfg: PipelineConfig) -> torch.Tensor:
+    """select_reference (quantize.py:150-200) weights (planes, N) fp64 on the device."""
     b, c, h, w = x.shape
-    hw = h * w
     planes = b * c
     n, t = cfg.n_bins, cfg.patch_size
-    s = N.stream()
-    lo, hi, flag = minmax_dev(x, planes, hw)
-    degen = ~(hi > lo)
-    bins = bins_dev(x, lo, hi, planes, hw, n)
-    # reference weights (planes, N) fp64
     if cfg.reference_mode == "median-quan":
         v = reference_stats_dev(bins, lo, hi, planes, h, w, n, t, cfg.pad, cfg.sample_budget,
                                 cfg.reference_mode).to(torch.float64)
@@ -202,7 +200,25 @@ def _general_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
         ns = ((h + st - 1) // st) * ((w + st - 1) // st)
         refw = torch.from_numpy(_weights_from_stats(stats, degen.cpu().numpy(),
                                                     cfg.reference_mode, t * t, ns)).to(x.device)
+    return refw
+
+
+def _general_partial(x: torch.Tensor, cfg: PipelineConfig, events=None):
+    """The reference's unfused route up to the channel sum (scoring.py:251-281,
+    the non-uniform branch 274-280 and bin_error_maps / associate_errors):
+    returns (acc (B, h*w) fp64 channel sums, used (B,) int32, non-finite flag)."""
+    b, c, h, w = x.shape
+    hw = h * w
+    planes = b * c
+    n, t = cfg.n_bins, cfg.patch_size
+    s = N.stream()
+    lo, hi, flag = minmax_dev(x, planes, hw)
+    degen = ~(hi > lo)
+    bins = bins_dev(x, lo, hi, planes, hw, n)
+    refw = _reference_weights_dev(x, bins, lo, hi, degen, cfg)
     centers = _centers_dev(lo, hi, n)
+    if events is not None:
+        events[0].record()
     taps, post = _smooth_taps(cfg)
     skip = degen.to(torch.uint8)
     acc = zeros((b, hw), torch.float64)
@@ -229,19 +245,37 @@ def _general_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
             del err, tmp
             N.call("qfca_channel_sum", score.data_ptr(), 1, np_, hw, skip[p0:p1].data_ptr(),
                    1, acc[i].data_ptr(), used[i:i + 1].data_ptr(), s)
-    agg = empty((b, hw), torch.float64)
-    N.call("qfca_divide_used", acc.data_ptr(), b, hw, used.data_ptr(), agg.data_ptr(), s)
+    if events is not None:
+        events[1].record()
+    return acc, used, flag
+
+
+def _finalize_dev(acc: torch.Tensor, used: torch.Tensor, cfg: PipelineConfig, h: int, w: int):
+    """scoring.py:284-291: acc / used (zeros when all degenerate), smooth_scores,
+    image_score_of, on (B, h*w) device sums -> (scores (B, h, w), image scores (B,))."""
+    b = acc.shape[0]
+    s = N.stream()
+    agg = empty((b, h * w), torch.float64)
+    N.call("qfca_divide_used", acc.data_ptr(), b, h * w, used.data_ptr(), agg.data_ptr(), s)
     agg = agg.reshape(b, h, w)
-    if cfg.sigma_s > 0:
-        final = sep_convolve_dev(agg, _gauss_kernel(cfg.sigma_s), cfg.pad)
-    else:
-        final = agg
+    final = sep_convolve_dev(agg, _gauss_kernel(cfg.sigma_s), cfg.pad) if cfg.sigma_s > 0 \
+        else agg
     img = empty((b,), torch.float64)
     N.call("qfca_image_score", final.data_ptr(), b, h, w, cfg.border, img.data_ptr(), s)
+    return final, img
+
+
+def _general_detect(x: torch.Tensor, cfg: PipelineConfig, events=None) -> DetectResult:
+    b, c, h, w = x.shape
+    acc, used, flag = _general_partial(x, cfg, events)
+    final, img = _finalize_dev(acc, used, cfg, h, w)
     return DetectResult(scores=final, image_scores=img, used=used, nonfinite=flag)
 
 
 # ------------------------------------------------------------ public API
+_MAX_ELEMS = (1 << 31) - 1  # features per detect_batch launch (32-bit offsets)
+
+
 def detect_batch(values: torch.Tensor, cfg: PipelineConfig | None = None,
                  groups: int = 0, out: DetectResult | None = None,
                  score_events=None) -> DetectResult:
@@ -260,15 +294,25 @@ def detect_batch(values: torch.Tensor, cfg: PipelineConfig | None = None,
         k = min(cfg.pca_components, x.shape[1])
         mean, comps, _ = pca_fit_batch(x, k)
         x = pca_residual_batch(x, mean, comps)
-    if fused_supported(cfg):
-        from .sharding import wide_supported
-        if wide_supported(cfg, x.shape[2], x.shape[3], x.shape[1]):
-            return _wide_detect(x, cfg)
+    b = x.shape[0]
+    per_image = int(np.prod(x.shape[1:]))
+    if b > 1 and b * per_image > _MAX_ELEMS and score_events is None:
+        # keep every launch's element count inside 32-bit plane offsets
+        step = max(1, _MAX_ELEMS // per_image)
+        parts = [detect_batch(x[i:i + step], cfg, groups) for i in range(0, b, step)]
+        return DetectResult(scores=torch.cat([p.scores for p in parts]),
+                            image_scores=torch.cat([p.image_scores for p in parts]),
+                            used=torch.cat([p.used for p in parts]),
+                            nonfinite=torch.stack([p.nonfinite for p in parts]).amax(0))
+    route = _route(x, cfg)
+    if route == "fused":
         return _fused_detect(x, cfg, groups, out, score_events)
-    return _general_detect(x, cfg)
+    if route == "wide":
+        return _wide_detect(x, cfg, events=score_events)
+    return _general_detect(x, cfg, events=score_events)
 
 
-def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
+def _wide_detect(x: torch.Tensor, cfg: PipelineConfig, events=None) -> DetectResult:
     """Feature planes wider than the fused kernels' 128 columns (an 8192^2
     texture: 1024^2 per channel): each image through the tiled fused path of
     sharding.py (one rank holding every channel), then the channel mean,
@@ -279,6 +323,8 @@ def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
                        image_scores=empty((b,), torch.float64),
                        used=empty((b,), torch.int32), nonfinite=zeros((1,), torch.int32))
     taps = _gauss_kernel(cfg.sigma_s) if cfg.sigma_s > 0 else None
+    if events is not None:
+        events[0].record()
     for i in range(b):
         acc, used, flag = _channel_partial(x[i], cfg)
         out.nonfinite.bitwise_or_(flag)
@@ -289,17 +335,43 @@ def _wide_detect(x: torch.Tensor, cfg: PipelineConfig) -> DetectResult:
         out.scores[i] = final
         N.call("qfca_image_score", out.scores[i].data_ptr(), 1, h, w, cfg.border,
                out.image_scores[i:i + 1].data_ptr(), N.stream())
+    if events is not None:
+        events[1].record()
     return out
+
+
+def _route(x: torch.Tensor, cfg: PipelineConfig) -> str:
+    """The path detect / detect_batch take for device features x (B, C, h, w)."""
+    if not fused_supported(cfg):
+        return "general"
+    from .sharding import wide_supported
+    if wide_supported(cfg, x.shape[2], x.shape[3], x.shape[1]):
+        return "wide"
+    L = N.lib()
+    qc = _qcfg(cfg)
+    if L.qfca_detect_workspace_bytes(x.shape[0], x.shape[1], x.shape[2], x.shape[3],
+                                     ctypes.byref(qc)) < 0:
+        return "general"  # shapes the fused kernels do not take (e.g. very wide planes)
+    return "fused"
 
 
 def detect(f: FeatureMap, cfg: PipelineConfig | None = None,
            timings: dict | None = None) -> AnomalyMap:
-    """scoring.py:235-299: full anomaly-map pipeline on one feature map."""
+    """scoring.py:235-299: full anomaly-map pipeline on one feature map.
+
+    ``timings`` receives the reference's four keys (scoring.py:294-298), timed
+    on the device with CUDA events: ``pca_ms`` (pca_fit + pca_residual),
+    ``quantize_ms`` (fit_quantizer + bin_indices + select_reference; on the fused
+    path the median-quan selection may run inside the scoring kernel, then it
+    is counted in transport_ms), ``transport_ms`` (histograms, transport,
+    association, channel sum) and ``postprocess_ms`` (channel mean, smoothing,
+    image score).
+    """
     cfg = cfg or PipelineConfig()
     _check_cfg(cfg)
     like = is_torch(f.values)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timings is not None \
-        else None
+    E = (lambda: torch.cuda.Event(enable_timing=True)) if timings is not None else None
+    ev = [E() for _ in range(5)] if E else None
     x = to_dev(f.values)[None]
     if ev:
         ev[0].record()
@@ -309,12 +381,20 @@ def detect(f: FeatureMap, cfg: PipelineConfig | None = None,
         x = pca_residual_batch(x, mean, comps)
     if ev:
         ev[1].record()
-    res = _fused_detect(x, cfg) if fused_supported(cfg) else _general_detect(x, cfg)
+    route = _route(x, cfg)
+    if route == "fused":
+        res = _fused_detect(x, cfg, events=(ev[2], ev[3]) if ev else None)
+    elif route == "wide":
+        res = _wide_detect(x, cfg, events=(ev[2], ev[3]) if ev else None)
+    else:
+        res = _general_detect(x, cfg, events=(ev[2], ev[3]) if ev else None)
     if ev:
-        ev[2].record()
-        torch.cuda.synchronize()
+        ev[4].record()
+        ev[4].synchronize()
         timings["pca_ms"] = ev[0].elapsed_time(ev[1])
-        timings["scoring_ms"] = ev[1].elapsed_time(ev[2])
+        timings["quantize_ms"] = ev[1].elapsed_time(ev[2])
+        timings["transport_ms"] = ev[2].elapsed_time(ev[3])
+        timings["postprocess_ms"] = ev[3].elapsed_time(ev[4])
     used = int(res.used[0])
     degenerate = used == 0
     if degenerate:
@@ -421,10 +501,20 @@ def upsample_scores(scores, out_h: int, out_w: int):
     return to_host(out.to(torch.float64), like)
 
 
-def upsample_batch(scores: torch.Tensor, out_h: int, out_w: int) -> torch.Tensor:
-    """(B, h, w) fp64 device maps -> (B, out_h, out_w) float32 device maps."""
+def upsample_batch(scores: torch.Tensor, out_h: int, out_w: int,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+    """(B, h, w) fp64 device maps -> (B, out_h, out_w) float32 device maps
+    (upsample_scores per map, scoring.py:149-152), into ``out`` when given."""
     b, h, w = scores.shape
-    out = empty((b, out_h, out_w), torch.float32)
+    if out is None:
+        out = empty((b, out_h, out_w), torch.float32)
+    elif (tuple(out.shape) != (b, out_h, out_w) or out.dtype != torch.float32
+          or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous (B, out_h, out_w) float32 tensor")
     N.call("qfca_upsample", scores.contiguous().data_ptr(), b, h, w, out_h, out_w,
            out.data_ptr(), N.stream())
     return out
+
+
+def upsample_batch_into(scores: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    return upsample_batch(scores, out.shape[1], out.shape[2], out)

@@ -105,8 +105,14 @@ def channel_partial(values: torch.Tensor, cfg) -> tuple[torch.Tensor, int]:
 
 
 def wide_supported(cfg, h: int, w: int, c: int) -> bool:
-    """Planes wider than STRIP_W that the tiled fused path takes."""
+    """Planes wider than STRIP_W that the tiled fused path takes: the kernel
+    scores a STRIP_H x STRIP_W tile, and strips() can cut the plane (a tile
+    keeps the outputs more than 2 * (T // 2) from its inner edges, so that halo
+    must leave a positive step along both axes)."""
     if not (USE_STRIPS and w > STRIP_W and cfg.pad == "reflect" and cfg.n_bins <= 256):
+        return False
+    halo = 2 * (cfg.patch_size // 2)
+    if STRIP_W - 2 * halo <= 0 or (h > STRIP_H and STRIP_H - 2 * halo <= 0):
         return False
     L = N.lib()
     return L.qfca_score_groups(min(h, STRIP_H), STRIP_W, cfg.n_bins, cfg.patch_size, c, 1, 0,
@@ -115,25 +121,34 @@ def wide_supported(cfg, h: int, w: int, c: int) -> bool:
 
 def _channel_partial(values: torch.Tensor, cfg):
     """channel_partial + the device non-finite flag of the slice."""
-    from .scoring import fused_supported
-    if not fused_supported(cfg):
-        raise NotImplementedError("channel sharding covers the fused configuration")
+    from .scoring import _general_partial, fused_supported
     x = values.contiguous()
     c, h, w = x.shape
     hw = h * w
+    L = N.lib()
+    pad = N.PAD_CODES.get(cfg.pad, -1)
+
+    def general():  # the reference's unfused route (any configuration), on the GPU
+        acc, used, flag = _general_partial(x[None], cfg)
+        return acc[0].reshape(h, w), used, flag
+
+    if not fused_supported(cfg):
+        return general()
+    groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                 cfg.sample_budget, 0)
+    groups_k3 = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                    cfg.sample_budget, 1)
+    wide = wide_supported(cfg, h, w, c)
+    if groups <= 0 and groups_k3 <= 0 and not wide:
+        return general()
     s = N.stream()
     lo, hi, flag = minmax_dev(x, c, hw)
     bins = bins_dev(x, lo, hi, c, hw, cfg.n_bins)
-    L = N.lib()
-    pad = N.PAD_CODES[cfg.pad]
-    groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
-                                 cfg.sample_budget, 0)
     ref = None
-    if bins.element_size() == 1 and wide_supported(cfg, h, w, c):
+    if bins.element_size() == 1 and wide:
         return _strip_partial(bins, lo, hi, cfg, c, h, w), _used(lo, hi, c), flag
     if groups <= 0:  # kernel without in-kernel reference selection: run K3 first
-        groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
-                                     cfg.sample_budget, 1)
+        groups = groups_k3
         ref = empty((c, cfg.n_bins), torch.int32)
         N.call("qfca_select_reference", bins.data_ptr(), bins.element_size(), lo.data_ptr(),
                hi.data_ptr(), c, h, w, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, 0,
