@@ -222,6 +222,35 @@ int qfca_gather_tiles(const void* bins, int32_t channels, int32_t h, int32_t w,
                       const int32_t* row_starts, int32_t n_rows, const int32_t* col_starts,
                       int32_t n_cols, int32_t tile_h, int32_t tile_w, void* out, void* stream);
 
+/* ---- box-pooling API (pooling.py:20-172).  Pad modes: 0 zero, 1 reflect,
+ * 2 wrap, 3 edge (np.pad 'edge': pad_plane's reflect on a length-1 axis,
+ * pooling.py:31-35); given per axis.  dtype codes: 0 f32, 1 f64, 2 u8,
+ * 3 i32, 4 i64, 5 i16, 6 u16, 7 bool. */
+/* pad_plane (pooling.py:20-38): planes (planes, h, w) of elem_bytes-sized
+ * elements -> out (planes, h + 2 margin, w + 2 margin), same element type. */
+int qfca_pad_planes(const void* x, int64_t planes, int32_t h, int32_t w, int32_t margin,
+                    int32_t mode_rows, int32_t mode_cols, int32_t elem_bytes, void* out,
+                    void* stream);
+/* build_sat (pooling.py:56-64): cumsum (planes, H + 1, W + 1) fp64, H = h +
+ * 2 margin, of the padded plane -- np.cumsum down the rows, then across the
+ * columns, both sequential (bit-identical to NumPy). */
+int qfca_build_sat(const void* x, int32_t dtype, int64_t planes, int32_t h, int32_t w,
+                   int32_t margin, int32_t mode_rows, int32_t mode_cols, double* cumsum,
+                   void* stream);
+/* _box_sum_map / box_average(_stack) (pooling.py:97-158) from a SAT: clamp = 1
+ * for zero padding (SAT without margin, clamped rectangles), 0 for a SAT with
+ * margin k / 2; out = ((c11 - c01) - c10) + c00, divided by divisor if > 0. */
+int qfca_sat_box(const double* cumsum, int64_t planes, int32_t h, int32_t w, int32_t k,
+                 int32_t clamp, double divisor, double* out, void* stream);
+/* box_sum (pooling.py:71-94) for n rectangles (r0, r1, c0, c1) of one SAT of
+ * row length sat_w. */
+int qfca_sat_rects(const double* cumsum, int32_t sat_w, const int32_t* rects, int64_t n,
+                   double* out, void* stream);
+/* naive_box_average (pooling.py:161-172): the k^2 shifted planes summed in
+ * (dy, dx) order in fp64, / k^2. */
+int qfca_naive_box(const void* x, int32_t dtype, int64_t planes, int32_t h, int32_t w, int32_t k,
+                   int32_t mode_rows, int32_t mode_cols, double* out, void* stream);
+
 /* Covariance of pca_fit (features.py:167-171): cov = (x - mean)^T (x - mean) / n
  * for a batch of images, x (images, C, hw) fp32 channel-major, mean (images, C)
  * fp64 -> cov (images, C, C) fp64.  fp64-accurate (~1e-11 relative): the

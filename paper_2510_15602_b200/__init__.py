@@ -14,7 +14,8 @@ __version__ = "0.1.0"
 
 from .features import (FeatureMap, FormatError, PcaModel, gaussian_blur, pca_fit,
                        pca_residual)
-from .pooling import box_average, box_average_stack
+from .pooling import (SummedAreaTable, box_average, box_average_stack, box_sum, build_sat,
+                      naive_box_average, pad_plane)
 from .quantize import (REFERENCE_MODES, BinIndexMap, HistogramField, Quantizer,
                        ReferenceHistogram, bin_indices, fit_quantizer, patch_histograms,
                        select_reference)
@@ -31,7 +32,8 @@ from .metrics import EvalSample, MetricReport
 
 __all__ = [
     "FeatureMap", "FormatError", "PcaModel", "gaussian_blur", "pca_fit", "pca_residual",
-    "box_average", "box_average_stack", "REFERENCE_MODES", "BinIndexMap", "HistogramField",
+    "box_average", "box_average_stack", "SummedAreaTable", "box_sum", "build_sat",
+    "naive_box_average", "pad_plane", "REFERENCE_MODES", "BinIndexMap", "HistogramField",
     "Quantizer", "ReferenceHistogram", "bin_indices", "fit_quantizer", "patch_histograms",
     "select_reference", "AnomalyMap", "DetectResult", "PipelineConfig", "aggregate_channels",
     "associate_errors", "bin_error_maps", "channel_error_maps", "detect", "detect_batch",

@@ -65,6 +65,11 @@ _SIGNATURES = {
     "qfca_lanczos": ([_P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "qfca_ritz": ([_P, _I64, _I32, _P, _I32, _P, _P, _P], _I32),
     "qfca_gather_tiles": ([_P, _I32, _I32, _I32, _P, _I32, _P, _I32, _I32, _I32, _P, _P], _I32),
+    "qfca_pad_planes": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
+    "qfca_build_sat": ([_P, _I32, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
+    "qfca_sat_box": ([_P, _I64, _I32, _I32, _I32, _I32, _F64, _P, _P], _I32),
+    "qfca_sat_rects": ([_P, _I32, _P, _I64, _P, _P], _I32),
+    "qfca_naive_box": ([_P, _I32, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
     "qfca_covariance_workspace_bytes": ([_I64, _I32, _I32], _I64),
     "qfca_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),
     "qfca_mean_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),

@@ -59,6 +59,11 @@ int launch_sym_eig(const double*, int64_t, int, double*, double*, cudaStream_t);
 int launch_lanczos(const double*, int64_t, int, int, const double*, double*, double*, double*,
                    double*, int*, cudaStream_t);
 int launch_ritz(const double*, int64_t, int, const double*, int, double*, double*, cudaStream_t);
+int launch_pad_planes(const void*, int64_t, int, int, int, int, int, int, void*, cudaStream_t);
+int launch_build_sat(const void*, int, int64_t, int, int, int, int, int, double*, cudaStream_t);
+int launch_sat_box(const double*, int64_t, int, int, int, int, double, double*, cudaStream_t);
+int launch_sat_rects(const double*, int, const int32_t*, int64_t, double*, cudaStream_t);
+int launch_naive_box(const void*, int, int64_t, int, int, int, int, int, double*, cudaStream_t);
 int launch_gather_tiles(const void*, int, int, int, const int*, int, const int*, int, int, int, void*,
                         cudaStream_t);
 int launch_cov_i8(const float*, int64_t, int, int, const double*, double*, void*, int64_t,
@@ -358,6 +363,36 @@ int qfca_lanczos(const double* cov, int64_t batch, int32_t C, int32_t passes, co
 int qfca_ritz(const double* h, int64_t batch, int32_t n, const double* x0, int32_t iters,
               double* x, double* hm, void* stream) {
     return counted(launch_ritz(h, batch, n, x0, iters, x, hm, S(stream)), 1);
+}
+
+int qfca_pad_planes(const void* x, int64_t planes, int32_t h, int32_t w, int32_t margin,
+                    int32_t mode_rows, int32_t mode_cols, int32_t elem_bytes, void* out,
+                    void* stream) {
+    return counted(launch_pad_planes(x, planes, h, w, margin, mode_rows, mode_cols, elem_bytes,
+                                     out, S(stream)), 1);
+}
+
+int qfca_build_sat(const void* x, int32_t dtype, int64_t planes, int32_t h, int32_t w,
+                   int32_t margin, int32_t mode_rows, int32_t mode_cols, double* cumsum,
+                   void* stream) {
+    return counted(launch_build_sat(x, dtype, planes, h, w, margin, mode_rows, mode_cols, cumsum,
+                                    S(stream)), 2);
+}
+
+int qfca_sat_box(const double* cumsum, int64_t planes, int32_t h, int32_t w, int32_t k,
+                 int32_t clamp, double divisor, double* out, void* stream) {
+    return counted(launch_sat_box(cumsum, planes, h, w, k, clamp, divisor, out, S(stream)), 1);
+}
+
+int qfca_sat_rects(const double* cumsum, int32_t sat_w, const int32_t* rects, int64_t n,
+                   double* out, void* stream) {
+    return counted(launch_sat_rects(cumsum, sat_w, rects, n, out, S(stream)), 1);
+}
+
+int qfca_naive_box(const void* x, int32_t dtype, int64_t planes, int32_t h, int32_t w, int32_t k,
+                   int32_t mode_rows, int32_t mode_cols, double* out, void* stream) {
+    return counted(launch_naive_box(x, dtype, planes, h, w, k, mode_rows, mode_cols, out,
+                                    S(stream)), 1);
 }
 
 int qfca_gather_tiles(const void* bins, int32_t channels, int32_t h, int32_t w,

@@ -31,10 +31,11 @@ def load_golden(name):
 
 
 def golden_names(prefix=""):
-    # metrics_*.npz belong to tests/test_metrics.py (different layout)
+    # metrics_*.npz / pooling.npz / planted_*.npz belong to test_metrics.py,
+    # test_pooling.py and test_planted.py (different layouts)
     return sorted(f[:-4] for f in os.listdir(GOLDEN)
                   if f.endswith(".npz") and f.startswith(prefix)
-                  and not f.startswith("metrics_"))
+                  and not f.startswith(("metrics_", "pooling", "planted_")))
 
 
 def cfg_of(d):

@@ -29,8 +29,9 @@ def _band_noise(g: torch.Generator, n: int, sigma: float, device) -> torch.Tenso
 
 
 def textures(count: int, size: int, seed: int = 0, device="cuda",
-             kinds=("noise", "tiles", "stripes"), defect_frac: float = 0.02):
-    """(count, 3, size, size) images in [0, 1] and (count, size, size) masks."""
+             kinds=("noise", "tiles", "stripes"), defect_frac: float = 0.02, n_good: int = 0):
+    """(count, 3, size, size) images in [0, 1] and (count, size, size) masks;
+    images i < n_good stay clean (no planted square)."""
     g = torch.Generator().manual_seed(seed)
     imgs = torch.empty((count, 3, size, size), device=device)
     masks = torch.zeros((count, size, size), dtype=torch.bool, device=device)
@@ -57,8 +58,9 @@ def textures(count: int, size: int, seed: int = 0, device="cuda",
         m = size // 8
         y0 = int(torch.randint(m, size - m - side, (1,), generator=g))
         x0 = int(torch.randint(m, size - m - side, (1,), generator=g))
-        masks[i, y0:y0 + side, x0:x0 + side] = True
-        img[:, y0:y0 + side, x0:x0 + side] += 0.28
+        if i >= n_good:
+            masks[i, y0:y0 + side, x0:x0 + side] = True
+            img[:, y0:y0 + side, x0:x0 + side] += 0.28
         imgs[i] = img.clamp(0, 1)
     return imgs, masks
 
