@@ -146,6 +146,23 @@ int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const floa
                int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
                int32_t groups, float* partial, void* stream);
 
+/* qfca_score with a caller-owned global scratch: the 128-column kernel (v6,
+ * csrc/score6.cu) keeps each plane's window counts in an L2-resident scratch;
+ * qfca_score_scratch_bytes gives its size for a configuration (0: the chosen
+ * kernel needs none, -1: unsupported) and qfca_score_groups_ex the channel
+ * groups of the kernel chosen with (with_scratch = 1) or without a scratch. */
+int qfca_score_ex(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
+                  const int32_t* ref_cum, int64_t images, int32_t channels, int32_t h, int32_t w,
+                  int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
+                  int32_t groups, void* scratch, int64_t scratch_bytes, float* partial,
+                  void* stream);
+int64_t qfca_score_scratch_bytes(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
+                                 int32_t channels, int64_t images, int32_t groups_hint,
+                                 int32_t pad, int32_t sample_budget, int32_t with_reference);
+int qfca_score_groups_ex(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
+                         int32_t channels, int64_t images, int32_t groups_hint, int32_t pad,
+                         int32_t sample_budget, int32_t with_reference, int32_t with_scratch);
+
 /* agg = (sum over groups, fixed order, fp64) / used   (scoring.py:283-289) */
 int qfca_reduce_partials(const float* partial, int64_t images, int32_t groups, int64_t hw,
                          const int32_t* used, double* agg, void* stream);

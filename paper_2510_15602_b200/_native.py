@@ -52,6 +52,12 @@ _SIGNATURES = {
     "qfca_score_groups": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32], _I32),
     "qfca_score": ([_P, _I32, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                     _P, _P], _I32),
+    "qfca_score_ex": ([_P, _I32, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                       _I32, _P, _I64, _P, _P], _I32),
+    "qfca_score_scratch_bytes": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32],
+                                 _I64),
+    "qfca_score_groups_ex": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32, _I32],
+                             _I32),
     "qfca_reduce_partials": ([_P, _I64, _I32, _I64, _P, _P, _P], _I32),
     "qfca_divide_used": ([_P, _I64, _I64, _P, _P, _P], _I32),
     "qfca_sep_conv": ([_P, _I64, _I32, _I32, _I32, _P, _I32, _I32, _P, _P], _I32),

@@ -81,9 +81,14 @@ int launch_score5(const void*, int, const float*, const float*, const int32_t*, 
                   int, int, int, int, int, int, float*, cudaStream_t);
 int launch_score4(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
+int score6_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
+int64_t score6_scratch_bytes(int);
+int launch_score6(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
+                  int, int, int, int, int, int, void*, int64_t, float*, cudaStream_t);
 
-// fused-kernel selection: 0 = auto (v4, else v3, else v5, else v2, else v1 --
-// the first that applies), 1 .. 5 = force that version
+// fused-kernel selection: 0 = auto (v4, else v6 when the caller supplies a
+// scratch, else v3, else v5, else v2, else v1 -- the first that applies),
+// 1 .. 6 = force that version
 static int g_score_kernel = 0;
 
 struct ScoreChoice {
@@ -95,8 +100,16 @@ struct ScoreChoice {
 // want_fref: the caller has no reference (V) and wants the kernel to select it
 static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t images,
                                 int groups_hint, int bins_bytes, int pad, int budget,
-                                int want_fref) {
+                                int want_fref, int allow_scratch = 0) {
     ScoreChoice ch{-1, 1, 0};
+    if (allow_scratch && (g_score_kernel == 0 || g_score_kernel == 6) && bins_bytes == 1) {
+        int fr = 0;
+        const int gg = score6_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
+                                    want_fref, &fr);
+        // v6 either selects the reference itself or takes the caller's
+        if (gg > 0 && fr == (want_fref ? 1 : 0)) return ScoreChoice{gg, 6, fr};
+    }
+    if (g_score_kernel == 6) return ch;
     if ((g_score_kernel == 0 || g_score_kernel == 4) && bins_bytes == 1) {
         int fr = 0;
         const int gg = score4_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
@@ -130,11 +143,20 @@ static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t 
     return ch;
 }
 
+static int64_t choice_scratch_bytes(const ScoreChoice& ch, int h) {
+    return ch.ver == 6 ? score6_scratch_bytes(h) : 0;
+}
+
 static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_bytes,
                             const float* lo, const float* hi, const int32_t* V, int64_t images,
                             int C, int h, int w, int n_bins, int t, int pad, int budget,
-                            float* partial, cudaStream_t st) {
+                            float* partial, cudaStream_t st, void* scratch = nullptr,
+                            int64_t scratch_bytes = 0) {
     if (ch.groups <= 0) return QFCA_ERR_UNSUPPORTED;
+    if (ch.ver == 6)
+        return launch_score6(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
+                             n_bins, t, pad, budget, ch.groups, scratch, scratch_bytes, partial,
+                             st);
     if (ch.ver == 5)
         return launch_score5(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
                              n_bins, t, pad, budget, ch.groups, partial, st);
@@ -268,6 +290,26 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
     return ch.groups;
 }
 
+int qfca_score_groups_ex(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
+                         int32_t channels, int64_t images, int32_t groups_hint, int32_t pad,
+                         int32_t sample_budget, int32_t with_reference, int32_t with_scratch) {
+    const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, groups_hint,
+                                        n_bins <= 256 ? 1 : 2, pad, sample_budget,
+                                        with_reference ? 0 : 1, with_scratch);
+    if (!with_reference && !ch.fref) return -1;
+    return ch.groups;
+}
+
+int64_t qfca_score_scratch_bytes(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
+                                 int32_t channels, int64_t images, int32_t groups_hint,
+                                 int32_t pad, int32_t sample_budget, int32_t with_reference) {
+    const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, groups_hint,
+                                        n_bins <= 256 ? 1 : 2, pad, sample_budget,
+                                        with_reference ? 0 : 1, 1);
+    if (ch.groups <= 0 || (!with_reference && !ch.fref)) return -1;
+    return choice_scratch_bytes(ch, h);
+}
+
 int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
                        int32_t channels, int64_t images, int32_t pad, int32_t sample_budget,
                        int32_t with_reference) {
@@ -279,7 +321,7 @@ int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
 }
 
 int qfca_set_score_kernel(int32_t version) {
-    if (version < 0 || version > 5) return QFCA_ERR_ARG;
+    if (version < 0 || version > 6) return QFCA_ERR_ARG;
     g_score_kernel = version;
     return QFCA_OK;
 }
@@ -294,6 +336,23 @@ int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const floa
     if (!ref_cum && !ch.fref) return QFCA_ERR_UNSUPPORTED;
     return counted(launch_score_any(ch, bins, bins_bytes, lo, hi, ref_cum, images, channels, h,
                                     w, n_bins, patch_size, pad, sample_budget, partial, S(stream)),
+                   1);
+}
+
+int qfca_score_ex(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
+                  const int32_t* ref_cum, int64_t images, int32_t channels, int32_t h, int32_t w,
+                  int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
+                  int32_t groups, void* scratch, int64_t scratch_bytes, float* partial,
+                  void* stream) {
+    const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, groups,
+                                        bins_bytes, pad, sample_budget, ref_cum ? 0 : 1,
+                                        scratch != nullptr && scratch_bytes > 0);
+    if (groups > 0 && ch.groups != groups) return QFCA_ERR_ARG;
+    if (!ref_cum && !ch.fref) return QFCA_ERR_UNSUPPORTED;
+    if (scratch_bytes < choice_scratch_bytes(ch, h)) return QFCA_ERR_ARG;
+    return counted(launch_score_any(ch, bins, bins_bytes, lo, hi, ref_cum, images, channels, h,
+                                    w, n_bins, patch_size, pad, sample_budget, partial, S(stream),
+                                    scratch, scratch_bytes),
                    1);
 }
 
@@ -425,7 +484,7 @@ int qfca_mean_covariance(const float* x, int64_t images, int32_t C, int32_t hw, 
 
 // ---------------------------------------------------------------- detect
 struct DetectLayout {
-    size_t lo, hi, bins, V, partial, used_scratch, agg, tmp, total;
+    size_t lo, hi, bins, V, partial, used_scratch, agg, tmp, kscratch, kscratch_bytes, total;
     int groups, bins_bytes;
     ScoreChoice choice;
 };
@@ -442,7 +501,7 @@ static int detect_layout(int64_t images, int32_t C, int32_t h, int32_t w, const 
     const int64_t planes = images * C, hw = (int64_t)h * w;
     L->bins_bytes = cfg->n_bins <= 256 ? 1 : 2;
     L->choice = score_choose(h, w, cfg->n_bins, cfg->patch_size, C, images, cfg->groups,
-                             L->bins_bytes, cfg->pad, cfg->sample_budget, 1);
+                             L->bins_bytes, cfg->pad, cfg->sample_budget, 1, 1);
     L->groups = L->choice.groups;
     if (L->groups <= 0) return QFCA_ERR_UNSUPPORTED;
     size_t off = 0;
@@ -454,6 +513,8 @@ static int detect_layout(int64_t images, int32_t C, int32_t h, int32_t w, const 
     L->used_scratch = off; off = align256(off + images * 4);
     L->agg = off; off = align256(off + images * hw * 8);
     L->tmp = off; off = align256(off + images * hw * 8);
+    L->kscratch_bytes = (size_t)choice_scratch_bytes(L->choice, h);
+    L->kscratch = off; off = align256(off + L->kscratch_bytes);
     L->total = off;
     return QFCA_OK;
 }
@@ -529,7 +590,8 @@ int qfca_detect_ex(const float* features, int64_t images, int32_t C, int32_t h, 
         return QFCA_ERR_CUDA;
     if ((rc = counted(launch_score_any(L.choice, bins, L.bins_bytes, lo, hi, V, images, C, h, w,
                                        cfg->n_bins, cfg->patch_size, cfg->pad,
-                                       cfg->sample_budget, partial, st),
+                                       cfg->sample_budget, partial, st, ws + L.kscratch,
+                                       (int64_t)L.kscratch_bytes),
                       1)))
         return rc;
     if (stage_events && stage_events[1] &&

@@ -1,0 +1,707 @@
+// score6.cu -- K4 v6: the fused scoring kernel for 128-wide planes (the
+// 128 x 128 feature planes of 1024^2 textures, configs[2]; the 256 x 128
+// tiles of wide planes, configs[4]).
+//
+// Same mathematics and the same fp32 arithmetic sequence as score3.cu (see
+// score2.cu's header for the closed forms), so v6 reproduces v3 bit for bit;
+// a different schedule, built from the ncu profile of v3 (shared-memory
+// wavefronts ~5 per (channel, pixel) and ~35% barrier stalls of its
+// producer / consumer warps):
+//
+//   phase 1  window counts of the whole plane, all 16 warps: vertical
+//            windows (H1, four threads per column, each sliding over a quarter
+//            of the rows) into a staging band of 32 rows, then the row windows
+//            (H2, 8-column segments, one task per thread) -> the cumulative
+//            thermometer counts of every pixel go to a per-SM scratch in
+//            global memory (L2-resident, word-major rows: [row][word][x]) and
+//            the sample-grid pixels' counts to SA4 in shared memory.  Counts
+//            are computed once per channel (v3 computed them twice).
+//   phase 2  the median-quan reference of all bins by lock-step binary search
+//            over SA4 (score4.cu's packed compares);
+//   phase 3  the transport tables G_i(v);
+//   phase 4  stream rows in sub-chunks of CH rows (CH divides T, so the E
+//            ring stays in registers with static indices): thread (x, group
+//            g) loads its two count words straight from the scratch (loads of
+//            the next sub-chunk in flight during this one), computes E for
+//            each of its 4 bins only when some lane of the warp has mass in
+//            that bin (per-bin, not per-group, warp vote), keeps the vertical
+//            box in the register ring, and stores the vertical sums of bin i
+//            only when some lane's window has bin i (the own-bin gather can
+//            only read those); the own-bin horizontal box of the previous
+//            sub-chunk runs in the same phase from the other Vb buffer, so
+//            there is ONE barrier per sub-chunk and every warp does the same
+//            work.
+// Degenerate channels are skipped outright.  The scratch is indexed by %smid:
+// the kernel's shared memory (> 114 KB) keeps one CTA per SM.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace qfca {
+
+constexpr int S6_THREADS = 512;
+constexpr int S6_W = 128;
+constexpr int S6_BAND = 8;                 // H1 steps per band (x 4 quarters = 32 rows)
+constexpr int S6_SLOTS = 4 * S6_BAND;      // staging rows
+constexpr int S6_SEG = 8;                  // H2 columns per task
+constexpr int S6_SMEM_MAX = 227 * 1024;
+
+struct Score6Geom {
+    int h, n_bins, pad, C, groups, cpg;
+    int S;      // stream rows h + 2R
+    int qrows;  // H1 rows per quarter, ceil(h / 4)
+    int fref, stride, sshift, nsx, nsamp;  // sshift = log2(stride) or -1
+    int dbsb;   // bins double-buffered (next channel prefetched)
+    uint32_t moff;
+    int o_sb, o_sa, o_stg, o_gt, o_th, o_xmap, o_rmap, o_stab, o_pj, o_misc, total;
+};
+
+__device__ __forceinline__ float rcp_approx6(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+template <int OFF>
+__device__ __forceinline__ float lds6_f32(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+__device__ __forceinline__ uint32_t smid6() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// staging element of padded column p: one pad element after every 8 columns,
+// so the 8-column H2 segments of a quarter-warp start in distinct bank groups
+__host__ __device__ constexpr int s6_elem(int p) { return p + (p >> 3); }
+
+template <int T>
+__host__ __device__ constexpr int s6_ch() {
+    return T % 3 == 0 ? 3 : (T % 5 == 0 ? 5 : (T % 7 == 0 ? 7 : T));
+}
+
+template <int T>
+static void score6_layout(Score6Geom& g) {
+    constexpr int R = T / 2;
+    constexpr int CH = s6_ch<T>();
+    constexpr int GP = T * T + 1;
+    const int wpp = s6_elem(S6_W + 2 * R) + 1;
+    int off = 0;
+    auto take = [&](long long bytes) {
+        const int o = off;
+        off = (int)((off + bytes + 15) & ~15LL);
+        return o;
+    };
+    g.o_sb = take((long long)(g.dbsb ? 2 : 1) * g.h * S6_W);
+    // SA4 (phases 1-2) and Vb (phase 4, 2 x CH rows x 16 bins x 128) share one region
+    const long long sa = (long long)g.nsamp * 16;
+    const long long vb = 2LL * CH * 16 * S6_W * 4;
+    g.o_sa = take(sa > vb ? sa : vb);
+    g.o_stg = take((long long)S6_SLOTS * wpp * 16);
+    g.o_gt = take((long long)16 * GP * 4);
+    g.o_pj = take((long long)GP * 4);
+    g.o_th = take(256 * 16);
+    g.o_xmap = take((long long)(S6_W + 2 * R) * 4);
+    const int n_chunks = (g.S + T - 1) / T;
+    g.o_rmap = take((long long)(n_chunks * T + 2 * T) * 4);
+    g.o_stab = take((long long)g.h * 8);
+    g.o_misc = take(2048);  // scale, V, search brackets / mids / per-warp counts
+    g.total = off;
+}
+
+template <int T>
+__global__ void __launch_bounds__(S6_THREADS, 1)
+k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
+         const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score6Geom g,
+         uint32_t* __restrict__ scratch, float* __restrict__ partial) {
+    constexpr int W = S6_W;
+    constexpr int R = T / 2;
+    constexpr int T2 = T * T;
+    constexpr int GP = T2 + 1;
+    constexpr int CH = s6_ch<T>();
+    constexpr int NSUB = T / CH;             // sub-chunks per ring period
+    constexpr int WPP = s6_elem(W + 2 * R) + 1;
+    constexpr uint32_t FULL = 0xffffffffu;
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint8_t* const sbase = sm + g.o_sb;
+    uint4* const SA4 = reinterpret_cast<uint4*>(sm + g.o_sa);
+    float* const Vb = reinterpret_cast<float*>(sm + g.o_sa);
+    uint4* const STG = reinterpret_cast<uint4*>(sm + g.o_stg);
+    float* const GT = reinterpret_cast<float*>(sm + g.o_gt);
+    float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
+    uint4* const TH = reinterpret_cast<uint4*>(sm + g.o_th);
+    int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
+    int* const rmap = reinterpret_cast<int*>(sm + g.o_rmap);
+    int2* const stab = reinterpret_cast<int2*>(sm + g.o_stab);
+    float* const sscale = reinterpret_cast<float*>(sm + g.o_misc);      // [1]
+    int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);         // [16]
+    int* const blo = reinterpret_cast<int*>(sm + g.o_misc + 80);        // [16]
+    int* const bhi = reinterpret_cast<int*>(sm + g.o_misc + 144);       // [16]
+    uint8_t* const qm8 = sm + g.o_misc + 208;                            // [16]
+    uint32_t* const cnt = reinterpret_cast<uint32_t*>(sm + g.o_misc + 256);  // [16 warps][8]
+
+    const int tid = threadIdx.x;
+    const int h = g.h;
+    const int hw = h * W;
+    const int img = blockIdx.x / g.groups, cgi = blockIdx.x % g.groups;
+    const int c_begin = cgi * g.cpg, c_end = min(g.C, c_begin + g.cpg);
+    float* const part = partial + ((int64_t)img * g.groups + cgi) * hw;
+    uint32_t* const scr = scratch + (size_t)smid6() * (size_t)(h + 1) * 4 * W;
+    const int n_chunks = (g.S + T - 1) / T;
+
+    // ---- per-CTA tables
+    for (int p = tid; p < W + 2 * R; p += S6_THREADS) xmap[p] = map_coord(p - R, W, g.pad);
+    // stream rows past the plane read row h of the scratch: all-zero counts, so
+    // E = 0 there without a branch
+    for (int s = tid; s < n_chunks * T + 2 * T; s += S6_THREADS)
+        rmap[s] = s < g.S ? map_coord(s - R, h, g.pad) : h;
+    for (int e = tid; e < h; e += S6_THREADS)
+        stab[e] = make_int2(map_coord(e + R, h, g.pad) * W, map_coord(e - 1 - R, h, g.pad) * W);
+    for (int b = tid; b < 256; b += S6_THREADS) {
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
+            const int d = b - 4 * q;
+            v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+        }
+        TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    for (int i = tid; i < 4 * W; i += S6_THREADS) scr[(size_t)h * 4 * W + i] = 0u;
+    // bins of the first channel
+    {
+        const int64_t plane = (int64_t)img * g.C + c_begin;
+        if (c_begin < c_end)
+            for (int i = tid; i < hw / 16; i += S6_THREADS)
+                cp_async16(sbase + 16 * i, bins + plane * hw + 16 * i);
+    }
+
+    __syncthreads();  // xmap (read below by every thread) complete
+    // phase-1 roles: H1 thread (column col, quarter q); H2 task (slot, segment)
+    const int col = tid & (W - 1), q1 = tid >> 7;
+    const int hy0 = q1 * g.qrows, hy1 = min(h, hy0 + g.qrows);
+    int halo0 = -1, halo1 = -1;  // padded columns (other than col + R) that map to col
+    for (int j = 0; j < 2 * R; ++j) {
+        const int p = j < R ? j : W + j;
+        if (xmap[p] == col) {
+            if (halo0 < 0) halo0 = p;
+            else if (halo1 < 0) halo1 = p;
+        }
+    }
+    const int t_slot = tid >> 4, t_seg = tid & 15;
+    const int t_q = t_slot >> 3, t_k = t_slot & 7;
+    // phase-4 roles: thread (column x, bin group grp)
+    const int x = tid & (W - 1), grp = tid >> 7;
+    const uint32_t gaddr =
+        (uint32_t)__cvta_generic_to_shared(GT + grp * 4 * GP) + g.moff;
+
+    int buf = 0;
+    for (int c = c_begin; c < c_end; ++c) {
+        const int64_t plane = (int64_t)img * g.C + c;
+        const uint8_t* const sb = sbase + (g.dbsb ? buf * hw : 0);
+        if (tid == 0) {
+            float sc = 0.f;
+            if (hi[plane] > lo[plane])
+                sc = (float)(((double)hi[plane] - (double)lo[plane]) / (double)g.n_bins /
+                             (double)T2);
+            sscale[0] = sc;
+        }
+        if (!g.fref && tid < 16) sV[tid] = tid < g.n_bins ? __ldg(Vref + plane * g.n_bins + tid) : T2;
+        cp_async_wait_all();
+        __syncthreads();
+        const float scale = sscale[0];
+        if (scale == 0.f) {  // degenerate channel: skipped (scoring.py:265-266)
+            __syncthreads();  // every thread has read sscale before tid 0 rewrites it
+            if (!g.dbsb) {
+                if (c + 1 < c_end)
+                    for (int i = tid; i < hw / 16; i += S6_THREADS)
+                        cp_async16(sbase + 16 * i, bins + (plane + 1) * hw + 16 * i);
+            } else {
+                buf ^= 1;
+                if (c + 1 < c_end)
+                    for (int i = tid; i < hw / 16; i += S6_THREADS)
+                        cp_async16(sbase + buf * hw + 16 * i, bins + (plane + 1) * hw + 16 * i);
+            }
+            continue;
+        }
+        // prefetch the next channel's bins into the other buffer
+        if (g.dbsb && c + 1 < c_end)
+            for (int i = tid; i < hw / 16; i += S6_THREADS)
+                cp_async16(sbase + (buf ^ 1) * hw + 16 * i, bins + (plane + 1) * hw + 16 * i);
+
+        // ======== phase 1: window counts -> scratch (word-major rows) + SA4 samples
+        {
+            uint4 cst = make_uint4(0, 0, 0, 0);
+            const uint8_t* const pb = sb + col;
+            for (int kb = 0; kb < g.qrows; kb += S6_BAND) {
+                // H1: S6_BAND rows of this quarter -> staging slots q1 * 8 + kk
+#pragma unroll 1
+                for (int kk = 0; kk < S6_BAND; ++kk) {
+                    const int y = hy0 + kb + kk;
+                    if (y >= hy1) break;
+                    if (y == hy0) {
+                        cst = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                        for (int dy = -R; dy <= R; ++dy) {
+                            const uint4 a = TH[pb[map_coord(y + dy, h, g.pad) * W]];
+                            cst.x += a.x;
+                            cst.y += a.y;
+                            cst.z += a.z;
+                            cst.w += a.w;
+                        }
+                    } else {
+                        const int2 st = stab[y];
+                        const uint4 a = TH[pb[st.x]], r = TH[pb[st.y]];
+                        cst.x += a.x - r.x;
+                        cst.y += a.y - r.y;
+                        cst.z += a.z - r.z;
+                        cst.w += a.w - r.w;
+                    }
+                    uint4* row = STG + (q1 * S6_BAND + kk) * WPP;
+                    row[s6_elem(col + R)] = cst;
+                    if (halo0 >= 0) row[s6_elem(halo0)] = cst;
+                    if (halo1 >= 0) row[s6_elem(halo1)] = cst;
+                }
+                __syncthreads();
+                // H2: task (slot, 8-column segment) -> 8 cumulative counts
+                {
+                    const int y = t_q * g.qrows + kb + t_k;
+                    if (kb + t_k < g.qrows && y < min(h, (t_q + 1) * g.qrows)) {
+                        const int x0 = t_seg * S6_SEG;
+                        const uint4* src = STG + t_slot * WPP + 9 * t_seg;  // elem(x0)
+                        uint4 out[S6_SEG];
+                        uint4 sum = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                        for (int p = 0; p < T; ++p) {
+                            const uint4 v = src[s6_elem(p)];
+                            sum.x += v.x;
+                            sum.y += v.y;
+                            sum.z += v.z;
+                            sum.w += v.w;
+                        }
+                        out[0] = sum;
+#pragma unroll
+                        for (int k = 1; k < S6_SEG; ++k) {
+                            const uint4 a = src[s6_elem(k + 2 * R)], rr = src[s6_elem(k - 1)];
+                            sum.x += a.x - rr.x;
+                            sum.y += a.y - rr.y;
+                            sum.z += a.z - rr.z;
+                            sum.w += a.w - rr.w;
+                            out[k] = sum;
+                        }
+                        uint32_t* dst = scr + (size_t)y * 4 * W + x0;
+                        reinterpret_cast<uint4*>(dst)[0] = make_uint4(out[0].x, out[1].x, out[2].x, out[3].x);
+                        reinterpret_cast<uint4*>(dst)[1] = make_uint4(out[4].x, out[5].x, out[6].x, out[7].x);
+                        reinterpret_cast<uint4*>(dst + W)[0] = make_uint4(out[0].y, out[1].y, out[2].y, out[3].y);
+                        reinterpret_cast<uint4*>(dst + W)[1] = make_uint4(out[4].y, out[5].y, out[6].y, out[7].y);
+                        reinterpret_cast<uint4*>(dst + 2 * W)[0] = make_uint4(out[0].z, out[1].z, out[2].z, out[3].z);
+                        reinterpret_cast<uint4*>(dst + 2 * W)[1] = make_uint4(out[4].z, out[5].z, out[6].z, out[7].z);
+                        reinterpret_cast<uint4*>(dst + 3 * W)[0] = make_uint4(out[0].w, out[1].w, out[2].w, out[3].w);
+                        reinterpret_cast<uint4*>(dst + 3 * W)[1] = make_uint4(out[4].w, out[5].w, out[6].w, out[7].w);
+                        if (g.fref) {
+                            if (g.sshift >= 0) {  // power-of-two stride
+                                const int sm1 = (1 << g.sshift) - 1;
+                                if ((y & sm1) == 0) {
+                                    uint4* sa = SA4 + (y >> g.sshift) * g.nsx;
+#pragma unroll
+                                    for (int k = 0; k < S6_SEG; ++k)
+                                        if (((x0 + k) & sm1) == 0) sa[(x0 + k) >> g.sshift] = out[k];
+                                }
+                            } else if (y % g.stride == 0) {
+                                uint4* sa = SA4 + (y / g.stride) * g.nsx;
+#pragma unroll
+                                for (int k = 0; k < S6_SEG; ++k)
+                                    if ((x0 + k) % g.stride == 0) sa[(x0 + k) / g.stride] = out[k];
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+
+        // ======== phase 2: reference (smallest v with #{samples: A_i <= v} >= S - m)
+        if (g.fref) {
+            constexpr int ROUNDS = T2 < 2 ? 1 : (T2 < 4 ? 2 : (T2 < 8 ? 3 : (T2 < 16 ? 4 :
+                                   (T2 < 32 ? 5 : (T2 < 64 ? 6 : 7)))));
+            constexpr int WPS = S6_THREADS / 32;
+            const int c0 = g.nsamp - (g.nsamp - 1) / 2;
+            if (tid < 16) {
+                const int top = tid < g.n_bins - 1 ? 0 : T2;
+                blo[tid] = top;
+                bhi[tid] = T2;
+                qm8[tid] = (uint8_t)((top + T2) >> 1);
+            }
+            __syncthreads();
+            const uint32_t* const qm = reinterpret_cast<const uint32_t*>(qm8);
+#pragma unroll 1
+            for (int r = 0; r < ROUNDS; ++r) {
+                uint32_t Q[4], acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) Q[qq] = 0x80808080u | qm[qq];
+                for (int s = tid; s < g.nsamp; s += S6_THREADS) {
+                    const uint4 v = SA4[s];
+                    acc[0] += __umulhi((Q[0] - v.x) & 0x80808080u, 1u << 25);
+                    acc[1] += __umulhi((Q[1] - v.y) & 0x80808080u, 1u << 25);
+                    acc[2] += __umulhi((Q[2] - v.z) & 0x80808080u, 1u << 25);
+                    acc[3] += __umulhi((Q[3] - v.w) & 0x80808080u, 1u << 25);
+                }
+                uint32_t* cp = cnt + (tid >> 5) * 8;
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    const uint32_t ev = __reduce_add_sync(FULL, acc[qq] & 0x00FF00FFu);
+                    const uint32_t od = __reduce_add_sync(FULL, (acc[qq] >> 8) & 0x00FF00FFu);
+                    if ((tid & 31) == 0) {
+                        cp[2 * qq] = ev;
+                        cp[2 * qq + 1] = od;
+                    }
+                }
+                __syncthreads();
+                if (tid < 16) {
+                    const int i = tid, j = i & 3, qq = i >> 2;
+                    uint32_t word = 0;  // 16-bit fields: nsamp < 65536
+#pragma unroll
+                    for (int w = 0; w < WPS; ++w) word += cnt[w * 8 + 2 * qq + (j & 1)];
+                    const int count = (int)((j >> 1) ? word >> 16 : word & 0xFFFFu);
+                    int a = blo[i], bnd = bhi[i];
+                    const int mid = (a + bnd) >> 1;
+                    if (count >= c0) bnd = mid; else a = mid + 1;
+                    blo[i] = a;
+                    bhi[i] = bnd;
+                    qm8[i] = (uint8_t)((a + bnd) >> 1);
+                }
+                __syncthreads();
+            }
+            if (tid < 16) sV[tid] = blo[tid];
+            __syncthreads();
+        }
+
+        // ======== phase 3: PJ = prefix of J, G_i(v) for every bin and count
+        for (int qq = tid; qq < T2; qq += S6_THREADS) {
+            int a = 0, bnd = g.n_bins - 1;
+            while (a < bnd) {
+                const int mid = (a + bnd) >> 1;
+                if (sV[mid] > qq) bnd = mid; else a = mid + 1;
+            }
+            sPJ[qq + 1] = (float)a;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const int lane = tid;
+            float carry = 0.f;
+            if (lane == 0) sPJ[0] = 0.f;
+            for (int base = 1; base <= T2; base += 32) {
+                const int qq = base + lane;
+                float v = qq <= T2 ? sPJ[qq] : 0.f;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float u = __shfl_up_sync(FULL, v, o);
+                    if (lane >= o) v += u;
+                }
+                v += carry;
+                if (qq <= T2) sPJ[qq] = v;
+                carry = __shfl_sync(FULL, v, 31);
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < 16 * GP; idx += S6_THREADS) {
+            const int i = idx / GP, v = idx - i * GP;
+            float vm = 0.f, d = 0.f;
+            if (i < g.n_bins) {
+                const int vmi = i > 0 ? sV[i - 1] : 0;
+                vm = (float)vmi;
+                d = 2.f * ((float)i * vm - sPJ[vmi]);
+            }
+            const float fv = (float)v;
+            const float nu = fmaf((float)i, fv, -sPJ[v]);
+            GT[idx] = fv < vm ? nu : d - nu;
+        }
+        __syncthreads();  // GT ready; SA4 free (Vb aliases it)
+
+        // ======== phase 4: E (register ring) + own-bin box, one barrier per sub-chunk.
+        // The count rows of sub-chunk u + 2 are copied (cp.async) from the scratch
+        // into a 3-slot ring in the (now free) staging region while sub-chunk u
+        // runs; each slot is [row][word][x].
+        {
+            uint32_t* const cring = reinterpret_cast<uint32_t*>(STG);
+            constexpr int SLOT = CH * 4 * W;  // uint32 per slot
+            const int n_sub = n_chunks * NSUB;
+            // copy tasks (row of the sub-chunk, 16-byte piece): 128 pieces per 2 KB row
+            constexpr int NCP = (CH * 128 + S6_THREADS - 1) / S6_THREADS;
+#define S6_COPY(SUB)                                                            \
+    {                                                                           \
+        const int sub_ = (SUB);                                                 \
+        if (sub_ < n_sub) {                                                     \
+            uint32_t* const dst_ = cring + (sub_ % 3) * SLOT;                   \
+            _Pragma("unroll") for (int k_ = 0; k_ < NCP; ++k_) {                \
+                const int task_ = tid + S6_THREADS * k_;                        \
+                if (task_ < CH * 128) {                                         \
+                    const int rr_ = task_ >> 7, pc_ = 4 * (task_ & 127);        \
+                    const int row_ = rmap[sub_ * CH + rr_];                     \
+                    cp_async16(dst_ + rr_ * 4 * W + pc_, scr + (size_t)row_ * 4 * W + pc_); \
+                }                                                               \
+            }                                                                   \
+        }                                                                       \
+        asm volatile("cp.async.commit_group;" ::: "memory");                    \
+    }
+            S6_COPY(0)
+            S6_COPY(1)
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();  // slot 0 visible
+            float ring[T][4];
+            bool mring[T];  // group mass of the last T stream rows (static slots)
+            float vs[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                vs[j] = 0.f;
+#pragma unroll
+                for (int qq = 0; qq < T; ++qq) ring[qq][j] = 0.f;
+            }
+#pragma unroll
+            for (int qq = 0; qq < T; ++qq) mring[qq] = false;
+            const bool g1 = grp > 0;
+            // own-bin box rows of a sub-chunk: row a * 4 + ((grp + 3) & 3), so bin
+            // group 0 (mass in nearly every window, the longest E) boxes last
+            const int arow0 = (grp + 3) & 3;
+            constexpr int NA = (CH + 3) / 4;
+            float pold[NA];  // partial-map values of the rows boxed next
+#pragma unroll
+            for (int a = 0; a < NA; ++a) pold[a] = 0.f;
+            auto own_bin_box = [&](int u, const float* pv, bool last) {
+                const float* const vbr = Vb + (size_t)((u & 1) * CH) * 16 * W;
+#pragma unroll
+                for (int a = 0; a < NA; ++a) {
+                    const int rr = arow0 + 4 * a;
+                    const int y = u * CH + rr - 2 * R;
+                    if (rr >= CH || y < 0 || y >= h) continue;
+                    const int bb = sb[y * W + x];
+                    const float* vb = vbr + (rr * 16 + bb) * W;
+                    float f = 0.f;
+                    if (x >= R && x + R < W) {
+#pragma unroll
+                        for (int d = -R; d <= R; ++d) f += vb[x + d];
+                    } else {
+#pragma unroll
+                        for (int d = 0; d < T; ++d) f += vb[xmap[x + d]];
+                    }
+                    const float old = last ? part[y * W + x] : pv[a];
+                    part[y * W + x] = old + fmaf(f, scale, 0.f);
+                }
+            };
+            for (int ck = 0; ck < n_chunks; ++ck) {
+#pragma unroll
+                for (int sc = 0; sc < NSUB; ++sc) {
+                    const int u = ck * NSUB + sc;  // sub-chunk index
+                    S6_COPY(u + 2)
+                    const uint32_t* const cs = cring + (u % 3) * SLOT + grp * W + x;
+                    float* const vbw = Vb + (size_t)((u & 1) * CH) * 16 * W;
+                    // ---- E for CH stream rows (rows past the plane read zero counts)
+#pragma unroll
+                    for (int rr = 0; rr < CH; ++rr) {
+                        const int rho = sc * CH + rr;  // static ring slot
+                        const int s = u * CH + rr;
+                        float E[4] = {0.f, 0.f, 0.f, 0.f};
+                        const uint32_t word = cs[rr * 4 * W];
+                        const uint32_t prev = g1 ? cs[rr * 4 * W - W] : 0u;
+                        const bool mass = (word >> 24) != (prev >> 24);  // any mass in the group
+                        if (__any_sync(FULL, mass)) {
+                            uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                            uint32_t aa = gaddr + 4u * ma;
+#define S6_E(J)                                                                 \
+    {                                                                           \
+        const uint32_t mb = __byte_perm(word, 0x4B000000u, 0x7650 + J);         \
+        const uint32_t ab = gaddr + 4u * mb;                                    \
+        const float gb = lds6_f32<J * GP * 4>(ab);                              \
+        const float ga = lds6_f32<J * GP * 4>(aa);                              \
+        const float pc = __uint_as_float(mb) - __uint_as_float(ma);             \
+        E[J] = (gb - ga) * rcp_approx6(fmaxf(pc, 1.f));                         \
+        ma = mb;                                                                \
+        aa = ab;                                                                \
+    }
+                            S6_E(0) S6_E(1) S6_E(2) S6_E(3)
+#undef S6_E
+                        }
+                        mring[rho] = mass;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            vs[j] += E[j] - ring[rho][j];
+                            ring[rho][j] = E[j];
+                        }
+                        if (rho == T - 1) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                float sum = ring[0][j];
+#pragma unroll
+                                for (int qq = 1; qq < T; ++qq) sum += ring[qq][j];
+                                vs[j] = sum;
+                            }
+                        }
+                        const int y = s - 2 * R;
+                        // vertical sums of output row y; the own-bin box reads bin i
+                        // at (y, x) only if the window centred there holds bin i,
+                        // i.e. only if this group has mass there (stream row s - R)
+                        if (y >= 0 && y < h && __any_sync(FULL, mring[(rho + T - R) % T])) {
+                            float* vb = vbw + (rr * 16 + grp * 4) * W + x;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
+                        }
+                    }
+                    // ---- own-bin horizontal box of sub-chunk u - 1 (other Vb buffer)
+                    if (u >= 1) own_bin_box(u - 1, pold, false);
+                    // partial-map values for the box of sub-chunk u (next iteration)
+#pragma unroll
+                    for (int a = 0; a < NA; ++a) {
+                        const int rr = arow0 + 4 * a;
+                        const int y = u * CH + rr - 2 * R;
+                        pold[a] = (rr < CH && y >= 0 && y < h) ? part[y * W + x] : 0.f;
+                    }
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");  // slot u + 1 landed
+                    __syncthreads();
+                }
+            }
+            own_bin_box(n_sub - 1, pold, false);  // the last sub-chunk
+        }
+#undef S6_COPY
+        __syncthreads();
+        if (g.dbsb) {
+            buf ^= 1;
+        } else if (c + 1 < c_end) {
+            for (int i = tid; i < hw / 16; i += S6_THREADS)
+                cp_async16(sbase + 16 * i, bins + (plane + 1) * hw + 16 * i);
+        }
+    }
+    cp_async_wait_all();
+}
+
+int sample_stride(int h, int w, int budget);
+
+__global__ void k_nsmid(int* out) {
+    uint32_t n;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+    *out = (int)n;
+}
+
+// %nsmid (an upper bound of %smid) of the current device, read once
+static int nsmid_cached() {
+    static int n = 0;
+    if (n <= 0) {
+        int* d = nullptr;
+        int v = 0;
+        if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+            k_nsmid<<<1, 1>>>(d);
+            if (cudaMemcpy(&v, d, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) v = 0;
+            cudaFree(d);
+        }
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+        n = v > sms ? v : sms + 32;
+    }
+    return n;
+}
+
+template <int T>
+static int s6_total(Score6Geom& g) {
+    score6_layout<T>(g);
+    return g.total;
+}
+
+static int score6_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                       int pad, int budget, bool has_ref, Score6Geom* out, size_t* smem_out) {
+    if (w != S6_W || t < 1 || t > 15 || (t & 1) == 0 || n_bins < 1 || n_bins > 16)
+        return QFCA_ERR_UNSUPPORTED;
+    if (h < 1 || h > 256 || (h * w) % 16) return QFCA_ERR_UNSUPPORTED;
+    if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
+    if (!(pad == QFCA_PAD_WRAP || h > 1)) return QFCA_ERR_UNSUPPORTED;
+    Score6Geom g;
+    memset(&g, 0, sizeof(g));
+    g.h = h; g.n_bins = n_bins; g.pad = pad; g.C = C;
+    g.S = h + 2 * (t / 2);
+    g.qrows = (h + 3) / 4;
+    g.moff = 0u - 4u * 0x4B000000u;
+    if (!has_ref) {
+        if (t * t > 126 || budget < 1) return QFCA_ERR_UNSUPPORTED;
+        g.fref = 1;
+        g.stride = sample_stride(h, w, budget);
+        g.sshift = -1;
+        for (int k = 0; k < 8; ++k)
+            if (g.stride == (1 << k)) g.sshift = k;
+        g.nsx = (w + g.stride - 1) / g.stride;
+        g.nsamp = ((h + g.stride - 1) / g.stride) * g.nsx;
+        if (g.nsamp > 4096 || g.nsamp >= 65536) return QFCA_ERR_UNSUPPORTED;
+    }
+    size_t bytes = 0;
+    for (int db = 1; db >= 0; --db) {
+        g.dbsb = db;
+        switch (t) {
+#define S6C(TT) case TT: bytes = s6_total<TT>(g); break;
+            S6C(1) S6C(3) S6C(5) S6C(7) S6C(9) S6C(11) S6C(13) S6C(15)
+#undef S6C
+            default: return QFCA_ERR_UNSUPPORTED;
+        }
+        if (bytes <= (size_t)S6_SMEM_MAX) break;
+    }
+    if (bytes > (size_t)S6_SMEM_MAX || bytes <= 114 * 1024) return QFCA_ERR_UNSUPPORTED;
+    int groups = groups_hint;
+    if (groups <= 0) groups = balanced_groups(images, C, 1, 1);
+    groups = groups < 1 ? 1 : (groups > C ? C : groups);
+    g.cpg = (C + groups - 1) / groups;
+    g.groups = (C + g.cpg - 1) / g.cpg;
+    *out = g;
+    *smem_out = bytes;
+    return QFCA_OK;
+}
+
+int score6_query(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                 int pad, int budget, int want_fref, int* fref) {
+    Score6Geom g;
+    size_t smem;
+    if (score6_plan(h, w, n_bins, t, C, images, groups_hint, pad, budget, want_fref == 0, &g,
+                    &smem) != QFCA_OK)
+        return -1;
+    if (fref) *fref = g.fref;
+    return g.groups;
+}
+
+int64_t score6_scratch_bytes(int h) {
+    return (int64_t)nsmid_cached() * (h + 1) * 4 * S6_W * 4;
+}
+
+int launch_score6(const void* bins, int bins_bytes, const float* lo, const float* hi,
+                  const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
+                  int pad, int budget, int groups, void* scratch, int64_t scratch_bytes,
+                  float* partial, cudaStream_t st) {
+    if (bins_bytes != 1) return QFCA_ERR_UNSUPPORTED;
+    if (!scratch || scratch_bytes < score6_scratch_bytes(h)) return QFCA_ERR_ARG;
+    Score6Geom g;
+    size_t smem;
+    int rc = score6_plan(h, w, n_bins, t, C, images, groups, pad, budget, V != nullptr, &g, &smem);
+    if (rc != QFCA_OK) return rc;
+    if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
+    void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score6Geom,
+                 uint32_t*, float*) = nullptr;
+    switch (t) {
+#define S6K(TT) case TT: kern = k_score6<TT>; break;
+        S6K(1) S6K(3) S6K(5) S6K(7) S6K(9) S6K(11) S6K(13) S6K(15)
+#undef S6K
+        default: return QFCA_ERR_UNSUPPORTED;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    const int64_t grid = images * g.groups;
+    kern<<<(unsigned)grid, S6_THREADS, smem, st>>>((const uint8_t*)bins, lo, hi, V, g,
+                                                   (uint32_t*)scratch, partial);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+}  // namespace qfca

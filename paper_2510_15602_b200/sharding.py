@@ -115,8 +115,8 @@ def wide_supported(cfg, h: int, w: int, c: int) -> bool:
     if STRIP_W - 2 * halo <= 0 or (h > STRIP_H and STRIP_H - 2 * halo <= 0):
         return False
     L = N.lib()
-    return L.qfca_score_groups(min(h, STRIP_H), STRIP_W, cfg.n_bins, cfg.patch_size, c, 1, 0,
-                               N.PAD_CODES[cfg.pad], cfg.sample_budget, 1) > 0
+    return L.qfca_score_groups_ex(min(h, STRIP_H), STRIP_W, cfg.n_bins, cfg.patch_size, c, 1, 0,
+                                  N.PAD_CODES[cfg.pad], cfg.sample_budget, 1, 1) > 0
 
 
 def _channel_partial(values: torch.Tensor, cfg):
@@ -134,10 +134,10 @@ def _channel_partial(values: torch.Tensor, cfg):
 
     if not fused_supported(cfg):
         return general()
-    groups = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
-                                 cfg.sample_budget, 0)
-    groups_k3 = L.qfca_score_groups(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
-                                    cfg.sample_budget, 1)
+    groups = L.qfca_score_groups_ex(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                    cfg.sample_budget, 0, 1)
+    groups_k3 = L.qfca_score_groups_ex(h, w, cfg.n_bins, cfg.patch_size, c, 1, 0, pad,
+                                       cfg.sample_budget, 1, 1)
     wide = wide_supported(cfg, h, w, c)
     if groups <= 0 and groups_k3 <= 0 and not wide:
         return general()
@@ -154,9 +154,7 @@ def _channel_partial(values: torch.Tensor, cfg):
                hi.data_ptr(), c, h, w, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, 0,
                ref.data_ptr(), s)
     partial = zeros((groups, hw), torch.float32)
-    N.call("qfca_score", bins.data_ptr(), bins.element_size(), lo.data_ptr(), hi.data_ptr(),
-           None if ref is None else ref.data_ptr(), 1, c, h, w, cfg.n_bins, cfg.patch_size,
-           pad, cfg.sample_budget, groups, partial.data_ptr(), s)
+    score_call(bins, lo, hi, ref, 1, c, h, w, cfg, groups, partial)
     used = empty((1,), torch.int32)
     N.call("qfca_count_used", lo.data_ptr(), hi.data_ptr(), 1, c, used.data_ptr(), s)
     ones = torch.ones((1,), dtype=torch.int32, device=x.device)
@@ -164,6 +162,29 @@ def _channel_partial(values: torch.Tensor, cfg):
     N.call("qfca_reduce_partials", partial.data_ptr(), 1, groups, hw, ones.data_ptr(),
            acc.data_ptr(), s)
     return acc.reshape(h, w), used, flag
+
+
+_SCRATCH: dict = {}
+
+
+def score_call(bins, lo, hi, ref, images, c, h, w, cfg, groups, partial):
+    """qfca_score_ex with a cached per-stream scratch (the 128-column kernel
+    keeps each plane's window counts in it)."""
+    L = N.lib()
+    pad = N.PAD_CODES[cfg.pad]
+    nbytes = L.qfca_score_scratch_bytes(h, w, cfg.n_bins, cfg.patch_size, c, images, groups, pad,
+                                        cfg.sample_budget, 0 if ref is None else 1)
+    scr = None
+    if nbytes > 0:
+        key = (bins.device.index, torch.cuda.current_stream(bins.device).cuda_stream)
+        scr = _SCRATCH.get(key)
+        if scr is None or scr.numel() < nbytes:
+            scr = torch.empty((nbytes,), dtype=torch.uint8, device=bins.device)
+            _SCRATCH[key] = scr
+    N.call("qfca_score_ex", bins.data_ptr(), bins.element_size(), lo.data_ptr(), hi.data_ptr(),
+           None if ref is None else ref.data_ptr(), images, c, h, w, cfg.n_bins, cfg.patch_size,
+           pad, cfg.sample_budget, groups, None if scr is None else scr.data_ptr(),
+           max(nbytes, 0), partial.data_ptr(), N.stream())
 
 
 def _used(lo, hi, c) -> torch.Tensor:
@@ -200,15 +221,13 @@ def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
     hi_r = hi.repeat(nt).contiguous()
     ref_r = ref.repeat(nt, 1).contiguous()
     L = N.lib()
-    groups = L.qfca_score_groups(th, STRIP_W, cfg.n_bins, cfg.patch_size, c, nt, 0, pad,
-                                 cfg.sample_budget, 1)
+    groups = L.qfca_score_groups_ex(th, STRIP_W, cfg.n_bins, cfg.patch_size, c, nt, 0, pad,
+                                    cfg.sample_budget, 1, 1)
     if groups <= 0:
         raise NotImplementedError("no fused kernel for the tile shape")
     hw = th * STRIP_W
     partial = zeros((nt * groups, hw), torch.float32)
-    N.call("qfca_score", sb.data_ptr(), 1, lo_r.data_ptr(), hi_r.data_ptr(), ref_r.data_ptr(),
-           nt, c, th, STRIP_W, cfg.n_bins, cfg.patch_size, pad, cfg.sample_budget, groups,
-           partial.data_ptr(), s)
+    score_call(sb, lo_r, hi_r, ref_r, nt, c, th, STRIP_W, cfg, groups, partial)
     ones = torch.ones((nt,), dtype=torch.int32, device=bins.device)
     acc = empty((nt, hw), torch.float64)
     N.call("qfca_reduce_partials", partial.data_ptr(), nt, groups, hw, ones.data_ptr(),

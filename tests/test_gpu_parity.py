@@ -254,8 +254,9 @@ def test_large_plane_properties(Q):
                                            ((1, 6, 40, 128), 13, 25, "reflect"),
                                            ((1, 8, 20, 32), 16, 65, "reflect")])
 def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
-    """v1 (score.cu), v2 (score2.cu), v3 (score3.cu), v4 (score4.cu) and v5
-    (score5.cu, any T) fused kernels all match the oracle wherever they apply."""
+    """v1 (score.cu), v2 (score2.cu), v3 (score3.cu), v4 (score4.cu), v5
+    (score5.cu, any T) and v6 (score6.cu, 128-wide planes) fused kernels all
+    match the oracle wherever they apply."""
     from paper_2510_15602_b200 import _native
     from oracle import qfca_oracle as O
     rng = np.random.default_rng(sum(shape) + n + t)
@@ -263,7 +264,7 @@ def test_fused_kernel_versions_vs_oracle(Q, shape, n, t, pad):
     cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
     refs = [O.detect(x[i], n_bins=n, patch_size=t, pad=pad)[0] for i in range(shape[0])]
     try:
-        for ver in (1, 2, 3, 4, 5):
+        for ver in (1, 2, 3, 4, 5, 6):
             _native.call("qfca_set_score_kernel", ver)
             if ver > 1 and Q.fused_supported(cfg):
                 try:
