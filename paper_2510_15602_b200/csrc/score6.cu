@@ -84,10 +84,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // so the 8-column H2 segments of a quarter-warp start in distinct bank groups
 __host__ __device__ constexpr int s6_elem(int p) { return p + (p >> 3); }
 
+// stream rows per sub-chunk (one barrier each) and rows per unrolled period:
+// the period is a multiple of T, so the E ring keeps static register slots
 template <int T>
-__host__ __device__ constexpr int s6_ch() {
-    return T % 3 == 0 ? 3 : (T % 5 == 0 ? 5 : (T % 7 == 0 ? 7 : T));
-}
+__host__ __device__ constexpr int s6_ch() { return 3; }
+template <int T>
+__host__ __device__ constexpr int s6_period() { return T % 3 == 0 ? T : 3 * T; }
 
 template <int T>
 static void score6_layout(Score6Geom& g) {
@@ -111,8 +113,9 @@ static void score6_layout(Score6Geom& g) {
     g.o_pj = take((long long)GP * 4);
     g.o_th = take(256 * 16);
     g.o_xmap = take((long long)(S6_W + 2 * R) * 4);
-    const int n_chunks = (g.S + T - 1) / T;
-    g.o_rmap = take((long long)(n_chunks * T + 2 * T) * 4);
+    constexpr int P = s6_period<T>();
+    const int n_chunks = (g.S + P - 1) / P;
+    g.o_rmap = take((long long)(n_chunks * P + 2 * CH) * 4);
     g.o_stab = take((long long)g.h * 8);
     g.o_misc = take(2048);  // scale, V, search brackets / mids / per-warp counts
     g.total = off;
@@ -128,7 +131,8 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     constexpr int T2 = T * T;
     constexpr int GP = T2 + 1;
     constexpr int CH = s6_ch<T>();
-    constexpr int NSUB = T / CH;             // sub-chunks per ring period
+    constexpr int P = s6_period<T>();        // stream rows per unrolled period
+    constexpr int NSUB = P / CH;             // sub-chunks per period
     constexpr int WPP = s6_elem(W + 2 * R) + 1;
     constexpr uint32_t FULL = 0xffffffffu;
     extern __shared__ __align__(16) uint8_t sm[];
@@ -156,13 +160,13 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int c_begin = cgi * g.cpg, c_end = min(g.C, c_begin + g.cpg);
     float* const part = partial + ((int64_t)img * g.groups + cgi) * hw;
     uint32_t* const scr = scratch + (size_t)smid6() * (size_t)(h + 1) * 4 * W;
-    const int n_chunks = (g.S + T - 1) / T;
+    const int n_chunks = (g.S + P - 1) / P;
 
     // ---- per-CTA tables
     for (int p = tid; p < W + 2 * R; p += S6_THREADS) xmap[p] = map_coord(p - R, W, g.pad);
     // stream rows past the plane read row h of the scratch: all-zero counts, so
     // E = 0 there without a branch
-    for (int s = tid; s < n_chunks * T + 2 * T; s += S6_THREADS)
+    for (int s = tid; s < n_chunks * P + 2 * CH; s += S6_THREADS)
         rmap[s] = s < g.S ? map_coord(s - R, h, g.pad) : h;
     for (int e = tid; e < h; e += S6_THREADS)
         stab[e] = make_int2(map_coord(e + R, h, g.pad) * W, map_coord(e - 1 - R, h, g.pad) * W);
@@ -297,15 +301,6 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             sum.w += a.w - rr.w;
                             out[k] = sum;
                         }
-                        uint32_t* dst = scr + (size_t)y * 4 * W + x0;
-                        reinterpret_cast<uint4*>(dst)[0] = make_uint4(out[0].x, out[1].x, out[2].x, out[3].x);
-                        reinterpret_cast<uint4*>(dst)[1] = make_uint4(out[4].x, out[5].x, out[6].x, out[7].x);
-                        reinterpret_cast<uint4*>(dst + W)[0] = make_uint4(out[0].y, out[1].y, out[2].y, out[3].y);
-                        reinterpret_cast<uint4*>(dst + W)[1] = make_uint4(out[4].y, out[5].y, out[6].y, out[7].y);
-                        reinterpret_cast<uint4*>(dst + 2 * W)[0] = make_uint4(out[0].z, out[1].z, out[2].z, out[3].z);
-                        reinterpret_cast<uint4*>(dst + 2 * W)[1] = make_uint4(out[4].z, out[5].z, out[6].z, out[7].z);
-                        reinterpret_cast<uint4*>(dst + 3 * W)[0] = make_uint4(out[0].w, out[1].w, out[2].w, out[3].w);
-                        reinterpret_cast<uint4*>(dst + 3 * W)[1] = make_uint4(out[4].w, out[5].w, out[6].w, out[7].w);
                         if (g.fref) {
                             if (g.sshift >= 0) {  // power-of-two stride
                                 const int sm1 = (1 << g.sshift) - 1;
@@ -322,6 +317,15 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                                     if ((x0 + k) % g.stride == 0) sa[(x0 + k) / g.stride] = out[k];
                             }
                         }
+                        uint32_t* dst = scr + (size_t)y * 4 * W + x0;
+                        reinterpret_cast<uint4*>(dst)[0] = make_uint4(out[0].x, out[1].x, out[2].x, out[3].x);
+                        reinterpret_cast<uint4*>(dst)[1] = make_uint4(out[4].x, out[5].x, out[6].x, out[7].x);
+                        reinterpret_cast<uint4*>(dst + W)[0] = make_uint4(out[0].y, out[1].y, out[2].y, out[3].y);
+                        reinterpret_cast<uint4*>(dst + W)[1] = make_uint4(out[4].y, out[5].y, out[6].y, out[7].y);
+                        reinterpret_cast<uint4*>(dst + 2 * W)[0] = make_uint4(out[0].z, out[1].z, out[2].z, out[3].z);
+                        reinterpret_cast<uint4*>(dst + 2 * W)[1] = make_uint4(out[4].z, out[5].z, out[6].z, out[7].z);
+                        reinterpret_cast<uint4*>(dst + 3 * W)[0] = make_uint4(out[0].w, out[1].w, out[2].w, out[3].w);
+                        reinterpret_cast<uint4*>(dst + 3 * W)[1] = make_uint4(out[4].w, out[5].w, out[6].w, out[7].w);
                     }
                 }
                 __syncthreads();
@@ -442,7 +446,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         if (sub_ < n_sub) {                                                     \
             uint32_t* const dst_ = cring + (sub_ % 3) * SLOT;                   \
             _Pragma("unroll") for (int k_ = 0; k_ < NCP; ++k_) {                \
-                const int task_ = tid + S6_THREADS * k_;                        \
+                const int task_ = (S6_THREADS - 1 - tid) + S6_THREADS * k_;     \
                 if (task_ < CH * 128) {                                         \
                     const int rr_ = task_ >> 7, pc_ = 4 * (task_ & 127);        \
                     const int row_ = rmap[sub_ * CH + rr_];                     \
@@ -503,37 +507,56 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     S6_COPY(u + 2)
                     const uint32_t* const cs = cring + (u % 3) * SLOT + grp * W + x;
                     float* const vbw = Vb + (size_t)((u & 1) * CH) * 16 * W;
-                    // ---- E for CH stream rows (rows past the plane read zero counts)
+                    // ---- E for CH stream rows (rows past the plane read zero counts):
+                    // all rows' count words first, one warp vote per sub-chunk, then
+                    // the CH x 4 transports as independent instruction streams
+                    uint32_t word[CH], prev[CH];
+                    bool mass[CH];
+                    bool any = false;
 #pragma unroll
                     for (int rr = 0; rr < CH; ++rr) {
-                        const int rho = sc * CH + rr;  // static ring slot
-                        const int s = u * CH + rr;
-                        float E[4] = {0.f, 0.f, 0.f, 0.f};
-                        const uint32_t word = cs[rr * 4 * W];
-                        const uint32_t prev = g1 ? cs[rr * 4 * W - W] : 0u;
-                        const bool mass = (word >> 24) != (prev >> 24);  // any mass in the group
-                        if (__any_sync(FULL, mass)) {
-                            uint32_t ma = __byte_perm(prev, 0x4B000000u, 0x7653);
+                        word[rr] = cs[rr * 4 * W];
+                        prev[rr] = g1 ? cs[rr * 4 * W - W] : 0u;
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < CH; ++rr) {
+                        mass[rr] = (word[rr] >> 24) != (prev[rr] >> 24);  // mass in the group
+                        any |= mass[rr];
+                    }
+                    float E[CH][4];
+#pragma unroll
+                    for (int rr = 0; rr < CH; ++rr)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) E[rr][j] = 0.f;
+                    if (__any_sync(FULL, any)) {
+#pragma unroll
+                        for (int rr = 0; rr < CH; ++rr) {
+                            uint32_t ma = __byte_perm(prev[rr], 0x4B000000u, 0x7653);
                             uint32_t aa = gaddr + 4u * ma;
 #define S6_E(J)                                                                 \
     {                                                                           \
-        const uint32_t mb = __byte_perm(word, 0x4B000000u, 0x7650 + J);         \
+        const uint32_t mb = __byte_perm(word[rr], 0x4B000000u, 0x7650 + J);     \
         const uint32_t ab = gaddr + 4u * mb;                                    \
         const float gb = lds6_f32<J * GP * 4>(ab);                              \
         const float ga = lds6_f32<J * GP * 4>(aa);                              \
         const float pc = __uint_as_float(mb) - __uint_as_float(ma);             \
-        E[J] = (gb - ga) * rcp_approx6(fmaxf(pc, 1.f));                         \
+        E[rr][J] = (gb - ga) * rcp_approx6(fmaxf(pc, 1.f));                     \
         ma = mb;                                                                \
         aa = ab;                                                                \
     }
                             S6_E(0) S6_E(1) S6_E(2) S6_E(3)
 #undef S6_E
                         }
-                        mring[rho] = mass;
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < CH; ++rr) {
+                        const int rho = (sc * CH + rr) % T;  // static ring slot
+                        const int s = u * CH + rr;
+                        mring[rho] = mass[rr];
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
-                            vs[j] += E[j] - ring[rho][j];
-                            ring[rho][j] = E[j];
+                            vs[j] += E[rr][j] - ring[rho][j];
+                            ring[rho][j] = E[rr][j];
                         }
                         if (rho == T - 1) {
 #pragma unroll

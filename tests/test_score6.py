@@ -37,7 +37,8 @@ def _partials(ver, bins, lo, hi, V, images, C, h, n, t, pad, groups):
     (2, 12, 128, 16, 9, 1, False), (1, 8, 128, 16, 9, 2, False), (2, 6, 128, 16, 3, 1, False),
     (1, 5, 128, 16, 5, 2, False), (1, 7, 128, 8, 1, 1, False), (1, 6, 256, 16, 9, 1, False),
     (1, 5, 128, 16, 5, 1, True), (2, 6, 128, 12, 9, 1, True), (1, 4, 40, 16, 9, 1, False),
-    (1, 6, 19, 5, 3, 2, False), (1, 4, 130, 2, 9, 1, False)])
+    (1, 6, 19, 5, 3, 2, False), (1, 4, 130, 2, 9, 1, False), (1, 5, 128, 16, 7, 1, False),
+    (1, 5, 128, 16, 11, 2, False), (1, 4, 64, 16, 13, 1, True), (1, 4, 128, 16, 1, 1, False)])
 def test_score6_bit_identical_to_score3(images, C, h, n, t, pad, ext):
     import torch
     import paper_2510_15602_b200 as Q
@@ -61,7 +62,7 @@ def test_score6_bit_identical_to_score3(images, C, h, n, t, pad, ext):
     np.testing.assert_array_equal(p6, p3)
 
 
-@pytest.mark.parametrize("t,pad", [(15, "reflect"), (5, "wrap")])
+@pytest.mark.parametrize("t,pad", [(15, "reflect"), (13, "reflect"), (5, "wrap")])
 def test_score6_vs_oracle_where_v3_cannot(t, pad):
     """T = 15 on 128-wide planes: v3's row buffers do not fit shared memory, v6
     runs it (the reference comes from K3); the map matches the oracle."""
