@@ -313,9 +313,10 @@ int64_t qfca_score_scratch_bytes(int32_t h, int32_t w, int32_t n_bins, int32_t p
 int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
                        int32_t channels, int64_t images, int32_t pad, int32_t sample_budget,
                        int32_t with_reference) {
+    // the choice qfca_detect makes (its workspace carries the v6 scratch)
     const ScoreChoice ch = score_choose(h, w, n_bins, patch_size, channels, images, 0,
                                         n_bins <= 256 ? 1 : 2, pad, sample_budget,
-                                        with_reference ? 0 : 1);
+                                        with_reference ? 0 : 1, 1);
     if (ch.groups <= 0 || (!with_reference && !ch.fref)) return -1;
     return ch.ver;
 }

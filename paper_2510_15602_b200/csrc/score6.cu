@@ -335,7 +335,10 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         // ======== phase 2: reference (smallest v with #{samples: A_i <= v} >= S - m)
         if (g.fref) {
             constexpr int ROUNDS = T2 < 2 ? 1 : (T2 < 4 ? 2 : (T2 < 8 ? 3 : (T2 < 16 ? 4 :
-                                   (T2 < 32 ? 5 : (T2 < 64 ? 6 : 7)))));
+                                   (T2 < 32 ? 5 : (T2 < 64 ? 6 : (T2 < 128 ? 7 : 8))))));
+            // counts <= 127: four 8-bit compares per word; up to 255 (T = 13, 15):
+            // the word's lanes widened to two words of 16-bit lanes
+            constexpr bool WIDE = T2 > 126;
             constexpr int WPS = S6_THREADS / 32;
             const int c0 = g.nsamp - (g.nsamp - 1) / 2;
             if (tid < 16) {
@@ -349,20 +352,32 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll 1
             for (int r = 0; r < ROUNDS; ++r) {
                 uint32_t Q[4], acc[4] = {0u, 0u, 0u, 0u};
+                uint32_t QE[4], QO[4], ace[4] = {0u, 0u, 0u, 0u}, aco[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq) Q[qq] = 0x80808080u | qm[qq];
+                for (int qq = 0; qq < 4; ++qq) {
+                    Q[qq] = 0x80808080u | qm[qq];
+                    QE[qq] = 0x80008000u | (qm[qq] & 0x00FF00FFu);
+                    QO[qq] = 0x80008000u | ((qm[qq] >> 8) & 0x00FF00FFu);
+                }
                 for (int s = tid; s < g.nsamp; s += S6_THREADS) {
                     const uint4 v = SA4[s];
-                    acc[0] += __umulhi((Q[0] - v.x) & 0x80808080u, 1u << 25);
-                    acc[1] += __umulhi((Q[1] - v.y) & 0x80808080u, 1u << 25);
-                    acc[2] += __umulhi((Q[2] - v.z) & 0x80808080u, 1u << 25);
-                    acc[3] += __umulhi((Q[3] - v.w) & 0x80808080u, 1u << 25);
+                    const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        if (WIDE) {  // 16-bit lanes (even / odd bytes), counts <= 255
+                            ace[qq] += ((QE[qq] - (vw[qq] & 0x00FF00FFu)) & 0x80008000u) >> 15;
+                            aco[qq] += ((QO[qq] - ((vw[qq] >> 8) & 0x00FF00FFu)) & 0x80008000u) >> 15;
+                        } else {
+                            acc[qq] += __umulhi((Q[qq] - vw[qq]) & 0x80808080u, 1u << 25);
+                        }
+                    }
                 }
                 uint32_t* cp = cnt + (tid >> 5) * 8;
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
-                    const uint32_t ev = __reduce_add_sync(FULL, acc[qq] & 0x00FF00FFu);
-                    const uint32_t od = __reduce_add_sync(FULL, (acc[qq] >> 8) & 0x00FF00FFu);
+                    const uint32_t ev = __reduce_add_sync(FULL, WIDE ? ace[qq] : acc[qq] & 0x00FF00FFu);
+                    const uint32_t od =
+                        __reduce_add_sync(FULL, WIDE ? aco[qq] : (acc[qq] >> 8) & 0x00FF00FFu);
                     if ((tid & 31) == 0) {
                         cp[2 * qq] = ev;
                         cp[2 * qq + 1] = od;
@@ -652,7 +667,7 @@ static int score6_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.qrows = (h + 3) / 4;
     g.moff = 0u - 4u * 0x4B000000u;
     if (!has_ref) {
-        if (t * t > 126 || budget < 1) return QFCA_ERR_UNSUPPORTED;
+        if (t * t > 255 || budget < 1) return QFCA_ERR_UNSUPPORTED;
         g.fref = 1;
         g.stride = sample_stride(h, w, budget);
         g.sshift = -1;

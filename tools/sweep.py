@@ -50,7 +50,7 @@ def run(n, t):
 
 res = {"workload": f"QFCA, {b} x 1024^2 textures, WRN50-2 random-init 512 x 128^2",
        "forced_kernel": a.force,
-       "patch_sweep": [run(16, t) for t in (3, 5, 9, 17, 33, 65)],
+       "patch_sweep": [run(16, t) for t in (3, 5, 7, 9, 11, 13, 15, 17, 33, 65)],
        "bin_sweep": [run(n, 9) for n in (8, 16, 32, 64, 128, 256)]}
 base_t = res["patch_sweep"][0]["ms_per_image"]
 base_n = res["bin_sweep"][0]["ms_per_image"]
