@@ -14,7 +14,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqfca_b200.so")
+# QFCA_B200_LIB: an alternative build of the same library (A/B timing of kernels)
+LIB_PATH = os.environ.get("QFCA_B200_LIB") or os.path.join(_HERE, "libqfca_b200.so")
 
 QFCA_OK, QFCA_ERR_ARG, QFCA_ERR_CUDA, QFCA_ERR_UNSUPPORTED = 0, 1, 2, 3
 PAD_CODES = {"zero": 0, "reflect": 1, "wrap": 2}  # scoring.py:155

@@ -245,34 +245,34 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         {
             uint4 cst = make_uint4(0, 0, 0, 0);
             const uint8_t* const pb = sb + col;
+            if (hy0 < hy1) {  // window sum of row hy0 - 1: the slide starts there
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) {
+                    const uint4 a = TH[pb[map_coord(hy0 - 1 + dy, h, g.pad) * W]];
+                    cst.x += a.x;
+                    cst.y += a.y;
+                    cst.z += a.z;
+                    cst.w += a.w;
+                }
+            }
             for (int kb = 0; kb < g.qrows; kb += S6_BAND) {
                 // H1: S6_BAND rows of this quarter -> staging slots q1 * 8 + kk
-#pragma unroll 1
+                // (cst enters as the window sum of row hy0 + kb - 1)
+#pragma unroll
                 for (int kk = 0; kk < S6_BAND; ++kk) {
                     const int y = hy0 + kb + kk;
-                    if (y >= hy1) break;
-                    if (y == hy0) {
-                        cst = make_uint4(0, 0, 0, 0);
-#pragma unroll
-                        for (int dy = -R; dy <= R; ++dy) {
-                            const uint4 a = TH[pb[map_coord(y + dy, h, g.pad) * W]];
-                            cst.x += a.x;
-                            cst.y += a.y;
-                            cst.z += a.z;
-                            cst.w += a.w;
-                        }
-                    } else {
+                    if (y < hy1) {
                         const int2 st = stab[y];
                         const uint4 a = TH[pb[st.x]], r = TH[pb[st.y]];
                         cst.x += a.x - r.x;
                         cst.y += a.y - r.y;
                         cst.z += a.z - r.z;
                         cst.w += a.w - r.w;
+                        uint4* row = STG + (q1 * S6_BAND + kk) * WPP;
+                        row[s6_elem(col + R)] = cst;
+                        if (halo0 >= 0) row[s6_elem(halo0)] = cst;
+                        if (halo1 >= 0) row[s6_elem(halo1)] = cst;
                     }
-                    uint4* row = STG + (q1 * S6_BAND + kk) * WPP;
-                    row[s6_elem(col + R)] = cst;
-                    if (halo0 >= 0) row[s6_elem(halo0)] = cst;
-                    if (halo1 >= 0) row[s6_elem(halo1)] = cst;
                 }
                 __syncthreads();
                 // H2: task (slot, 8-column segment) -> 8 cumulative counts
@@ -490,6 +490,8 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             // own-bin box rows of a sub-chunk: row a * 4 + ((grp + 3) & 3), so bin
             // group 0 (mass in nearly every window, the longest E) boxes last
             const int arow0 = (grp + 3) & 3;
+            // the warps of columns 0-31 and 96-127 hold the 2R edge columns (R <= 7)
+            const bool edge_warp = x < 32 || x >= W - 32;
             constexpr int NA = (CH + 3) / 4;
             float pold[NA];  // partial-map values of the rows boxed next
 #pragma unroll
@@ -504,12 +506,18 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     const int bb = sb[y * W + x];
                     const float* vb = vbr + (rr * 16 + bb) * W;
                     float f = 0.f;
-                    if (x >= R && x + R < W) {
+                    if (!edge_warp) {  // warp-uniform: the middle 64 columns
 #pragma unroll
                         for (int d = -R; d <= R; ++d) f += vb[x + d];
+                    } else if (g.pad == QFCA_PAD_REFLECT) {
+#pragma unroll
+                        for (int d = -R; d <= R; ++d) {  // one reflection (R < W)
+                            const int p = abs(x + d);
+                            f += vb[(W - 1) - abs((W - 1) - p)];
+                        }
                     } else {
 #pragma unroll
-                        for (int d = 0; d < T; ++d) f += vb[xmap[x + d]];
+                        for (int d = -R; d <= R; ++d) f += vb[(x + d + W) & (W - 1)];
                     }
                     const float old = last ? part[y * W + x] : pv[a];
                     part[y * W + x] = old + fmaf(f, scale, 0.f);
