@@ -91,6 +91,7 @@ class ClockSampler:
                      "--format=csv,noheader,nounits", "-lms",
                      os.environ.get("QFCA_BENCH_SMI_MS", "200")],
                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self._live = True  # samples from just before the region count too
                 self._thr = threading.Thread(target=self._run, daemon=True)
                 self._thr.start()
                 time.sleep(0.3)  # let the first sample land before the timed region

@@ -38,6 +38,7 @@ extern "C" {
 #define QFCA_ERR_UNSUPPORTED 3
 
 #define QFCA_REF_MEDIAN_QUAN 0 /* quantize.py:174-183 (default) */
+#define QFCA_REF_MEAN_QUAN 1   /* quantize.py:174-183 (per-rank mean) */
 #define QFCA_REF_QUAN_MEDIAN 2 /* quantize.py:184-199 */
 #define QFCA_REF_QUAN_MEAN 3   /* quantize.py:184-199 */
 
@@ -76,6 +77,21 @@ int qfca_select_reference(const void* bins, int32_t bins_bytes, const float* lo,
                           int64_t planes, int32_t h, int32_t w, int32_t n_bins,
                           int32_t patch_size, int32_t pad, int32_t sample_budget, int32_t mode,
                           int32_t* stats, void* stream);
+
+/* select_reference (quantize.py:150-200) of any mode as the reference's fp64
+ * (planes, n_bins) weights, bit-identical: median-quan / quan-median / quan-mean
+ * from the bins (K3 statistics, then NumPy's arithmetic for the quan-* rescale);
+ * mean-quan from the float32 values (sample patches, per-patch sort, per-rank
+ * fp64 mean in sample order, binned).  mode: QFCA_REF_*.  Degenerate planes
+ * (hi <= lo) get [T^2, 0, ...]. */
+int64_t qfca_reference_weights_workspace_bytes(int64_t planes, int32_t h, int32_t w,
+                                               int32_t n_bins, int32_t patch_size,
+                                               int32_t sample_budget, int32_t mode);
+int qfca_reference_weights(const float* values, const void* bins, int32_t bins_bytes,
+                           const float* lo, const float* hi, int64_t planes, int32_t h, int32_t w,
+                           int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
+                           int32_t mode, void* workspace, int64_t workspace_bytes,
+                           double* weights, void* stream);
 
 /* patch_histograms (quantize.py:85-106): window counts (planes, n_bins, h, w),
  * counts_kind 0 = float32, 1 = uint16.  scratch: planes*n_bins*h*w uint16. */

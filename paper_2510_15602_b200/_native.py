@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("QFCA_B200_LIB") or os.path.join(_HERE, "libqfca_b200.
 
 QFCA_OK, QFCA_ERR_ARG, QFCA_ERR_CUDA, QFCA_ERR_UNSUPPORTED = 0, 1, 2, 3
 PAD_CODES = {"zero": 0, "reflect": 1, "wrap": 2}  # scoring.py:155
-REF_MODE_CODES = {"median-quan": 0, "quan-median": 2, "quan-mean": 3}
+REF_MODE_CODES = {"median-quan": 0, "mean-quan": 1, "quan-median": 2, "quan-mean": 3}
 
 _P, _I32, _I64, _F64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 
@@ -40,6 +40,10 @@ _SIGNATURES = {
     "qfca_sample_stride": ([_I32, _I32, _I32], _I32),
     "qfca_select_reference": ([_P, _I32, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32,
                                _I32, _P, _P], _I32),
+    "qfca_reference_weights_workspace_bytes": ([_I64, _I32, _I32, _I32, _I32, _I32, _I32],
+                                               _I64),
+    "qfca_reference_weights": ([_P, _P, _I32, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32,
+                                _I32, _P, _I64, _P, _P], _I32),
     "qfca_window_counts": ([_P, _I32, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P],
                            _I32),
     "qfca_mismatch_pixels": ([_P, _I64, _I64, _I32, _P, _P, _P, _P, _P], _I32),

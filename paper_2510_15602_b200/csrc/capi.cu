@@ -82,6 +82,10 @@ int launch_score5(const void*, int, const float*, const float*, const int32_t*, 
 int launch_score4(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, float*, cudaStream_t);
 int score6_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
+int64_t reference_weights_workspace_bytes(int64_t, int, int, int, int, int, int);
+int launch_reference_weights(const float*, const void*, int, const float*, const float*, int64_t,
+                             int, int, int, int, int, int, int, void*, int64_t, double*,
+                             cudaStream_t);
 int64_t score6_scratch_bytes(int);
 int launch_score6(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, void*, int64_t, float*, cudaStream_t);
@@ -453,6 +457,24 @@ int qfca_naive_box(const void* x, int32_t dtype, int64_t planes, int32_t h, int3
                    int32_t mode_rows, int32_t mode_cols, double* out, void* stream) {
     return counted(launch_naive_box(x, dtype, planes, h, w, k, mode_rows, mode_cols, out,
                                     S(stream)), 1);
+}
+
+int64_t qfca_reference_weights_workspace_bytes(int64_t planes, int32_t h, int32_t w,
+                                               int32_t n_bins, int32_t patch_size,
+                                               int32_t sample_budget, int32_t mode) {
+    return reference_weights_workspace_bytes(planes, h, w, n_bins, patch_size, sample_budget,
+                                             mode);
+}
+
+int qfca_reference_weights(const float* values, const void* bins, int32_t bins_bytes,
+                           const float* lo, const float* hi, int64_t planes, int32_t h, int32_t w,
+                           int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
+                           int32_t mode, void* workspace, int64_t workspace_bytes,
+                           double* weights, void* stream) {
+    return counted(launch_reference_weights(values, bins, bins_bytes, lo, hi, planes, h, w,
+                                            n_bins, patch_size, pad, sample_budget, mode,
+                                            workspace, workspace_bytes, weights, S(stream)),
+                   mode == QFCA_REF_MEAN_QUAN ? 4 : 2);
 }
 
 int qfca_gather_tiles(const void* bins, int32_t channels, int32_t h, int32_t w,

@@ -172,63 +172,25 @@ def patch_histograms(b: BinIndexMap, patch_size: int, pad: str = "reflect") -> H
     return HistogramField(counts=to_host(counts, is_torch(b.indices)), patch_size=patch_size)
 
 
-def _weights_from_stats(stats: np.ndarray, degen: np.ndarray, mode: str, t2: int,
-                        n_samples: int) -> np.ndarray:
-    """Reference weights from the kernel's integer statistics (quantize.py:168-199)."""
-    c, n = stats.shape
-    if mode == "median-quan":
-        v = stats.astype(np.int64)
-        return np.diff(np.concatenate([np.zeros((c, 1), np.int64), v], 1), axis=1).astype(
-            np.float64)
-    weights = np.zeros((c, n), np.float64)
-    for ch in range(c):
-        if degen[ch]:
-            weights[ch, 0] = t2
-            continue
-        if mode == "quan-median":
-            wv = stats[ch].astype(np.float64)
-        else:  # quan-mean: hists.mean(axis=0) of integer counts
-            wv = stats[ch].astype(np.float64) / n_samples
-        total = wv.sum()
-        weights[ch] = wv * (t2 / total) if total > 0 else 0.0
-        if total <= 0:
-            weights[ch, 0] = t2
-    return weights
-
-
-def _mean_quan_dev(x: torch.Tensor, lo64, hi64, degen, t: int, budget: int, pad: str):
-    """mean-quan (quantize.py:174-183): per-rank mean of the sorted sampled
-    patches, then binned.  Sorting on the GPU (torch.sort), fp64 mean."""
-    c, h, w = x.shape
-    r = t // 2
-    s = sample_stride(h, w, budget)
-    ys = torch.arange(0, h, s, device=x.device)
-    xs = torch.arange(0, w, s, device=x.device)
-    edge = pad == "reflect" and not (h > 1 and w > 1)
-
-    def idx(n, lim):
-        i = torch.arange(-r, n + r, device=x.device)
-        if pad == "wrap":
-            return torch.remainder(i, n), None
-        if pad == "zero":
-            return i.clamp(0, n - 1), (i >= 0) & (i < n)
-        if edge or n == 1:
-            return i.clamp(0, n - 1), None
-        while bool(((i < 0) | (i >= n)).any()):
-            i = torch.where(i < 0, -i, i)
-            i = torch.where(i >= n, 2 * n - 2 - i, i)
-        return i, None
-
-    yi, ym = idx(h, h)
-    xi, xm = idx(w, w)
-    padded = x[:, yi][:, :, xi]
-    if pad == "zero":
-        mask = ym[:, None] & xm[None, :]
-        padded = padded * mask.to(padded.dtype)
-    win = padded.unfold(1, t, 1).unfold(2, t, 1)  # (C, h, w, t, t)
-    pts = win[:, ys][:, :, xs].reshape(c, -1, t * t)
-    ranked = torch.sort(pts, dim=2).values
-    return ranked.to(torch.float64).mean(dim=1)  # (C, T^2)
+def reference_weights_dev(x: torch.Tensor, bins: torch.Tensor | None, lo: torch.Tensor,
+                          hi: torch.Tensor, planes: int, h: int, w: int, n_bins: int, t: int,
+                          pad: str, budget: int, mode: str) -> torch.Tensor:
+    """select_reference weights (planes, n_bins) fp64 of any mode on the device
+    (quantize.py:150-200; csrc/refmodes.cu), bit-identical to the reference.
+    mean-quan reads the float32 values x, the other modes the bins."""
+    L = N.lib()
+    code = N.REF_MODE_CODES[mode]
+    nbytes = L.qfca_reference_weights_workspace_bytes(planes, h, w, n_bins, t, budget, code)
+    if nbytes < 0:
+        raise ValueError("unsupported reference configuration")
+    ws = empty((max(int(nbytes), 1),), torch.uint8)
+    out = empty((planes, n_bins), torch.float64)
+    N.call("qfca_reference_weights", x.data_ptr() if x is not None else None,
+           bins.data_ptr() if bins is not None else None,
+           bins.element_size() if bins is not None else 1, lo.data_ptr(), hi.data_ptr(), planes,
+           h, w, n_bins, t, N.PAD_CODES[pad], budget, code, ws.data_ptr(), nbytes,
+           out.data_ptr(), N.stream())
+    return out
 
 
 def select_reference(values, q: Quantizer, patch_size: int, mode: str = "median-quan",
@@ -244,28 +206,9 @@ def select_reference(values, q: Quantizer, patch_size: int, mode: str = "median-
         raise ValueError(f"unknown pad mode {pad!r}")
     x = to_dev(values)
     c, h, w = x.shape
-    t2 = patch_size * patch_size
     lo, hi = _qtensors(q)
-    degen = np.asarray(q.degenerate.cpu() if is_torch(q.degenerate) else q.degenerate, bool)
-    if mode == "mean-quan":
-        ref = _mean_quan_dev(x, lo, hi, degen, patch_size, sample_budget, pad).cpu().numpy()
-        weights = np.zeros((c, q.n_bins), np.float64)
-        lo_h = np.asarray(q.lo.cpu() if is_torch(q.lo) else q.lo, np.float64)
-        hi_h = np.asarray(q.hi.cpu() if is_torch(q.hi) else q.hi, np.float64)
-        for ch in range(c):
-            if degen[ch]:
-                weights[ch, 0] = t2
-                continue
-            span = hi_h[ch] - lo_h[ch] if hi_h[ch] > lo_h[ch] else 1.0
-            idx = np.clip(np.floor((ref[ch] - lo_h[ch]) * q.n_bins / span), 0, q.n_bins - 1)
-            weights[ch] = np.bincount(idx.astype(np.int64), minlength=q.n_bins)
-    else:
-        b = bins_dev(x, lo, hi, c, h * w, q.n_bins)
-        stats = reference_stats_dev(b, lo, hi, c, h, w, q.n_bins, patch_size, pad,
-                                    sample_budget, mode).cpu().numpy()
-        s = sample_stride(h, w, sample_budget)
-        n_samples = ((h + s - 1) // s) * ((w + s - 1) // s)
-        weights = _weights_from_stats(stats, degen, mode, t2, n_samples)
-    if is_torch(values):
-        weights = torch.from_numpy(weights).to(x.device)
+    b = None if mode == "mean-quan" else bins_dev(x, lo, hi, c, h * w, q.n_bins)
+    weights = reference_weights_dev(x, b, lo, hi, c, h, w, q.n_bins, patch_size, pad,
+                                    sample_budget, mode)
+    weights = to_host(weights, is_torch(values))
     return ReferenceHistogram(weights=weights, patch_size=patch_size)

@@ -30,8 +30,8 @@ from ._dev import empty, is_torch, to_dev, to_host, zeros
 from .features import (FeatureMap, _gauss_kernel, gaussian_blur, pca_fit_batch,
                        pca_residual_batch, sep_convolve_dev)
 from .quantize import (BinIndexMap, HistogramField, Quantizer, ReferenceHistogram,
-                       _mean_quan_dev, _weights_from_stats, bins_dev, bins_dtype, minmax_dev,
-                       reference_stats_dev, sample_stride, window_counts_dev)
+                       bins_dev, bins_dtype, minmax_dev, reference_weights_dev, sample_stride,
+                       window_counts_dev)
 
 __all__ = ["PipelineConfig", "AnomalyMap", "DetectResult", "detect", "detect_batch",
            "bin_error_maps", "channel_error_maps", "associate_errors", "aggregate_channels",
@@ -172,35 +172,8 @@ def _smooth_taps(cfg: PipelineConfig):
 def _reference_weights_dev(x, bins, lo, hi, degen, cfg: PipelineConfig) -> torch.Tensor:
     """select_reference (quantize.py:150-200) weights (planes, N) fp64 on the device."""
     b, c, h, w = x.shape
-    planes = b * c
-    n, t = cfg.n_bins, cfg.patch_size
-    if cfg.reference_mode == "median-quan":
-        v = reference_stats_dev(bins, lo, hi, planes, h, w, n, t, cfg.pad, cfg.sample_budget,
-                                cfg.reference_mode).to(torch.float64)
-        refw = torch.diff(v, dim=1, prepend=torch.zeros_like(v[:, :1]))
-    elif cfg.reference_mode == "mean-quan":
-        ws = []
-        for i in range(b):
-            xi = x[i]
-            ref = _mean_quan_dev(xi, None, None, None, t, cfg.sample_budget, cfg.pad)
-            lo64, hi64 = lo[i * c:(i + 1) * c].double(), hi[i * c:(i + 1) * c].double()
-            span = torch.where(hi64 > lo64, hi64 - lo64, torch.ones_like(lo64))
-            idx = torch.clamp(torch.floor((ref - lo64[:, None]) * n / span[:, None]), 0, n - 1)
-            wgt = torch.zeros((c, n), dtype=torch.float64, device=x.device)
-            wgt.scatter_add_(1, idx.long(), torch.ones_like(idx))
-            dg = degen[i * c:(i + 1) * c]
-            wgt[dg] = 0.0
-            wgt[dg, 0] = t * t
-            ws.append(wgt)
-        refw = torch.cat(ws)
-    else:
-        stats = reference_stats_dev(bins, lo, hi, planes, h, w, n, t, cfg.pad,
-                                    cfg.sample_budget, cfg.reference_mode).cpu().numpy()
-        st = sample_stride(h, w, cfg.sample_budget)
-        ns = ((h + st - 1) // st) * ((w + st - 1) // st)
-        refw = torch.from_numpy(_weights_from_stats(stats, degen.cpu().numpy(),
-                                                    cfg.reference_mode, t * t, ns)).to(x.device)
-    return refw
+    return reference_weights_dev(x.reshape(b * c, h, w), bins, lo, hi, b * c, h, w, cfg.n_bins,
+                                 cfg.patch_size, cfg.pad, cfg.sample_budget, cfg.reference_mode)
 
 
 def _general_partial(x: torch.Tensor, cfg: PipelineConfig, events=None):

@@ -126,6 +126,7 @@ def small_cases():
                       with_counts=False))
     save("sigma_p_2", run_case(v, dict(n_bins=8, patch_size=5, sigma_p=2.0),
                                with_counts=False))
+    extra_mode_cases()
     # T and N sweeps on one medium map
     v = smooth_random_map(np.random.default_rng(12), 4, 40, 40)
     for t in (3, 5, 9, 17, 33, 65):
@@ -134,6 +135,26 @@ def small_cases():
     for n in (8, 64, 256):
         save(f"sweep_n{n}", run_case(v, dict(n_bins=n, patch_size=9),
                                      with_counts=False))
+
+
+def extra_mode_cases():
+    """The other reference modes beyond the defaults: zero / wrap padding, sparse
+    sample grids, N above 8 and 128 (NumPy's pairwise-sum branches in the quan-*
+    rescale), patches of more than 128 values (mean-quan's segmented sort)."""
+    rng = np.random.default_rng(21)
+    v = np.maximum(smooth_random_map(rng, 3, 33, 37) + 0.2, 0).astype(np.float32)
+    save("mode_mean_quan_zero", run_case(v, dict(n_bins=16, patch_size=9, pad="zero",
+                                                 reference_mode="mean-quan", sample_budget=200),
+                                         with_counts=False))
+    save("mode_mean_quan_t17", run_case(v, dict(n_bins=16, patch_size=17,
+                                                reference_mode="mean-quan", sample_budget=300),
+                                        with_counts=False))
+    save("mode_quan_mean_wrap_n32", run_case(v, dict(n_bins=32, patch_size=7, pad="wrap",
+                                                     reference_mode="quan-mean"),
+                                             with_counts=False))
+    save("mode_quan_median_n200", run_case(v, dict(n_bins=200, patch_size=3,
+                                                   reference_mode="quan-median"),
+                                           with_counts=False))
 
 
 def transport_cases():
