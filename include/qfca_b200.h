@@ -207,6 +207,14 @@ int qfca_center(const float* x, int64_t planes, int64_t plane_len, const double*
 int qfca_pca_residual(const float* x, int64_t images, int32_t channels, int64_t hw,
                       const double* mean, const double* comps, int32_t k,
                       int32_t per_image_model, float* out, void* stream);
+/* pca_residual of the channel slice [c_lo, c_hi) only -> out (images, c_hi - c_lo,
+ * hw): z = V (x - mu) still contracts all channels (a channel-sharded rank's
+ * residual, sharding.detect_pca_sharded).  QFCA_ERR_UNSUPPORTED unless C % 8 == 0,
+ * C >= 16, hw % 4 == 0 (the fp64 tensor-core kernel). */
+int qfca_pca_residual_slice(const float* x, int64_t images, int32_t channels, int64_t hw,
+                            const double* mean, const double* comps, int32_t k,
+                            int32_t per_image_model, int32_t c_lo, int32_t c_hi, float* out,
+                            void* stream);
 
 /* Cholesky QR of a batch of tall fp64 blocks (batch, rows, cols) row-major,
  * in place: Y <- Y L^-T, L L^T = Y^T Y (re-orthonormalisation step of the

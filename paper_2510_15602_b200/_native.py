@@ -85,6 +85,8 @@ _SIGNATURES = {
     "qfca_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),
     "qfca_mean_covariance": ([_P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], _I32),
     "qfca_pca_residual": ([_P, _I64, _I32, _I64, _P, _P, _I32, _I32, _P, _P], _I32),
+    "qfca_pca_residual_slice": ([_P, _I64, _I32, _I64, _P, _P, _I32, _I32, _I32, _I32, _P, _P],
+                                _I32),
     "qfca_detect_workspace_bytes": ([_I64, _I32, _I32, _I32, ctypes.POINTER(QfcaConfig)], _I64),
     "qfca_detect": ([_P, _I64, _I32, _I32, _I32, ctypes.POINTER(QfcaConfig), _P, _I64, _P, _P,
                      _P, _P, _P], _I32),

@@ -83,6 +83,8 @@ int launch_score4(const void*, int, const float*, const float*, const int32_t*, 
                   int, int, int, int, int, int, float*, cudaStream_t);
 int score6_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int64_t reference_weights_workspace_bytes(int64_t, int, int, int, int, int, int);
+int launch_pca_residual_slice(const float*, int64_t, int, int64_t, const double*, const double*,
+                              int, int, int, int, float*, cudaStream_t);
 int launch_reference_weights(const float*, const void*, int, const float*, const float*, int64_t,
                              int, int, int, int, int, int, int, void*, int64_t, double*,
                              cudaStream_t);
@@ -457,6 +459,15 @@ int qfca_naive_box(const void* x, int32_t dtype, int64_t planes, int32_t h, int3
                    int32_t mode_rows, int32_t mode_cols, double* out, void* stream) {
     return counted(launch_naive_box(x, dtype, planes, h, w, k, mode_rows, mode_cols, out,
                                     S(stream)), 1);
+}
+
+int qfca_pca_residual_slice(const float* x, int64_t images, int32_t channels, int64_t hw,
+                            const double* mean, const double* comps, int32_t k,
+                            int32_t per_image_model, int32_t c_lo, int32_t c_hi, float* out,
+                            void* stream) {
+    return counted(launch_pca_residual_slice(x, images, channels, hw, mean, comps, k,
+                                             per_image_model, c_lo, c_hi, out, S(stream)),
+                   1);
 }
 
 int64_t qfca_reference_weights_workspace_bytes(int64_t planes, int32_t h, int32_t w,

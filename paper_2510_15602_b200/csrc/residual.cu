@@ -178,7 +178,7 @@ template <int K>
 __global__ void __launch_bounds__(RS_THREADS, 1)
 k_pca_residual_dmma(const float* __restrict__ x, int C, int hw, const double* __restrict__ mean,
                     const double* __restrict__ comps, int per_image_model, int64_t items,
-                    int tiles_per_image, float* __restrict__ out) {
+                    int tiles_per_image, int c_lo, int c_hi, float* __restrict__ out) {
     constexpr int KK = (K + 3) & ~3;    // k-dim of r (multiple of 4), also V row length
     constexpr int KN = (K + 7) & ~7;    // n-dim of z (multiple of 8)
     constexpr int NZ = KN / 8;          // z n-tiles
@@ -265,10 +265,13 @@ k_pca_residual_dmma(const float* __restrict__ x, int C, int hw, const double* __
         }
         __syncthreads();
 
-        // ---- r = xc - V z^T: warp -> 16 output tiles (8 channels x 8 px)
+        // ---- r = xc - V z^T: warp -> output tiles (8 channels x 8 px) of the
+        //      channel slice [c_lo, c_hi) (every channel unless a rank's slice)
         const bool full = p0 + RS_TP <= hw;
-        for (int t = warp; t < (C / 8) * 4; t += NW) {
-            const int mt = t >> 2, nt = t & 3;
+        const int mt0 = c_lo >> 3, nmt = ((c_hi + 7) >> 3) - mt0;
+        const int cs = c_hi - c_lo;
+        for (int t = warp; t < nmt * 4; t += NW) {
+            const int mt = mt0 + (t >> 2), nt = t & 3;
             double d0 = 0.0, d1 = 0.0;
 #pragma unroll
             for (int kb = 0; kb < KK; kb += 4) {
@@ -281,7 +284,8 @@ k_pca_residual_dmma(const float* __restrict__ x, int C, int hw, const double* __
             const float2 xv = *reinterpret_cast<const float2*>(xs + c * RD_LDX + pp);
             const float r0 = (float)(((double)xv.x - mu) - d0);
             const float r1 = (float)(((double)xv.y - mu) - d1);
-            float* op = out + (img * (int64_t)C + c) * hw + p0 + pp;
+            if (c < c_lo || c >= c_hi) continue;
+            float* op = out + (img * (int64_t)cs + (c - c_lo)) * hw + p0 + pp;
             if (full) {
                 *reinterpret_cast<float2*>(op) = make_float2(r0, r1);
             } else {
@@ -301,7 +305,9 @@ size_t residual_dmma_smem(int C, int K) {
 
 template <int K>
 static int launch_dmma_k(const float* x, int64_t images, int C, int64_t hw, const double* mean,
-                         const double* comps, int per_image_model, float* out, cudaStream_t st) {
+                         const double* comps, int per_image_model, float* out, cudaStream_t st,
+                         int c_lo = 0, int c_hi = -1) {
+    if (c_hi < 0) c_hi = C;
     const size_t smem = residual_dmma_smem(C, K);
     if (smem > 227 * 1024 || hw % 4 != 0 || hw > (1 << 30) || C % 8 != 0 || C < 16)
         return QFCA_ERR_UNSUPPORTED;
@@ -315,8 +321,29 @@ static int launch_dmma_k(const float* x, int64_t images, int C, int64_t hw, cons
     const int64_t items = images * tpi;
     const int64_t grid = items < sms ? items : sms;
     k_pca_residual_dmma<K><<<(unsigned)grid, RS_THREADS, smem, st>>>(
-        x, C, (int)hw, mean, comps, per_image_model, items, tpi, out);
+        x, C, (int)hw, mean, comps, per_image_model, items, tpi, c_lo, c_hi, out);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+// the residual of channels [c_lo, c_hi) only (a channel-sharded rank's slice):
+// z = V (x - mu) still contracts every channel, the output is (images, c_hi -
+// c_lo, hw); the fp64 tensor-core kernel only
+int launch_pca_residual_slice(const float* x, int64_t images, int C, int64_t hw,
+                              const double* mean, const double* comps, int k,
+                              int per_image_model, int c_lo, int c_hi, float* out,
+                              cudaStream_t st) {
+    if (c_lo < 0 || c_hi > C || c_lo >= c_hi) return QFCA_ERR_ARG;
+    switch (k) {
+#define QFCA_RS_K(KK)                                                                     \
+    case KK:                                                                              \
+        return launch_dmma_k<KK>(x, images, C, hw, mean, comps, per_image_model, out, st, \
+                                 c_lo, c_hi);
+        QFCA_RS_K(1) QFCA_RS_K(2) QFCA_RS_K(3) QFCA_RS_K(4) QFCA_RS_K(5) QFCA_RS_K(6)
+        QFCA_RS_K(7) QFCA_RS_K(8) QFCA_RS_K(9) QFCA_RS_K(10) QFCA_RS_K(11) QFCA_RS_K(12)
+        QFCA_RS_K(13) QFCA_RS_K(14) QFCA_RS_K(15) QFCA_RS_K(16)
+#undef QFCA_RS_K
+    }
+    return QFCA_ERR_UNSUPPORTED;
 }
 
 int launch_pca_residual_tiled(const float* x, int64_t images, int C, int64_t hw,

@@ -356,6 +356,23 @@ def pca_residual_batch(x: torch.Tensor, mean: torch.Tensor, comps: torch.Tensor,
     return out
 
 
+def pca_residual_slice(x: torch.Tensor, mean: torch.Tensor, comps: torch.Tensor, c0: int,
+                       c1: int) -> torch.Tensor:
+    """Residual of channels [c0, c1) only, (B, c1 - c0, H, W): a channel-sharded
+    rank's slice (the projection still uses every channel)."""
+    b, c, h, w = x.shape
+    k = comps.shape[-2]
+    out = empty((b, c1 - c0, h, w), torch.float32)
+    per_image = 1 if mean.dim() == 2 else 0
+    rc = N.lib().qfca_pca_residual_slice(x.data_ptr(), b, c, h * w, mean.contiguous().data_ptr(),
+                                         comps.contiguous().data_ptr(), k, per_image, c0, c1,
+                                         out.data_ptr(), N.stream())
+    if rc == N.QFCA_ERR_UNSUPPORTED:  # shapes the tensor-core kernel does not take
+        return pca_residual_batch(x, mean, comps)[:, c0:c1].contiguous()
+    N.check(rc, "qfca_pca_residual_slice")
+    return out
+
+
 def pca_fit(f: FeatureMap, k: int) -> PcaModel:
     """features.py:157-180: top-k principal components of the pixel vectors."""
     c = f.n_channels

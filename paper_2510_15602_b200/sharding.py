@@ -364,7 +364,7 @@ def detect_pca_sharded(values: torch.Tensor, cfg=None, group=None):
     (C, h, w) stack on every rank.  Returns what detect_channel_sharded does."""
     import dataclasses
 
-    from .features import pca_residual_batch
+    from .features import pca_residual_slice
     from .scoring import PipelineConfig
     cfg = cfg or PipelineConfig()
     world, rank = _world(group)
@@ -372,8 +372,7 @@ def detect_pca_sharded(values: torch.Tensor, cfg=None, group=None):
     if cfg.pca_components > 0:
         mean, comps, _ = pca_fit_sharded(values, min(cfg.pca_components, c), group)
         c0, c1 = shard_range(c, world, rank)
-        resid = pca_residual_batch(values[None].contiguous(), mean[None], comps[None])[0]
-        local = resid[c0:c1].contiguous()
+        local = pca_residual_slice(values[None].contiguous(), mean[None], comps[None], c0, c1)[0]
     else:
         c0, c1 = shard_range(c, world, rank)
         local = values[c0:c1].contiguous()

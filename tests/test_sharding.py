@@ -205,3 +205,19 @@ def test_pca_sharded_gpu():
     assert np.abs(final.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
     assert abs(float(img) - img_ref) <= 1e-4 * np.abs(ref).max()
     assert not bool(degen)
+
+
+@pytest.mark.gpu
+def test_pca_residual_slice_matches_full():
+    """A rank's channel-sliced residual (qfca_pca_residual_slice) is the same
+    float32 values as the full residual's slice, for slices on and off the
+    8-channel tiles."""
+    import torch
+    from paper_2510_15602_b200 import features as F
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(np.maximum(rng.standard_normal((2, 64, 24, 20)), 0).astype(np.float32)).cuda()
+    mean, comps, _ = F.pca_fit_batch(x, 10)
+    full = F.pca_residual_batch(x, mean, comps)
+    for c0, c1 in ((0, 64), (0, 8), (8, 24), (5, 13), (21, 64), (63, 64)):
+        part = F.pca_residual_slice(x, mean, comps, c0, c1)
+        assert torch.equal(part, full[:, c0:c1]), (c0, c1)
