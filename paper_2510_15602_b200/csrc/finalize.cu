@@ -180,10 +180,67 @@ int launch_sep_conv(const double* in, int64_t images, int h, int w, int axis,
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
 }
 
+// large maps: each of `parts` CTAs per image takes a band of interior rows;
+// the band maxima are combined by a second kernel (max is order-free: exact)
+__global__ void k_image_score_part(const double* __restrict__ scores, int h, int w, int border,
+                                   int parts, double* __restrict__ part_max) {
+    const int64_t b = blockIdx.x / parts;
+    const int pi = blockIdx.x % parts;
+    const double* p = scores + b * (int64_t)h * w;
+    int bb = min(min(border, (h - 1) / 2), (w - 1) / 2);
+    if (bb < 0) bb = 0;
+    const int ih = h - 2 * bb, iw = w - 2 * bb;
+    const int y0 = bb + (int)((int64_t)pi * ih / parts), y1 = bb + (int)((int64_t)(pi + 1) * ih / parts);
+    double m = -INFINITY;
+    for (int y = y0; y < y1; ++y) {
+        const double* row = p + (int64_t)y * w + bb;
+        for (int x = threadIdx.x; x < iw; x += blockDim.x) m = fmax(m, row[x]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ double sh[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[warp] = m;
+    __syncthreads();
+    if (warp == 0) {
+        m = lane < (int)(blockDim.x >> 5) ? sh[lane] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) part_max[blockIdx.x] = m;
+    }
+}
+
+__global__ void k_image_score_combine(const double* __restrict__ part_max, int64_t images,
+                                      int parts, double* __restrict__ image_score) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= images) return;
+    double m = -INFINITY;
+    for (int k = 0; k < parts; ++k) m = fmax(m, part_max[b * parts + k]);
+    image_score[b] = m;
+}
+
 int launch_image_score(const double* scores, int64_t images, int h, int w, int border,
                        double* image_score, cudaStream_t st) {
     if (images <= 0 || h <= 0 || w <= 0) return QFCA_ERR_ARG;
-    // one CTA per image; large maps (an 8192^2 texture's 1024^2 map) get 1024 threads
+    if ((int64_t)h * w > 65536 && images < 148) {
+        // few large maps (an 8192^2 texture's 1024^2 map): split each over CTAs
+        int bb = min(min(border, (h - 1) / 2), (w - 1) / 2);
+        if (bb < 0) bb = 0;
+        const int ih = h - 2 * bb;
+        int parts = (int)((148 * 2 + images - 1) / images);
+        parts = parts > ih ? ih : (parts < 1 ? 1 : parts);
+        double* tmp = nullptr;
+        if (cudaMallocAsync(&tmp, (size_t)images * parts * sizeof(double), st) != cudaSuccess)
+            return QFCA_ERR_CUDA;
+        k_image_score_part<<<(unsigned)(images * parts), 256, 0, st>>>(scores, h, w, border,
+                                                                       parts, tmp);
+        k_image_score_combine<<<(unsigned)((images + 127) / 128), 128, 0, st>>>(tmp, images,
+                                                                                 parts, image_score);
+        const bool ok = cudaGetLastError() == cudaSuccess;
+        cudaFreeAsync(tmp, st);
+        return ok ? QFCA_OK : QFCA_ERR_CUDA;
+    }
+    // one CTA per image
     const int threads = (int64_t)h * w > 65536 ? 1024 : 256;
     k_image_score<<<(unsigned)images, threads, 0, st>>>(scores, h, w, border, image_score);
     return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;

@@ -34,7 +34,7 @@ __all__ = ["shard_range", "shard_batch", "combine_partials", "channel_partial",
            "detect_channel_sharded", "strips", "pca_fit_sharded", "detect_pca_sharded"]
 
 STRIP_W = 128  # widest plane of the fused kernels
-STRIP_H = 256  # tile height: the whole-tile bins + row tables stay in shared memory
+STRIP_H = 128  # tile height: 128 x 128 tiles keep the v6 count scratch L2-resident
 USE_STRIPS = True  # route wide planes through strips (False: whole-plane generic kernel)
 
 
