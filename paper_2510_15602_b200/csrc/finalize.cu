@@ -95,8 +95,8 @@ __global__ void k_image_score(const double* __restrict__ scores, int h, int w, i
 // shared memory, the row weights once per row, so each output costs four
 // loads and the six rounded products / three sums of the reference formula.
 constexpr int UP_THREADS = 256;
-constexpr int UP_ROWS = 8;
-constexpr int UP_CHUNK = 2048;  // output columns per CTA (shared weight table)
+constexpr int UP_ROWS = 32;
+constexpr int UP_CHUNK = 1024;  // output columns per CTA (shared weight table)
 
 __device__ __forceinline__ void up_coord(int o, int n, int on, int& i0, int& i1, double& f) {
     const double s = ((double)o + 0.5) * (double)n / (double)on - 0.5;
@@ -110,12 +110,16 @@ __global__ void __launch_bounds__(UP_THREADS)
 k_upsample(const double* __restrict__ in, int h, int w, int oh, int ow, int bands, int chunks,
            float* __restrict__ out) {
     __shared__ int sx0[UP_CHUNK], sx1[UP_CHUNK];
-    __shared__ double sfx[UP_CHUNK];
+    __shared__ double sfx[UP_CHUNK], sgx[UP_CHUNK];
+    __shared__ int sy0[UP_ROWS], sy1[UP_ROWS];
+    __shared__ double sfy[UP_ROWS], sgy[UP_ROWS];
     const int b = blockIdx.x / (bands * chunks);
     const int band = (blockIdx.x / chunks) % bands, cx0 = (blockIdx.x % chunks) * UP_CHUNK;
     const int cw = min(UP_CHUNK, ow - cx0);
+    const int oy0 = band * UP_ROWS, nrows = min(oh, oy0 + UP_ROWS) - oy0;
     const double* p = in + (int64_t)b * h * w;
     float* o = out + (int64_t)b * oh * ow + cx0;
+    // column and row weights once per CTA (fp64 divisions are the costly part)
     for (int i = threadIdx.x; i < cw; i += UP_THREADS) {
         int x0, x1;
         double fx;
@@ -123,26 +127,30 @@ k_upsample(const double* __restrict__ in, int h, int w, int oh, int ow, int band
         sx0[i] = x0;
         sx1[i] = x1;
         sfx[i] = fx;
+        sgx[i] = 1.0 - fx;
     }
-    __syncthreads();
-    const int oy1 = min(oh, (band + 1) * UP_ROWS);
-    for (int oy = band * UP_ROWS; oy < oy1; ++oy) {
+    for (int i = threadIdx.x; i < nrows; i += UP_THREADS) {
         int y0, y1;
         double fy;
-        up_coord(oy, h, oh, y0, y1, fy);
-        const double* r0 = p + (int64_t)y0 * w;
-        const double* r1 = p + (int64_t)y1 * w;
-        for (int ox = threadIdx.x; ox < cw; ox += UP_THREADS) {
-            const int x0 = sx0[ox], x1 = sx1[ox];
-            const double fx = sfx[ox];
-            // explicit rounding (no FMA contraction) to match NumPy bit for bit
-            const double top = __dadd_rn(__dmul_rn(__ldg(r0 + x0), 1.0 - fx),
-                                         __dmul_rn(__ldg(r0 + x1), fx));
-            const double bot = __dadd_rn(__dmul_rn(__ldg(r1 + x0), 1.0 - fx),
-                                         __dmul_rn(__ldg(r1 + x1), fx));
-            o[(int64_t)oy * ow + ox] = (float)__dadd_rn(__dmul_rn(top, 1.0 - fy),
-                                                        __dmul_rn(bot, fy));
-        }
+        up_coord(oy0 + i, h, oh, y0, y1, fy);
+        sy0[i] = y0;
+        sy1[i] = y1;
+        sfy[i] = fy;
+        sgy[i] = 1.0 - fy;
+    }
+    __syncthreads();
+    const int per = nrows * cw;
+    for (int e = threadIdx.x; e < per; e += UP_THREADS) {
+        const int r = e / cw, ox = e - r * cw;
+        const double* r0 = p + (int64_t)sy0[r] * w;
+        const double* r1 = p + (int64_t)sy1[r] * w;
+        const int x0 = sx0[ox], x1 = sx1[ox];
+        const double fx = sfx[ox], gx = sgx[ox];
+        // explicit rounding (no FMA contraction) to match NumPy bit for bit
+        const double top = __dadd_rn(__dmul_rn(__ldg(r0 + x0), gx), __dmul_rn(__ldg(r0 + x1), fx));
+        const double bot = __dadd_rn(__dmul_rn(__ldg(r1 + x0), gx), __dmul_rn(__ldg(r1 + x1), fx));
+        o[(int64_t)(oy0 + r) * ow + ox] =
+            (float)__dadd_rn(__dmul_rn(top, sgy[r]), __dmul_rn(bot, sfy[r]));
     }
 }
 

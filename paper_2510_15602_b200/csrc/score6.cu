@@ -45,6 +45,7 @@ constexpr int S6_BAND = 8;                 // H1 steps per band (x 4 quarters = 
 constexpr int S6_SLOTS = 4 * S6_BAND;      // staging rows
 constexpr int S6_SEG = 8;                  // H2 columns per task
 constexpr int S6_SMEM_MAX = 227 * 1024;
+constexpr int S6_MAXNB = 76;               // table bins of 5 passes (N <= 76)
 
 struct Score6Geom {
     int h, n_bins, pad, C, groups, cpg;
@@ -52,6 +53,7 @@ struct Score6Geom {
     int qrows;  // H1 rows per quarter, ceil(h / 4)
     int fref, stride, sshift, nsx, nsamp;  // sshift = log2(stride) or -1
     int dbsb;   // bins double-buffered (next channel prefetched)
+    int passes, nbt;  // bin passes (16 lanes each, 15 new bins after the first), table bins
     uint32_t moff;
     int o_sb, o_sa, o_stg, o_gt, o_th, o_xmap, o_rmap, o_stab, o_pj, o_misc, total;
 };
@@ -109,7 +111,7 @@ static void score6_layout(Score6Geom& g) {
     const long long vb = 2LL * CH * 16 * S6_W * 4;
     g.o_sa = take(sa > vb ? sa : vb);
     g.o_stg = take((long long)S6_SLOTS * wpp * 16);
-    g.o_gt = take((long long)16 * GP * 4);
+    g.o_gt = take((long long)g.nbt * GP * 4);
     g.o_pj = take((long long)GP * 4);
     g.o_th = take(256 * 16);
     g.o_xmap = take((long long)(S6_W + 2 * R) * 4);
@@ -121,7 +123,7 @@ static void score6_layout(Score6Geom& g) {
     g.total = off;
 }
 
-template <int T>
+template <int T, bool MP>  // MP: more than 16 bins (several bin passes)
 __global__ void __launch_bounds__(S6_THREADS, 1)
 k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
          const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score6Geom g,
@@ -147,11 +149,11 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     int* const rmap = reinterpret_cast<int*>(sm + g.o_rmap);
     int2* const stab = reinterpret_cast<int2*>(sm + g.o_stab);
     float* const sscale = reinterpret_cast<float*>(sm + g.o_misc);      // [1]
-    int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);         // [16]
-    int* const blo = reinterpret_cast<int*>(sm + g.o_misc + 80);        // [16]
-    int* const bhi = reinterpret_cast<int*>(sm + g.o_misc + 144);       // [16]
-    uint8_t* const qm8 = sm + g.o_misc + 208;                            // [16]
-    uint32_t* const cnt = reinterpret_cast<uint32_t*>(sm + g.o_misc + 256);  // [16 warps][8]
+    int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);         // [S6_MAXNB]
+    int* const blo = reinterpret_cast<int*>(sm + g.o_misc + 352);       // [16]
+    int* const bhi = reinterpret_cast<int*>(sm + g.o_misc + 416);       // [16]
+    uint8_t* const qm8 = sm + g.o_misc + 480;                            // [16]
+    uint32_t* const cnt = reinterpret_cast<uint32_t*>(sm + g.o_misc + 512);  // [16 warps][8]
 
     const int tid = threadIdx.x;
     const int h = g.h;
@@ -170,15 +172,16 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         rmap[s] = s < g.S ? map_coord(s - R, h, g.pad) : h;
     for (int e = tid; e < h; e += S6_THREADS)
         stab[e] = make_int2(map_coord(e + R, h, g.pad) * W, map_coord(e - 1 - R, h, g.pad) * W);
-    for (int b = tid; b < 256; b += S6_THREADS) {
-        uint32_t v[4];
+    if (!MP)
+        for (int b = tid; b < 256; b += S6_THREADS) {
+            uint32_t v[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
-            const int d = b - 4 * q;
-            v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+            for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
+                const int d = b - 4 * q;
+                v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+            }
+            TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
         }
-        TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
-    }
     for (int i = tid; i < 4 * W; i += S6_THREADS) scr[(size_t)h * 4 * W + i] = 0u;
     // bins of the first channel
     {
@@ -204,8 +207,22 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int t_q = t_slot >> 3, t_k = t_slot & 7;
     // phase-4 roles: thread (column x, bin group grp)
     const int x = tid & (W - 1), grp = tid >> 7;
-    const uint32_t gaddr =
-        (uint32_t)__cvta_generic_to_shared(GT + grp * 4 * GP) + g.moff;
+    // thermometer words of a pass whose 16 lanes count bins <= tb .. tb + 15:
+    // lane j of word q = [b <= tb + 4q + j]
+    auto build_th = [&](int tb) {
+        if (!MP) return;  // built once below
+        __syncthreads();  // the previous pass's readers are done
+        for (int b = tid; b < 256; b += S6_THREADS) {
+            uint32_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int d = b - tb - 4 * q;
+                v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+            }
+            TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
+        }
+        __syncthreads();
+    };
 
     int buf = 0;
     for (int c = c_begin; c < c_end; ++c) {
@@ -218,7 +235,9 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                              (double)T2);
             sscale[0] = sc;
         }
-        if (!g.fref && tid < 16) sV[tid] = tid < g.n_bins ? __ldg(Vref + plane * g.n_bins + tid) : T2;
+        if (!g.fref)
+            for (int i = tid; i < S6_MAXNB; i += S6_THREADS)
+                sV[i] = i < g.n_bins ? __ldg(Vref + plane * g.n_bins + i) : T2;
         cp_async_wait_all();
         __syncthreads();
         const float scale = sscale[0];
@@ -242,7 +261,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 cp_async16(sbase + (buf ^ 1) * hw + 16 * i, bins + (plane + 1) * hw + 16 * i);
 
         // ======== phase 1: window counts -> scratch (word-major rows) + SA4 samples
-        {
+        auto phase1 = [&](bool samples) {
             uint4 cst = make_uint4(0, 0, 0, 0);
             const uint8_t* const pb = sb + col;
             if (hy0 < hy1) {  // window sum of row hy0 - 1: the slide starts there
@@ -301,7 +320,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             sum.w += a.w - rr.w;
                             out[k] = sum;
                         }
-                        if (g.fref) {
+                        if (samples) {
                             if (g.sshift >= 0) {  // power-of-two stride
                                 const int sm1 = (1 << g.sshift) - 1;
                                 if ((y & sm1) == 0) {
@@ -330,10 +349,12 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
                 __syncthreads();
             }
-        }
+        };
 
         // ======== phase 2: reference (smallest v with #{samples: A_i <= v} >= S - m)
-        if (g.fref) {
+        // of the pass's bins tb + klo .. tb + 15 (lane 0 of a later pass is the
+        // previous pass's last threshold)
+        auto search = [&](int tb, int klo) {
             constexpr int ROUNDS = T2 < 2 ? 1 : (T2 < 4 ? 2 : (T2 < 8 ? 3 : (T2 < 16 ? 4 :
                                    (T2 < 32 ? 5 : (T2 < 64 ? 6 : (T2 < 128 ? 7 : 8))))));
             // counts <= 127: four 8-bit compares per word; up to 255 (T = 13, 15):
@@ -342,7 +363,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             constexpr int WPS = S6_THREADS / 32;
             const int c0 = g.nsamp - (g.nsamp - 1) / 2;
             if (tid < 16) {
-                const int top = tid < g.n_bins - 1 ? 0 : T2;
+                const int top = (tid >= klo && tb + tid < g.n_bins - 1) ? 0 : T2;
                 blo[tid] = top;
                 bhi[tid] = T2;
                 qm8[tid] = (uint8_t)((top + T2) >> 1);
@@ -399,9 +420,17 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
                 __syncthreads();
             }
-            if (tid < 16) sV[tid] = blo[tid];
+            if (tid >= klo && tid < 16) sV[tb + tid] = blo[tid];
             __syncthreads();
-        }
+        };
+
+        const int npass = MP ? g.passes : 1;
+        if (g.fref)
+            for (int p = 0; p < npass; ++p) {
+                build_th(15 * p);
+                phase1(true);
+                search(15 * p, p > 0 ? 1 : 0);
+            }
 
         // ======== phase 3: PJ = prefix of J, G_i(v) for every bin and count
         for (int qq = tid; qq < T2; qq += S6_THREADS) {
@@ -431,7 +460,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
         __syncthreads();
-        for (int idx = tid; idx < 16 * GP; idx += S6_THREADS) {
+        for (int idx = tid; idx < g.nbt * GP; idx += S6_THREADS) {
             const int i = idx / GP, v = idx - i * GP;
             float vm = 0.f, d = 0.f;
             if (i < g.n_bins) {
@@ -448,8 +477,11 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         // ======== phase 4: E (register ring) + own-bin box, one barrier per sub-chunk.
         // The count rows of sub-chunk u + 2 are copied (cp.async) from the scratch
         // into a 3-slot ring in the (now free) staging region while sub-chunk u
-        // runs; each slot is [row][word][x].
-        {
+        // runs; each slot is [row][word][x].  A pass scores the pixels whose bin
+        // is in [bin_lo, bin_hi]; its lanes are bins tb .. tb + 15.
+        auto phase4 = [&](int tb, int bin_lo, int bin_hi) {
+            const uint32_t gaddr =
+                (uint32_t)__cvta_generic_to_shared(GT + (tb + grp * 4) * GP) + g.moff;
             uint32_t* const cring = reinterpret_cast<uint32_t*>(STG);
             constexpr int SLOT = CH * 4 * W;  // uint32 per slot
             const int n_sub = n_chunks * NSUB;
@@ -504,7 +536,8 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     const int y = u * CH + rr - 2 * R;
                     if (rr >= CH || y < 0 || y >= h) continue;
                     const int bb = sb[y * W + x];
-                    const float* vb = vbr + (rr * 16 + bb) * W;
+                    if (MP && (bb < bin_lo || bb > bin_hi)) continue;  // another pass's pixel
+                    const float* vb = vbr + (rr * 16 + bb - (MP ? tb : 0)) * W;
                     float f = 0.f;
                     if (!edge_warp) {  // warp-uniform: the middle 64 columns
 #pragma unroll
@@ -614,8 +647,15 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
             }
             own_bin_box(n_sub - 1, pold, false);  // the last sub-chunk
-        }
+        };
 #undef S6_COPY
+        for (int p = npass - 1; p >= 0; --p) {
+            if (!(g.fref && p == npass - 1)) {  // else the last search pass left them
+                build_th(15 * p);
+                phase1(false);
+            }
+            phase4(15 * p, p == 0 ? 0 : 15 * p + 1, min(15 * p + 15, g.n_bins - 1));
+        }
         __syncthreads();
         if (g.dbsb) {
             buf ^= 1;
@@ -663,7 +703,7 @@ static int s6_total(Score6Geom& g) {
 
 static int score6_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
                        int pad, int budget, bool has_ref, Score6Geom* out, size_t* smem_out) {
-    if (w != S6_W || t < 1 || t > 15 || (t & 1) == 0 || n_bins < 1 || n_bins > 16)
+    if (w != S6_W || t < 1 || t > 15 || (t & 1) == 0 || n_bins < 1 || n_bins > 64)
         return QFCA_ERR_UNSUPPORTED;
     if (h < 1 || h > 256 || (h * w) % 16) return QFCA_ERR_UNSUPPORTED;
     if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
@@ -674,6 +714,9 @@ static int score6_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.S = h + 2 * (t / 2);
     g.qrows = (h + 3) / 4;
     g.moff = 0u - 4u * 0x4B000000u;
+    // pass p covers lanes 15p .. 15p + 15: bins 0..15, then 15 new bins per pass
+    g.passes = n_bins <= 16 ? 1 : 1 + (n_bins - 16 + 14) / 15;
+    g.nbt = 15 * (g.passes - 1) + 16;
     if (!has_ref) {
         if (t * t > 255 || budget < 1) return QFCA_ERR_UNSUPPORTED;
         g.fref = 1;
@@ -735,8 +778,9 @@ int launch_score6(const void* bins, int bins_bytes, const float* lo, const float
     if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
     void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score6Geom,
                  uint32_t*, float*) = nullptr;
+    const bool mp = g.passes > 1;
     switch (t) {
-#define S6K(TT) case TT: kern = k_score6<TT>; break;
+#define S6K(TT) case TT: kern = mp ? k_score6<TT, true> : k_score6<TT, false>; break;
         S6K(1) S6K(3) S6K(5) S6K(7) S6K(9) S6K(11) S6K(13) S6K(15)
 #undef S6K
         default: return QFCA_ERR_UNSUPPORTED;

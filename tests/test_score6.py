@@ -81,3 +81,26 @@ def test_score6_vs_oracle_where_v3_cannot(t, pad):
     ref, img, _ = O.detect(x[0], patch_size=t, pad=pad)
     got = res.scores[0].cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("n,t,pad", [(17, 9, "reflect"), (31, 9, "reflect"), (32, 9, "wrap"),
+                                     (46, 5, "reflect"), (64, 9, "reflect"), (64, 3, "wrap"),
+                                     (48, 11, "reflect")])
+def test_score6_bin_passes_vs_oracle(n, t, pad):
+    """N > 16 on v6: bins in passes of 16 thermometer lanes (15 new bins per
+    pass after the first); maps match the oracle, the detect path uses v6."""
+    import torch
+    import paper_2510_15602_b200 as Q
+    from paper_2510_15602_b200 import _native as N
+    from oracle import qfca_oracle as O
+    rng = np.random.default_rng(n * 10 + t)
+    x = np.maximum(rng.standard_normal((2, 5, 128, 128)) + 0.3, 0).astype(np.float32)
+    x[1, 2] = 0.25  # degenerate
+    cfg = Q.PipelineConfig(n_bins=n, patch_size=t, pad=pad)
+    L = N.lib()
+    assert L.qfca_score_version(128, 128, n, t, 5, 2, N.PAD_CODES[pad], 4096, 0) == 6
+    res = Q.detect_batch(torch.from_numpy(x).cuda(), cfg)
+    for i in range(2):
+        ref, img, _ = O.detect(x[i], n_bins=n, patch_size=t, pad=pad)
+        got = res.scores[i].cpu().numpy()
+        assert np.abs(got - ref).max() <= 1e-4 * np.abs(ref).max(), (n, t, pad, i)
