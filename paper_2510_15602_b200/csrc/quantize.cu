@@ -178,12 +178,16 @@ __global__ void __launch_bounds__(256)
 k_bin_table(const float* __restrict__ x, int64_t plane_len, int splits,
             const float* __restrict__ lo, const float* __restrict__ hi,
             const float* __restrict__ tau, int n_bins, BT* __restrict__ out) {
-    __shared__ float st[BT_MAXN + 1];
+    __shared__ float stp[BT_MAXN + 2];  // stp[k] = lower bound of bin k, +-inf sentinels
     // one CTA per plane (the setup is paid once), or per 1/splits of a large plane
     const int64_t plane = blockIdx.x / splits;
     const int part = blockIdx.x - (int)(plane * splits);
     const int nt = n_bins - 1;
-    for (int k = threadIdx.x; k < nt; k += blockDim.x) st[k] = tau[plane * nt + k];
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) stp[k + 1] = tau[plane * nt + k];
+    if (threadIdx.x == 0) {
+        stp[0] = -INFINITY;
+        stp[n_bins] = INFINITY;
+    }
     const float lf = lo[plane], hf = hi[plane];
     const float inv = hf > lf ? (float)((double)n_bins / ((double)hf - (double)lf)) : 0.f;
     const float top = (float)nt;
@@ -194,11 +198,12 @@ k_bin_table(const float* __restrict__ x, int64_t plane_len, int splits,
     const int64_t len = splits == 1 ? plane_len : max((int64_t)0, min(q4, plane_len - b0_));
     const float* p = x + plane * plane_len + b0_;
     BT* o = out + plane * plane_len + b0_;
-    // fp32 estimate, then exact fix-up against the thresholds (bin k starts at st[k-1])
+    // fp32 estimate (within one bin of the exact fp64 rule), then one branch-free
+    // correction each way against the thresholds (bin k starts at stp[k])
     auto bin = [&](float v) {
         int b = (int)fminf(fmaxf((v - lf) * inv, 0.f), top);  // NaN -> 0
-        while (b < nt && v >= st[b]) ++b;
-        while (b > 0 && v < st[b - 1]) --b;
+        b = min(b + ((v >= stp[b + 1]) ? 1 : 0), nt);  // (+inf input: stays at nt)
+        b -= (v < stp[b]) ? 1 : 0;
         return b;
     };
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(FQ_THREADS)
 k_quantize_plane(const float* __restrict__ x, int plane_len, int n_bins, float* __restrict__ lo,
                  float* __restrict__ hi, int* __restrict__ nonfinite, BT* __restrict__ out) {
     extern __shared__ __align__(16) float fq_x[];  // [plane_len]
-    __shared__ float st[BT_MAXN + 1];
+    __shared__ float st[BT_MAXN + 2];
     __shared__ float smn[FQ_THREADS / 32], smx[FQ_THREADS / 32];
     __shared__ int sbad;
     const int64_t plane = blockIdx.x;
@@ -272,15 +277,23 @@ k_quantize_plane(const float* __restrict__ x, int plane_len, int n_bins, float* 
         if (sbad && nonfinite) atomicOr(nonfinite, 1);
     }
     const int nt = n_bins - 1;
+    // stp[k] = lower bound of bin k (stp[0] = -inf, stp[N] = +inf sentinels)
+    float* const stp = st;
     for (int k = 1 + tid; k <= nt; k += FQ_THREADS)
-        st[k - 1] = mx > mn ? fq_threshold(k, mn, mx, n_bins) : INFINITY;
+        stp[k] = mx > mn ? fq_threshold(k, mn, mx, n_bins) : INFINITY;
+    if (tid == 0) {
+        stp[0] = -INFINITY;
+        stp[n_bins] = INFINITY;
+    }
     const float inv = mx > mn ? (float)((double)n_bins / ((double)mx - (double)mn)) : 0.f;
     const float top = (float)nt;
     __syncthreads();
+    // the fp32 estimate is within one bin of the exact fp64 rule (its relative
+    // error is a few ulps, N * 1e-7 bins): one branch-free correction each way
     auto bin = [&](float v) {
         int b = (int)fminf(fmaxf((v - mn) * inv, 0.f), top);  // NaN -> 0
-        while (b < nt && v >= st[b]) ++b;
-        while (b > 0 && v < st[b - 1]) --b;
+        b = min(b + ((v >= stp[b + 1]) ? 1 : 0), nt);  // (+inf input: stays at nt)
+        b -= (v < stp[b]) ? 1 : 0;
         return b;
     };
     BT* o = out + plane * plane_len;
