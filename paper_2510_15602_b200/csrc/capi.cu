@@ -91,15 +91,18 @@ int launch_reference_weights(const float*, const void*, int, const float*, const
 int64_t score6_scratch_bytes(int);
 int launch_score6(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, void*, int64_t, float*, cudaStream_t);
+int score7_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
+int64_t score7_scratch_bytes(int);
+int launch_score7(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
+                  int, int, int, int, int, int, void*, int64_t, float*, cudaStream_t);
 
-// fused-kernel selection: 0 = auto (v4, else v6 when the caller supplies a
-// scratch, else v3, else v5, else v2, else v1 -- the first that applies),
-// 1 .. 6 = force that version
+// fused-kernel selection: 0 = auto (with a caller-supplied scratch v6, else v7;
+// then v4, v3, v5, v2, v1 -- the first that applies), 1 .. 7 = force that version
 static int g_score_kernel = 0;
 
 struct ScoreChoice {
     int groups;  // channel groups (partial maps per image); <= 0: unsupported
-    int ver;     // 5: score5.cu, 4: score4.cu, 3: score3.cu, 2: score2.cu, 1: score.cu
+    int ver;     // N: scoreN.cu (1: score.cu)
     int fref;    // 1: the reference is selected inside the kernel
 };
 
@@ -116,6 +119,13 @@ static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t 
         if (gg > 0 && fr == (want_fref ? 1 : 0)) return ScoreChoice{gg, 6, fr};
     }
     if (g_score_kernel == 6) return ch;
+    if (allow_scratch && (g_score_kernel == 0 || g_score_kernel == 7) && bins_bytes == 1) {
+        // large patches: v7 always takes the caller's (K3) reference
+        int fr = 0;
+        const int gg = score7_query(h, w, n_bins, t, C, images, groups_hint, pad, budget, 0, &fr);
+        if (gg > 0) return ScoreChoice{gg, 7, 0};
+    }
+    if (g_score_kernel == 7) return ch;
     if ((g_score_kernel == 0 || g_score_kernel == 4) && bins_bytes == 1) {
         int fr = 0;
         const int gg = score4_query(h, w, n_bins, t, C, images, groups_hint, pad, budget,
@@ -150,7 +160,7 @@ static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t 
 }
 
 static int64_t choice_scratch_bytes(const ScoreChoice& ch, int h) {
-    return ch.ver == 6 ? score6_scratch_bytes(h) : 0;
+    return ch.ver == 6 ? score6_scratch_bytes(h) : ch.ver == 7 ? score7_scratch_bytes(h) : 0;
 }
 
 static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_bytes,
@@ -163,6 +173,9 @@ static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_by
         return launch_score6(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
                              n_bins, t, pad, budget, ch.groups, scratch, scratch_bytes, partial,
                              st);
+    if (ch.ver == 7)
+        return launch_score7(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, budget,
+                             ch.groups, scratch, scratch_bytes, partial, st);
     if (ch.ver == 5)
         return launch_score5(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
                              n_bins, t, pad, budget, ch.groups, partial, st);
@@ -328,7 +341,7 @@ int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
 }
 
 int qfca_set_score_kernel(int32_t version) {
-    if (version < 0 || version > 6) return QFCA_ERR_ARG;
+    if (version < 0 || version > 7) return QFCA_ERR_ARG;
     g_score_kernel = version;
     return QFCA_OK;
 }

@@ -1,0 +1,474 @@
+// score7.cu -- K4 v7: the fused scoring kernel for LARGE patch sizes (T = 17..65)
+// on 128-wide planes / tiles (configs[3]'s patch sweep at 1024^2).
+//
+// v6 keeps the vertical box of the transport errors E in a T-row register ring
+// and gathers the own-bin horizontal box with T taps: both scale with T.  v7
+// keeps no T-row state at all.  Same closed-form transport (score2.cu's fp32
+// G_i, rcp.approx; bit-identical E for the same counts) and the same window
+// counts, but the association is an exact 2D prefix (summed-area table) of E
+// over the reflect-padded window-centre grid, evaluated incrementally:
+//
+//   Q_i(s, p) = sum_{s' <= s, p' <= p} E_i(centre(s'), column(p'))     (fp64)
+//   score(y, x) = Q_b(y+2R, x+2R) - Q_b(y+2R, x-1) - Q_b(y-1, x+2R) + Q_b(y-1, x-1)
+//
+// with b = bin(y, x).  The stream walks the padded centre rows s = 0 .. h+2R-1
+// once; after row s the CTA holds the row Q(s, .) of all 16 bins; a pixel
+// whose window starts at s + 1 snapshots the first difference of its own bin,
+// a pixel whose window ends at s subtracts it (per-pixel snapshots in a ring of
+// 2R + 2 rows).  Every cost per (channel, pixel) is independent of T:
+//
+//   phase RW  row windows of the thermometer counts (8-bit lanes, one warp per
+//             row: warp prefix scan over the padded row, window = difference of
+//             two prefix words) -> per-SM scratch in L2 (word-major rows);
+//   phase 4   per stream row: the vertical window counts slide by one row in
+//             registers (16-bit lanes: add the entering row's windows, remove
+//             the leaving row's), E of the thread's 4 bins from the shared
+//             prefix table PJ (the G values computed, not tabulated: 16 x (T^2
+//             + 1) floats do not fit), E row -> shared memory; one warp per bin
+//             scans the row (fp64, registers keep Q for its columns) and
+//             publishes Q(s, .); bin groups 2 / 3 (rare mass, light E) take the
+//             snapshots and the finished pixels.
+// The reference comes from K3 (reference.cu).  fp64 prefixes: the result is the
+// reference's own fp64 SAT association (scoring.py:218-232) up to summation
+// order, far inside the 1e-4 bar.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace qfca {
+
+constexpr int S7_THREADS = 512;
+constexpr int S7_W = 128;
+constexpr int S7_EST = S7_W + 2;  // E row stride (conflict-free stores)
+constexpr int S7_SMEM_MAX = 227 * 1024;
+
+struct Score7Geom {
+    int h, n_bins, pad, C, groups, cpg;
+    int S;      // stream rows h + 2R
+    int nsnap;  // snapshot rows 2R + 2
+    int o_sb, o_pj, o_erow, o_qrow, o_prow, o_snap, o_xmap, o_stab, o_misc, total;
+};
+
+__device__ __forceinline__ float rcp_approx7(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t smid7() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+template <int T>
+static void score7_layout(Score7Geom& g) {
+    constexpr int R = T / 2;
+    constexpr int WP = S7_W + 2 * R;
+    int off = 0;
+    auto take = [&](long long bytes) {
+        const int o = off;
+        off = (int)((off + bytes + 15) & ~15LL);
+        return o;
+    };
+    g.o_sb = take((long long)g.h * S7_W);
+    g.o_pj = take((long long)(T * T + 1) * 4);
+    g.o_erow = take(16LL * S7_EST * 4);
+    g.o_qrow = take(16LL * WP * 8);
+    g.o_prow = take(16LL * WP * 16);  // one padded prefix row per warp (RW phase)
+    g.o_snap = take((long long)g.nsnap * S7_W * 8);
+    g.o_xmap = take((long long)WP * 4);
+    g.o_stab = take((long long)g.S * 16);
+    g.o_misc = take(1024);
+    g.total = off;
+}
+
+template <int T>
+__global__ void __launch_bounds__(S7_THREADS, 1)
+k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
+         const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score7Geom g,
+         uint32_t* __restrict__ scratch, float* __restrict__ partial) {
+    constexpr int W = S7_W;
+    constexpr int R = T / 2;
+    constexpr int T2 = T * T;
+    constexpr int WP = W + 2 * R;             // padded columns
+    constexpr int CPL = (WP + 31) / 32;       // padded columns per lane (scans)
+    constexpr int EST = S7_EST;
+    constexpr uint32_t FULL = 0xffffffffu;
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint8_t* const sb = sm + g.o_sb;
+    float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
+    float* const Erow = reinterpret_cast<float*>(sm + g.o_erow);     // [16][EST]
+    double* const Qrow = reinterpret_cast<double*>(sm + g.o_qrow);   // [16][WP]
+    uint4* const Prow = reinterpret_cast<uint4*>(sm + g.o_prow);     // [16 warps][WP]
+    double* const snap = reinterpret_cast<double*>(sm + g.o_snap);   // [nsnap][W]
+    int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
+    int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);        // per stream row
+    float* const sscale = reinterpret_cast<float*>(sm + g.o_misc);    // [1]
+    int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);       // [16]
+    float* const svm = reinterpret_cast<float*>(sm + g.o_misc + 80);  // [16]
+    float* const sd = reinterpret_cast<float*>(sm + g.o_misc + 144);  // [16]
+    __shared__ uint4 TH[256];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int h = g.h;
+    const int hw = h * W;
+    const int img = blockIdx.x / g.groups, cgi = blockIdx.x % g.groups;
+    const int c_begin = cgi * g.cpg, c_end = min(g.C, c_begin + g.cpg);
+    float* const part = partial + ((int64_t)img * g.groups + cgi) * hw;
+    uint32_t* const scr = scratch + (size_t)smid7() * (size_t)h * 4 * W;
+
+    // ---- per-CTA tables
+    for (int p = tid; p < WP; p += S7_THREADS) xmap[p] = map_coord(p - R, W, g.pad);
+    // stream row s = padded centre row, centre c = map(s - R): how the window
+    // counts move from row s - 1 (x = +1 / -1: slide, add / remove row;
+    // x = 0: recount all rows around the centre)
+    for (int s = tid; s < g.S; s += S7_THREADS) {
+        const int c = map_coord(s - R, h, g.pad);
+        int mode = 0, add = 0, rem = 0;
+        if (s > 0) {
+            const int cp = map_coord(s - 1 - R, h, g.pad);
+            if (c == cp + 1) { mode = 1; add = map_coord(c + R, h, g.pad); rem = map_coord(cp - R, h, g.pad); }
+            else if (c == cp - 1) { mode = 1; add = map_coord(c - R, h, g.pad); rem = map_coord(cp + R, h, g.pad); }
+            else if (c == cp) { mode = 2; }
+        }
+        stab[s] = make_int4(c, mode, add, rem);
+    }
+    for (int b = tid; b < 256; b += S7_THREADS) {
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
+            const int d = b - 4 * q;
+            v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
+        }
+        TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+
+    // phase-4 roles: thread (column x, bin group grp), the 4 groups of a column
+    // in adjacent lanes (warp = 8 columns: balanced E work per warp, the
+    // group-below count is one shuffle away); scan roles: warp = bin
+    const int grp = tid & 3, x = tid >> 2;
+    int scol[CPL];  // the columns this scan lane reads: padded p = lane * CPL + k
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+        const int p = lane * CPL + k;
+        scol[k] = p < WP ? xmap[p] : 0;
+    }
+    // row windows in the scratch: [row][x][4 words], word q = bins 4q .. 4q+3
+    const uint32_t* const rwt = scr + x * 4 + grp;
+
+    for (int c = c_begin; c < c_end; ++c) {
+        const int64_t plane = (int64_t)img * g.C + c;
+        if (tid == 0) {
+            float sc = 0.f;
+            if (hi[plane] > lo[plane])
+                sc = (float)(((double)hi[plane] - (double)lo[plane]) / (double)g.n_bins /
+                             (double)T2);
+            sscale[0] = sc;
+        }
+        if (tid < 16) sV[tid] = tid < g.n_bins ? __ldg(Vref + plane * g.n_bins + tid) : T2;
+        for (int i = tid; i < hw / 16; i += S7_THREADS)
+            reinterpret_cast<uint4*>(sb)[i] = __ldg(reinterpret_cast<const uint4*>(bins + plane * hw) + i);
+        __syncthreads();
+        const float scale = sscale[0];
+        if (scale == 0.f) {  // degenerate channel (scoring.py:265-266)
+            __syncthreads();
+            continue;
+        }
+
+        // ======== phase RW: row windows of every plane row -> scratch, one warp per row
+        for (int y = warp; y < h; y += S7_THREADS / 32) {
+            const uint8_t* const brow = sb + y * W;
+            uint4 pre[CPL];
+            uint4 run = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                const int p = lane * CPL + k;
+                const uint4 v = p < WP ? TH[brow[scol[k]]] : make_uint4(0, 0, 0, 0);
+                run.x += v.x; run.y += v.y; run.z += v.z; run.w += v.w;
+                pre[k] = run;
+            }
+            // exclusive scan of the lane totals (8-bit lanes stay <= WP <= 255: exact)
+            uint4 off = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t ax = __shfl_up_sync(FULL, off.x, o), ay = __shfl_up_sync(FULL, off.y, o);
+                const uint32_t az = __shfl_up_sync(FULL, off.z, o), aw = __shfl_up_sync(FULL, off.w, o);
+                if (lane >= o) { off.x += ax; off.y += ay; off.z += az; off.w += aw; }
+            }
+            off.x -= run.x; off.y -= run.y; off.z -= run.z; off.w -= run.w;
+            uint4* const pr = Prow + warp * WP;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                const int p = lane * CPL + k;
+                if (p < WP)
+                    pr[p] = make_uint4(pre[k].x + off.x, pre[k].y + off.y, pre[k].z + off.z,
+                                       pre[k].w + off.w);
+            }
+            __syncwarp();
+            uint4* const dst = reinterpret_cast<uint4*>(scr + (size_t)y * 4 * W);
+#pragma unroll
+            for (int k = 0; k < W / 32; ++k) {
+                const int xx = lane + 32 * k;
+                const uint4 a = pr[xx + 2 * R];
+                const uint4 b = xx > 0 ? pr[xx - 1] : make_uint4(0, 0, 0, 0);
+                dst[xx] = make_uint4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+            }
+            __syncwarp();
+        }
+        // ======== tables: PJ = prefix of J; (V_{i-1}, D_i) per bin
+        for (int qq = tid; qq < T2; qq += S7_THREADS) {
+            int a = 0, bnd = g.n_bins - 1;
+            while (a < bnd) {
+                const int mid = (a + bnd) >> 1;
+                if (sV[mid] > qq) bnd = mid; else a = mid + 1;
+            }
+            sPJ[qq + 1] = (float)a;
+        }
+        for (int i = tid; i < g.nsnap * W; i += S7_THREADS) snap[i] = 0.0;
+        __syncthreads();
+        if (warp == 0) {
+            float carry = 0.f;
+            if (lane == 0) sPJ[0] = 0.f;
+            for (int base = 1; base <= T2; base += 32) {
+                const int qq = base + lane;
+                float v = qq <= T2 ? sPJ[qq] : 0.f;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float u = __shfl_up_sync(FULL, v, o);
+                    if (lane >= o) v += u;
+                }
+                v += carry;
+                if (qq <= T2) sPJ[qq] = v;
+                carry = __shfl_sync(FULL, v, 31);
+            }
+        }
+        __syncthreads();
+        if (tid < 16) {
+            const int i = tid;
+            float vm = 0.f, d = 0.f;
+            if (i < g.n_bins) {
+                const int vmi = i > 0 ? sV[i - 1] : 0;
+                vm = (float)vmi;
+                d = 2.f * ((float)i * vm - sPJ[vmi]);
+            }
+            svm[i] = vm;
+            sd[i] = d;
+        }
+        __syncthreads();  // scratch rows, PJ, (vm, d) ready
+
+        // ======== phase 4: stream the padded centre rows
+        {
+            // this thread's 4 bins: i = 4 grp + j
+            float vmj[4], dj[4], fi[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                vmj[j] = svm[grp * 4 + j];
+                dj[j] = sd[grp * 4 + j];
+                fi[j] = (float)(grp * 4 + j);
+            }
+            // vertical window counts, 16-bit lanes: lo = lanes (4g, 4g+2), hi =
+            // (4g+1, 4g+3); the count below the group (lane 4g-1) is the
+            // neighbour lane's top lane
+            uint32_t alo = 0, ahi = 0;
+            uint32_t na = 0, nr = 0;  // entering / leaving row windows of row s (prefetched)
+            double q[CPL];  // scan lane's running column prefixes Q(s, p) of bin `warp`
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) q[k] = 0.0;
+            const int xl = tid & (W - 1);  // snapshot / finish roles: tid < 2 W
+            float pold = 0.f;
+            for (int s = 0; s < g.S; ++s) {
+                const int4 st = stab[s];
+                // ---- vertical slide (or recount) of the window counts
+                if (st.y == 1) {
+                    alo += (na & 0x00FF00FFu) - (nr & 0x00FF00FFu);
+                    ahi += ((na >> 8) & 0x00FF00FFu) - ((nr >> 8) & 0x00FF00FFu);
+                } else if (st.y == 0) {
+                    alo = ahi = 0;
+                    for (int dy = -R; dy <= R; ++dy) {
+                        const uint32_t wa = rwt[(size_t)map_coord(st.x + dy, h, g.pad) * 4 * W];
+                        alo += wa & 0x00FF00FFu;
+                        ahi += (wa >> 8) & 0x00FF00FFu;
+                    }
+                }
+                if (s + 1 < g.S) {  // prefetch the next row's entering / leaving windows
+                    const int4 sn = stab[s + 1];
+                    if (sn.y == 1) {
+                        na = rwt[(size_t)sn.z * 4 * W];
+                        nr = rwt[(size_t)sn.w * 4 * W];
+                    }
+                }
+                // ---- E of the 4 bins (G from the shared PJ prefix table)
+                const int a0 = (int)(alo & 0xFFFFu), a1 = (int)(ahi & 0xFFFFu),
+                          a2 = (int)(alo >> 16), a3 = (int)(ahi >> 16);
+                int a_1 = __shfl_up_sync(FULL, a3, 1);
+                if (grp == 0) a_1 = 0;
+                float E[4] = {0.f, 0.f, 0.f, 0.f};
+                if (__any_sync(FULL, a3 != a_1)) {
+                    const int av[5] = {a_1, a0, a1, a2, a3};
+                    float pj[5];
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) pj[k] = sPJ[av[k]];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float fa = (float)av[j], fb = (float)av[j + 1];
+                        const float nua = fmaf(fi[j], fa, -pj[j]), nub = fmaf(fi[j], fb, -pj[j + 1]);
+                        const float ga = fa < vmj[j] ? nua : dj[j] - nua;
+                        const float gb = fb < vmj[j] ? nub : dj[j] - nub;
+                        E[j] = (gb - ga) * rcp_approx7(fmaxf(fb - fa, 1.f));
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) Erow[(grp * 4 + j) * EST + x] = E[j];
+                // partial map of the pixel that finishes at this row (fetched early)
+                const int yf = s - 2 * R;
+                if (tid >= W && tid < 2 * W && yf >= 0 && yf < h) pold = part[yf * W + xl];
+                __syncthreads();  // E row complete; the previous row's Q readers done
+                // ---- one warp per bin: the padded E row's prefix (fp32 within the
+                //      row), added to the fp64 running prefixes Q
+                {
+                    const float* const er = Erow + warp * EST;
+                    float rp[CPL];
+                    float run = 0.f;
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k) {
+                        const int p = lane * CPL + k;
+                        run += p < WP ? er[scol[k]] : 0.f;
+                        rp[k] = run;
+                    }
+                    float off = run;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const float u = __shfl_up_sync(FULL, off, o);
+                        if (lane >= o) off += u;
+                    }
+                    off -= run;
+                    double* const qr = Qrow + warp * WP;
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k) {
+                        const int p = lane * CPL + k;
+                        q[k] += (double)(rp[k] + off);
+                        if (p < WP) qr[p] = q[k];
+                    }
+                }
+                __syncthreads();  // Q(s, .) published
+                // ---- snapshots (pixels whose window starts at s + 1) and the
+                //      pixels whose window ended at s
+                if (tid < W) {
+                    const int ys = s + 1;
+                    if (ys < h) {
+                        const int b = sb[ys * W + xl];
+                        const double* const qr = Qrow + b * WP;
+                        snap[(ys % g.nsnap) * W + xl] = qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0);
+                    }
+                } else if (tid < 2 * W && yf >= 0 && yf < h) {
+                    const int b = sb[yf * W + xl];
+                    const double* const qr = Qrow + b * WP;
+                    const double sc = (qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0)) -
+                                      snap[(yf % g.nsnap) * W + xl];
+                    part[yf * W + xl] = pold + fmaf((float)sc, scale, 0.f);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int sample_stride(int h, int w, int budget);
+
+template <int T>
+static int s7_total(Score7Geom& g) {
+    score7_layout<T>(g);
+    return g.total;
+}
+
+static int nsmid7() {
+    static int n = 0;
+    if (n <= 0) {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+        n = sms + 64;  // %smid < %nsmid; generous headroom for id gaps
+    }
+    return n;
+}
+
+static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                       int pad, bool has_ref, Score7Geom* out, size_t* smem_out) {
+    if (!has_ref) return QFCA_ERR_UNSUPPORTED;  // the reference comes from K3
+    if (w != S7_W || t < 17 || t > 65 || (t & 1) == 0 || n_bins < 1 || n_bins > 16)
+        return QFCA_ERR_UNSUPPORTED;
+    if (h < 2 || h > 128 || (h * w) % 16) return QFCA_ERR_UNSUPPORTED;
+    if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
+    Score7Geom g;
+    memset(&g, 0, sizeof(g));
+    g.h = h; g.n_bins = n_bins; g.pad = pad; g.C = C;
+    g.S = h + 2 * (t / 2);
+    g.nsnap = 2 * (t / 2) + 2;
+    size_t bytes = 0;
+    switch (t) {
+#define S7C(TT) case TT: bytes = s7_total<TT>(g); break;
+        S7C(17) S7C(19) S7C(21) S7C(23) S7C(25) S7C(27) S7C(29) S7C(31) S7C(33) S7C(35)
+        S7C(37) S7C(39) S7C(41) S7C(43) S7C(45) S7C(47) S7C(49) S7C(51) S7C(53) S7C(55)
+        S7C(57) S7C(59) S7C(61) S7C(63) S7C(65)
+#undef S7C
+        default: return QFCA_ERR_UNSUPPORTED;
+    }
+    if (bytes > (size_t)S7_SMEM_MAX - 4096) return QFCA_ERR_UNSUPPORTED;  // + static TH
+    int groups = groups_hint;
+    if (groups <= 0) groups = balanced_groups(images, C, 1, 1);
+    groups = groups < 1 ? 1 : (groups > C ? C : groups);
+    g.cpg = (C + groups - 1) / groups;
+    g.groups = (C + g.cpg - 1) / g.cpg;
+    *out = g;
+    *smem_out = bytes;
+    return QFCA_OK;
+}
+
+int score7_query(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
+                 int pad, int budget, int want_fref, int* fref) {
+    (void)budget;
+    Score7Geom g;
+    size_t smem;
+    if (score7_plan(h, w, n_bins, t, C, images, groups_hint, pad, want_fref == 0, &g, &smem) !=
+        QFCA_OK)
+        return -1;
+    if (fref) *fref = 0;
+    return g.groups;
+}
+
+int64_t score7_scratch_bytes(int h) { return (int64_t)nsmid7() * h * 4 * S7_W * 4; }
+
+int launch_score7(const void* bins, int bins_bytes, const float* lo, const float* hi,
+                  const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
+                  int pad, int budget, int groups, void* scratch, int64_t scratch_bytes,
+                  float* partial, cudaStream_t st) {
+    (void)budget;
+    if (bins_bytes != 1 || !V) return QFCA_ERR_UNSUPPORTED;
+    if (!scratch || scratch_bytes < score7_scratch_bytes(h)) return QFCA_ERR_ARG;
+    Score7Geom g;
+    size_t smem;
+    int rc = score7_plan(h, w, n_bins, t, C, images, groups, pad, true, &g, &smem);
+    if (rc != QFCA_OK) return rc;
+    if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
+    void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score7Geom,
+                 uint32_t*, float*) = nullptr;
+    switch (t) {
+#define S7K(TT) case TT: kern = k_score7<TT>; break;
+        S7K(17) S7K(19) S7K(21) S7K(23) S7K(25) S7K(27) S7K(29) S7K(31) S7K(33) S7K(35)
+        S7K(37) S7K(39) S7K(41) S7K(43) S7K(45) S7K(47) S7K(49) S7K(51) S7K(53) S7K(55)
+        S7K(57) S7K(59) S7K(61) S7K(63) S7K(65)
+#undef S7K
+        default: return QFCA_ERR_UNSUPPORTED;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return QFCA_ERR_CUDA;
+    const int64_t grid = images * g.groups;
+    kern<<<(unsigned)grid, S7_THREADS, smem, st>>>((const uint8_t*)bins, lo, hi, V, g,
+                                                   (uint32_t*)scratch, partial);
+    return cudaGetLastError() == cudaSuccess ? QFCA_OK : QFCA_ERR_CUDA;
+}
+
+}  // namespace qfca
