@@ -120,10 +120,13 @@ static ScoreChoice score_choose(int h, int w, int n_bins, int t, int C, int64_t 
     }
     if (g_score_kernel == 6) return ch;
     if (allow_scratch && (g_score_kernel == 0 || g_score_kernel == 7) && bins_bytes == 1) {
-        // large patches: v7 always takes the caller's (K3) reference
+        // large patches: v7 selects the reference itself when its sample store
+        // fits, else takes the caller's (K3)
         int fr = 0;
-        const int gg = score7_query(h, w, n_bins, t, C, images, groups_hint, pad, budget, 0, &fr);
-        if (gg > 0) return ScoreChoice{gg, 7, 0};
+        int gg = score7_query(h, w, n_bins, t, C, images, groups_hint, pad, budget, want_fref, &fr);
+        if (gg <= 0 && want_fref)
+            gg = score7_query(h, w, n_bins, t, C, images, groups_hint, pad, budget, 0, &fr);
+        if (gg > 0) return ScoreChoice{gg, 7, fr};
     }
     if (g_score_kernel == 7) return ch;
     if ((g_score_kernel == 0 || g_score_kernel == 4) && bins_bytes == 1) {
@@ -174,8 +177,9 @@ static int launch_score_any(const ScoreChoice& ch, const void* bins, int bins_by
                              n_bins, t, pad, budget, ch.groups, scratch, scratch_bytes, partial,
                              st);
     if (ch.ver == 7)
-        return launch_score7(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, budget,
-                             ch.groups, scratch, scratch_bytes, partial, st);
+        return launch_score7(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
+                             n_bins, t, pad, budget, ch.groups, scratch, scratch_bytes, partial,
+                             st);
     if (ch.ver == 5)
         return launch_score5(bins, bins_bytes, lo, hi, ch.fref ? nullptr : V, images, C, h, w,
                              n_bins, t, pad, budget, ch.groups, partial, st);

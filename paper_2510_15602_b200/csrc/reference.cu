@@ -28,6 +28,7 @@ constexpr int REF_NW = 5;  // 4 packed count words + 1 "below chunk" word
 
 struct RefGeom {
     int h, w, t, r, wp, stride, ny, nx, S, G;
+    int stage;  // 1: the plane's bins are staged in shared memory first
 };
 
 template <int LANE>
@@ -91,6 +92,19 @@ k_reference(const BT* __restrict__ bins, const float* __restrict__ lo,
     uint32_t* CC = reinterpret_cast<uint32_t*>(smem + off);      // [G][NW][wp]
     off += (size_t)g.G * REF_NW * g.wp * 4;
     uint32_t* WS = reinterpret_cast<uint32_t*>(smem + off);      // [G][NW][nx]
+    off += (size_t)g.G * REF_NW * g.nx * 4;
+    if (g.stage) {  // one coalesced read of the plane; the window sweeps then hit smem
+        BT* sbins = reinterpret_cast<BT*>(smem + ((off + 15) & ~(size_t)15));
+        const int64_t n = (int64_t)g.h * g.w;
+        if ((n * (int64_t)sizeof(BT)) % 16 == 0 && (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
+            for (int64_t i = tid; i < n * (int64_t)sizeof(BT) / 16; i += REF_THREADS)
+                reinterpret_cast<uint4*>(sbins)[i] = __ldg(reinterpret_cast<const uint4*>(bp) + i);
+        } else {
+            for (int64_t i = tid; i < n; i += REF_THREADS) sbins[i] = bp[i];
+        }
+        bp = sbins;
+        __syncthreads();
+    }
 
     for (int i0 = 0; i0 < n_bins; i0 += NBC) {
         const int nb = min(NBC, n_bins - i0);
@@ -224,12 +238,13 @@ k_reference(const BT* __restrict__ bins, const float* __restrict__ lo,
     }
 }
 
-static size_t ref_smem_bytes(const RefGeom& g, int st_bytes, int nbc) {
+static size_t ref_smem_bytes(const RefGeom& g, int st_bytes, int nbc, int bt_bytes) {
     const int srow = (g.S + 3) & ~3;
     size_t off = ((size_t)nbc * srow * st_bytes + 15) & ~(size_t)15;
     off += (size_t)REF_NW * g.wp * 4;
     off += (size_t)g.G * REF_NW * g.wp * 4;
     off += (size_t)g.G * REF_NW * g.nx * 4;
+    if (g.stage) off = ((off + 15) & ~(size_t)15) + (size_t)g.h * g.w * bt_bytes;
     return off;
 }
 
@@ -256,9 +271,19 @@ static int launch_reference_t(const BT* bins, const float* lo, const float* hi, 
     const int nbc = lane8 ? 16 : 8;
     const int st_bytes = st8 ? 1 : 2;
     const size_t limit = 200 * 1024;
+    const int bt = (int)sizeof(BT);
+    // stage small planes in shared memory (the sliding window sweeps re-read
+    // every row 2 x (chunks) times; from global memory they are latency-bound)
+    // while two CTAs still fit per SM, else read them from global memory
+    g.stage = 0;
     g.G = 8;
-    while (g.G > 1 && ref_smem_bytes(g, st_bytes, nbc) > limit) g.G >>= 1;
-    const size_t smem = ref_smem_bytes(g, st_bytes, nbc);
+    if ((int64_t)h * w * bt <= 48 * 1024) {
+        g.stage = 1;
+        while (g.G > 2 && ref_smem_bytes(g, st_bytes, nbc, bt) > 110 * 1024) g.G >>= 1;
+        if (ref_smem_bytes(g, st_bytes, nbc, bt) > 110 * 1024) { g.stage = 0; g.G = 8; }
+    }
+    while (g.G > 1 && ref_smem_bytes(g, st_bytes, nbc, bt) > limit) g.G >>= 1;
+    const size_t smem = ref_smem_bytes(g, st_bytes, nbc, bt);
     if (smem > limit) return QFCA_ERR_UNSUPPORTED;
     cudaError_t e;
 #define QFCA_REF_LAUNCH(LANE, STT)                                                         \

@@ -46,7 +46,9 @@ struct Score7Geom {
     int h, n_bins, pad, C, groups, cpg;
     int S;      // stream rows h + 2R
     int nsnap;  // snapshot rows 2R + 2
-    int o_sb, o_pj, o_erow, o_qrow, o_prow, o_snap, o_xmap, o_stab, o_misc, total;
+    // in-kernel reference (median-quan, quantize.py:150-200): sample grid
+    int fref, stride, nsy, nsx, nsamp, srow;
+    int o_sb, o_pj, o_erow, o_qrow, o_prow, o_snap, o_sa, o_xmap, o_stab, o_misc, total;
 };
 
 __device__ __forceinline__ float rcp_approx7(float x) {
@@ -71,11 +73,18 @@ static void score7_layout(Score7Geom& g) {
         return o;
     };
     g.o_sb = take((long long)g.h * S7_W);
+    // the sample store (fref) aliases the buffers of the other phases
+    const int ubase = off;
     g.o_pj = take((long long)(T * T + 1) * 4);
-    g.o_erow = take(16LL * S7_EST * 4);
     g.o_qrow = take(16LL * WP * 8);
     g.o_prow = take(16LL * WP * 16);  // one padded prefix row per warp (RW phase)
     g.o_snap = take((long long)g.nsnap * S7_W * 8);
+    g.o_sa = ubase;
+    if (g.fref) {
+        const long long sab = ((long long)g.srow * 16 * 2 + 15) & ~15LL;
+        if (ubase + sab > off) off = (int)(ubase + sab);
+    }
+    g.o_erow = take(16LL * S7_EST * 4);
     g.o_xmap = take((long long)WP * 4);
     g.o_stab = take((long long)g.S * 16);
     g.o_misc = take(1024);
@@ -103,6 +112,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     double* const snap = reinterpret_cast<double*>(sm + g.o_snap);   // [nsnap][W]
     int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
     int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);        // per stream row
+    uint16_t* const SA = reinterpret_cast<uint16_t*>(sm + g.o_sa);     // [16][srow] (fref)
     float* const sscale = reinterpret_cast<float*>(sm + g.o_misc);    // [1]
     int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);       // [16]
     float* const svm = reinterpret_cast<float*>(sm + g.o_misc + 80);  // [16]
@@ -166,7 +176,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                              (double)T2);
             sscale[0] = sc;
         }
-        if (tid < 16) sV[tid] = tid < g.n_bins ? __ldg(Vref + plane * g.n_bins + tid) : T2;
+        if (tid < 16) sV[tid] = (tid < g.n_bins && !g.fref) ? __ldg(Vref + plane * g.n_bins + tid) : T2;
         for (int i = tid; i < hw / 16; i += S7_THREADS)
             reinterpret_cast<uint4*>(sb)[i] = __ldg(reinterpret_cast<const uint4*>(bins + plane * hw) + i);
         __syncthreads();
@@ -215,6 +225,68 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 dst[xx] = make_uint4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
             }
             __syncwarp();
+        }
+        if (g.fref) {
+            // ======== the reference (median-quan) from this plane's own window
+            // counts: the cumulative counts A_i(s) at the stride-grid samples
+            // (reference.cu's statistic: V_i = the (S-1-m)-th smallest A_i(s))
+            __syncthreads();  // scratch rows complete
+            const int nsx = g.nsx, nsy = g.nsy, sd_ = g.stride;
+            const int cols = 4 * nsx;
+            const int nsub = max(1, S7_THREADS / cols);
+            const int per = (nsy + nsub - 1) / nsub;
+            if (tid < cols * nsub) {
+                const int sub = tid / cols, r = tid % cols, jx = r >> 2, gq = r & 3;
+                const uint32_t* const col = scr + (jx * sd_) * 4 + gq;
+                uint16_t* const sa = SA + (size_t)(4 * gq) * g.srow;
+                const int j0 = sub * per, j1 = min(nsy, j0 + per);
+                uint32_t l16 = 0, h16 = 0;
+                for (int j = j0; j < j1; ++j) {
+                    const int cy = j * sd_;
+                    if (j == j0 || sd_ >= T) {
+                        l16 = h16 = 0;
+                        for (int dy = -R; dy <= R; ++dy) {
+                            const uint32_t w = col[(size_t)map_coord(cy + dy, h, g.pad) * 4 * W];
+                            l16 += w & 0x00FF00FFu;
+                            h16 += (w >> 8) & 0x00FF00FFu;
+                        }
+                    } else {
+                        for (int d = 0; d < sd_; ++d) {
+                            const uint32_t wa = col[(size_t)map_coord(cy + R - sd_ + 1 + d, h, g.pad) * 4 * W];
+                            const uint32_t wr = col[(size_t)map_coord(cy - sd_ - R + d, h, g.pad) * 4 * W];
+                            l16 += (wa & 0x00FF00FFu) - (wr & 0x00FF00FFu);
+                            h16 += ((wa >> 8) & 0x00FF00FFu) - ((wr >> 8) & 0x00FF00FFu);
+                        }
+                    }
+                    const int si = j * nsx + jx;
+                    sa[si] = (uint16_t)(l16 & 0xFFFFu);
+                    sa[g.srow + si] = (uint16_t)(h16 & 0xFFFFu);
+                    sa[2 * g.srow + si] = (uint16_t)(l16 >> 16);
+                    sa[3 * g.srow + si] = (uint16_t)(h16 >> 16);
+                }
+            }
+            // pad the sample rows so packed compares see values > any query
+            const int padn = g.srow - g.nsamp;
+            for (int idx = tid; idx < 16 * padn; idx += S7_THREADS)
+                SA[(size_t)(idx / padn) * g.srow + g.nsamp + idx % padn] = 32767;
+            __syncthreads();
+            const int m = (g.nsamp - 1) / 2, c0 = g.nsamp - m;
+            const int words = g.srow / 2;
+            for (int bi = warp; bi < g.n_bins; bi += S7_THREADS / 32) {
+                const uint32_t* const row = reinterpret_cast<const uint32_t*>(SA + (size_t)bi * g.srow);
+                int a = 0, b = T2;
+                while (a < b) {  // smallest v with #{A <= v} >= c0
+                    const int mid = (a + b) >> 1;
+                    const uint32_t q = 0x80008000u | ((uint32_t)mid * 0x00010001u);
+                    int cnt = 0;
+                    for (int wi = lane; wi < words; wi += 32)
+                        cnt += __popc((q - row[wi]) & 0x80008000u);
+                    cnt = __reduce_add_sync(FULL, cnt);
+                    if (cnt >= c0) b = mid; else a = mid + 1;
+                }
+                if (lane == 0) sV[bi] = a;
+            }
+            __syncthreads();  // sV ready; the sample store is free again
         }
         // ======== tables: PJ = prefix of J; (V_{i-1}, D_i) per bin
         for (int qq = tid; qq < T2; qq += S7_THREADS) {
@@ -395,8 +467,7 @@ static int nsmid7() {
 }
 
 static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
-                       int pad, bool has_ref, Score7Geom* out, size_t* smem_out) {
-    if (!has_ref) return QFCA_ERR_UNSUPPORTED;  // the reference comes from K3
+                       int pad, int budget, bool has_ref, Score7Geom* out, size_t* smem_out) {
     if (w != S7_W || t < 17 || t > 65 || (t & 1) == 0 || n_bins < 1 || n_bins > 16)
         return QFCA_ERR_UNSUPPORTED;
     if (h < 2 || h > 128 || (h * w) % 16) return QFCA_ERR_UNSUPPORTED;
@@ -406,6 +477,16 @@ static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.h = h; g.n_bins = n_bins; g.pad = pad; g.C = C;
     g.S = h + 2 * (t / 2);
     g.nsnap = 2 * (t / 2) + 2;
+    if (!has_ref) {  // in-kernel reference: the sample store must fit shared memory
+        if (budget < 1) return QFCA_ERR_ARG;
+        g.fref = 1;
+        g.stride = sample_stride(h, w, budget);
+        g.nsy = (h + g.stride - 1) / g.stride;
+        g.nsx = (w + g.stride - 1) / g.stride;
+        g.nsamp = g.nsy * g.nsx;
+        g.srow = (g.nsamp + 3) & ~3;
+        if (g.nsamp > 4096) return QFCA_ERR_UNSUPPORTED;
+    }
     size_t bytes = 0;
     switch (t) {
 #define S7C(TT) case TT: bytes = s7_total<TT>(g); break;
@@ -428,13 +509,12 @@ static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
 
 int score7_query(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
                  int pad, int budget, int want_fref, int* fref) {
-    (void)budget;
     Score7Geom g;
     size_t smem;
-    if (score7_plan(h, w, n_bins, t, C, images, groups_hint, pad, want_fref == 0, &g, &smem) !=
-        QFCA_OK)
+    if (score7_plan(h, w, n_bins, t, C, images, groups_hint, pad, budget, want_fref == 0, &g,
+                    &smem) != QFCA_OK)
         return -1;
-    if (fref) *fref = 0;
+    if (fref) *fref = g.fref;
     return g.groups;
 }
 
@@ -444,12 +524,11 @@ int launch_score7(const void* bins, int bins_bytes, const float* lo, const float
                   const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
                   int pad, int budget, int groups, void* scratch, int64_t scratch_bytes,
                   float* partial, cudaStream_t st) {
-    (void)budget;
-    if (bins_bytes != 1 || !V) return QFCA_ERR_UNSUPPORTED;
+    if (bins_bytes != 1) return QFCA_ERR_UNSUPPORTED;
     if (!scratch || scratch_bytes < score7_scratch_bytes(h)) return QFCA_ERR_ARG;
     Score7Geom g;
     size_t smem;
-    int rc = score7_plan(h, w, n_bins, t, C, images, groups, pad, true, &g, &smem);
+    int rc = score7_plan(h, w, n_bins, t, C, images, groups, pad, budget, V != nullptr, &g, &smem);
     if (rc != QFCA_OK) return rc;
     if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
     void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score7Geom,

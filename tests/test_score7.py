@@ -92,3 +92,45 @@ def test_score7_batch_matches_single():
     for i in range(3):
         one = Q.detect_batch(xd[i:i + 1].contiguous(), cfg).scores.cpu().numpy()
         np.testing.assert_array_equal(both[i], one[0])
+
+
+@pytest.mark.parametrize("t,h,n,pad,budget", [
+    (33, 128, 16, 1, 4096), (17, 128, 12, 2, 4096), (65, 100, 16, 1, 4096),
+    (21, 128, 16, 1, 1000), (45, 60, 7, 2, 4096)])
+def test_score7_inkernel_reference_equals_k3(t, h, n, pad, budget):
+    """v7 selecting the reference itself (sample sweep over its own window
+    counts + packed-compare order statistic) gives K3's reference exactly:
+    the partial maps with and without the caller's K3 reference are
+    bit-identical."""
+    import torch
+    from paper_2510_15602_b200 import _native as N
+    from paper_2510_15602_b200 import quantize
+    images, C = 2, 5
+    x = _features(t + h + budget, images, C, h)
+    xd = torch.from_numpy(x).cuda().reshape(images * C, h * 128)
+    lo, hi, _ = quantize.minmax_dev(xd, images * C, h * 128)
+    bins = quantize.bins_dev(xd, lo, hi, images * C, h * 128, n)
+    padname = {1: "reflect", 2: "wrap"}[pad]
+    V = quantize.reference_stats_dev(bins, lo, hi, images * C, h, 128, n, t, padname, budget,
+                                     "median-quan").contiguous()
+    L = N.lib()
+    out = []
+    for ref in (V, None):
+        N.call("qfca_set_score_kernel", 7)
+        try:
+            groups = L.qfca_score_groups_ex(h, 128, n, t, C, images, 1, pad, budget,
+                                            0 if ref is None else 1, 1)
+            assert groups == 1
+            nbytes = L.qfca_score_scratch_bytes(h, 128, n, t, C, images, 1, pad, budget,
+                                                0 if ref is None else 1)
+            assert nbytes > 0
+            scr = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+            part = torch.zeros((images, 1, h * 128), dtype=torch.float32, device="cuda")
+            N.call("qfca_score_ex", bins.data_ptr(), 1, lo.data_ptr(), hi.data_ptr(),
+                   None if ref is None else ref.data_ptr(), images, C, h, 128, n, t, pad,
+                   budget, 1, scr.data_ptr(), nbytes, part.data_ptr(), N.stream())
+            out.append(part.cpu().numpy())
+        finally:
+            N.call("qfca_set_score_kernel", 0)
+    assert np.abs(out[0]).max() > 0
+    np.testing.assert_array_equal(out[1], out[0])
