@@ -46,6 +46,11 @@ constexpr int S6_SLOTS = 4 * S6_BAND;      // staging rows
 constexpr int S6_SEG = 8;                  // H2 columns per task
 constexpr int S6_SMEM_MAX = 227 * 1024;
 constexpr int S6_MAXNB = 76;               // table bins of 5 passes (N <= 76)
+// Vb row pitch: the 128 columns plus mirrored copies of the R <= 7 edge
+// columns on both sides (padded to a multiple of 32 floats, so lanes reading
+// different bins' rows at consecutive columns stay in distinct banks)
+constexpr int S6_VP = S6_W + 32;
+constexpr int S6_VO = 16;                  // column 0's position in a Vb row
 
 struct Score6Geom {
     int h, n_bins, pad, C, groups, cpg;
@@ -106,9 +111,9 @@ static void score6_layout(Score6Geom& g) {
         return o;
     };
     g.o_sb = take((long long)(g.dbsb ? 2 : 1) * g.h * S6_W);
-    // SA4 (phases 1-2) and Vb (phase 4, 2 x CH rows x 16 bins x 128) share one region
+    // SA4 (phases 1-2) and Vb (phase 4, 2 x CH rows x 16 bins x S6_VP) share one region
     const long long sa = (long long)g.nsamp * 16;
-    const long long vb = 2LL * CH * 16 * S6_W * 4;
+    const long long vb = 2LL * CH * 16 * S6_VP * 4;
     g.o_sa = take(sa > vb ? sa : vb);
     g.o_stg = take((long long)S6_SLOTS * wpp * 16);
     g.o_gt = take((long long)g.nbt * GP * 4);
@@ -522,14 +527,23 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             // own-bin box rows of a sub-chunk: row a * 4 + ((grp + 3) & 3), so bin
             // group 0 (mass in nearly every window, the longest E) boxes last
             const int arow0 = (grp + 3) & 3;
-            // the warps of columns 0-31 and 96-127 hold the 2R edge columns (R <= 7)
-            const bool edge_warp = x < 32 || x >= W - 32;
+            // the padded position (if any) that mirrors column x: the box then
+            // reads Vb rows straight, without index reflection
+            constexpr int NOM = 1 << 20;  // no mirror position
+            int xm = NOM;
+            if (g.pad == QFCA_PAD_REFLECT) {
+                if (x >= 1 && x <= R) xm = -x;
+                else if (x >= W - 1 - R && x <= W - 2) xm = 2 * (W - 1) - x;
+            } else {
+                if (x < R) xm = W + x;
+                else if (x >= W - R) xm = x - W;
+            }
             constexpr int NA = (CH + 3) / 4;
             float pold[NA];  // partial-map values of the rows boxed next
 #pragma unroll
             for (int a = 0; a < NA; ++a) pold[a] = 0.f;
             auto own_bin_box = [&](int u, const float* pv, bool last) {
-                const float* const vbr = Vb + (size_t)((u & 1) * CH) * 16 * W;
+                const float* const vbr = Vb + (size_t)((u & 1) * CH) * 16 * S6_VP + S6_VO;
 #pragma unroll
                 for (int a = 0; a < NA; ++a) {
                     const int rr = arow0 + 4 * a;
@@ -537,21 +551,10 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     if (rr >= CH || y < 0 || y >= h) continue;
                     const int bb = sb[y * W + x];
                     if (MP && (bb < bin_lo || bb > bin_hi)) continue;  // another pass's pixel
-                    const float* vb = vbr + (rr * 16 + bb - (MP ? tb : 0)) * W;
+                    const float* vb = vbr + (rr * 16 + bb - (MP ? tb : 0)) * S6_VP;
                     float f = 0.f;
-                    if (!edge_warp) {  // warp-uniform: the middle 64 columns
 #pragma unroll
-                        for (int d = -R; d <= R; ++d) f += vb[x + d];
-                    } else if (g.pad == QFCA_PAD_REFLECT) {
-#pragma unroll
-                        for (int d = -R; d <= R; ++d) {  // one reflection (R < W)
-                            const int p = abs(x + d);
-                            f += vb[(W - 1) - abs((W - 1) - p)];
-                        }
-                    } else {
-#pragma unroll
-                        for (int d = -R; d <= R; ++d) f += vb[(x + d + W) & (W - 1)];
-                    }
+                    for (int d = -R; d <= R; ++d) f += vb[x + d];
                     const float old = last ? part[y * W + x] : pv[a];
                     part[y * W + x] = old + fmaf(f, scale, 0.f);
                 }
@@ -562,7 +565,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     const int u = ck * NSUB + sc;  // sub-chunk index
                     S6_COPY(u + 2)
                     const uint32_t* const cs = cring + (u % 3) * SLOT + grp * W + x;
-                    float* const vbw = Vb + (size_t)((u & 1) * CH) * 16 * W;
+                    float* const vbw = Vb + (size_t)((u & 1) * CH) * 16 * S6_VP + S6_VO;
                     // ---- E for CH stream rows (rows past the plane read zero counts):
                     // all rows' count words first, one warp vote per sub-chunk, then
                     // the CH x 4 transports as independent instruction streams
@@ -628,9 +631,12 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         // at (y, x) only if the window centred there holds bin i,
                         // i.e. only if this group has mass there (stream row s - R)
                         if (y >= 0 && y < h && __any_sync(FULL, mring[(rho + T - R) % T])) {
-                            float* vb = vbw + (rr * 16 + grp * 4) * W + x;
+                            float* vb = vbw + (rr * 16 + grp * 4) * S6_VP;
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
+                            for (int j = 0; j < 4; ++j) vb[j * S6_VP + x] = vs[j];
+                            if (xm != NOM)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) vb[j * S6_VP + xm] = vs[j];
                         }
                     }
                     // ---- own-bin horizontal box of sub-chunk u - 1 (other Vb buffer)
