@@ -41,6 +41,7 @@ constexpr int S7_THREADS = 512;
 constexpr int S7_W = 128;
 constexpr int S7_EST = S7_W + 2;  // E row stride (conflict-free stores)
 constexpr int S7_SMEM_MAX = 227 * 1024;
+constexpr int S7_GT_MAXT = 43;  // largest T whose 16 x (T^2 + 1) G table is built
 
 struct Score7Geom {
     int h, n_bins, pad, C, groups, cpg;
@@ -48,7 +49,9 @@ struct Score7Geom {
     int nsnap;  // snapshot rows 2R + 2
     // in-kernel reference (median-quan, quantize.py:150-200): sample grid
     int fref, stride, nsy, nsx, nsamp, srow;
-    int o_sb, o_pj, o_erow, o_qrow, o_prow, o_snap, o_sa, o_xmap, o_stab, o_misc, total;
+    int o_sb, o_pj, o_gt, o_erow, o_qrow, o_prow, o_snap, o_sa, o_xmap, o_stab, o_misc, total;
+    int gt;         // 1: the G_i(v) table (T <= 43 and it fits), else G from PJ
+    uint32_t moff;  // G-table address of the magic float 2^23 + v is base + 4 v
 };
 
 __device__ __forceinline__ float rcp_approx7(float x) {
@@ -62,7 +65,7 @@ __device__ __forceinline__ uint32_t smid7() {
     return r;
 }
 
-template <int T>
+template <int T, bool GT>
 static void score7_layout(Score7Geom& g) {
     constexpr int R = T / 2;
     constexpr int WP = S7_W + 2 * R;
@@ -73,17 +76,24 @@ static void score7_layout(Score7Geom& g) {
         return o;
     };
     g.o_sb = take((long long)g.h * S7_W);
-    // the sample store (fref) aliases the buffers of the other phases
+    // one region, three lives: the RW phase's prefix rows, then the sample
+    // store (fref), then the phase-4 tables and rows
     const int ubase = off;
     g.o_pj = take((long long)(T * T + 1) * 4);
+    g.o_gt = GT ? take(16LL * (T * T + 1) * 4) : 0;
     g.o_qrow = take(16LL * WP * 8);
-    g.o_prow = take(16LL * WP * 16);  // one padded prefix row per warp (RW phase)
     g.o_snap = take((long long)g.nsnap * S7_W * 8);
+    const int p4end = off;
+    g.o_prow = ubase;  // one padded prefix row per warp (RW phase)
     g.o_sa = ubase;
+    long long uend = p4end;
+    const long long prb = 16LL * WP * 16;
+    if (ubase + prb > uend) uend = ubase + prb;
     if (g.fref) {
-        const long long sab = ((long long)g.srow * 16 * 2 + 15) & ~15LL;
-        if (ubase + sab > off) off = (int)(ubase + sab);
+        const long long sab = (long long)g.srow * 16 * 2;
+        if (ubase + sab > uend) uend = ubase + sab;
     }
+    off = (int)((uend + 15) & ~15LL);
     g.o_erow = take(16LL * S7_EST * 4);
     g.o_xmap = take((long long)WP * 4);
     g.o_stab = take((long long)g.S * 16);
@@ -91,7 +101,7 @@ static void score7_layout(Score7Geom& g) {
     g.total = off;
 }
 
-template <int T>
+template <int T, bool GT>
 __global__ void __launch_bounds__(S7_THREADS, 1)
 k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
          const float* __restrict__ hi, const int32_t* __restrict__ Vref, const Score7Geom g,
@@ -102,6 +112,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     constexpr int WP = W + 2 * R;             // padded columns
     constexpr int CPL = (WP + 31) / 32;       // padded columns per lane (scans)
     constexpr int EST = S7_EST;
+    constexpr int GP = T2 + 1;
     constexpr uint32_t FULL = 0xffffffffu;
     extern __shared__ __align__(16) uint8_t sm[];
     uint8_t* const sb = sm + g.o_sb;
@@ -141,7 +152,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             else if (c == cp - 1) { mode = 1; add = map_coord(c - R, h, g.pad); rem = map_coord(cp + R, h, g.pad); }
             else if (c == cp) { mode = 2; }
         }
-        stab[s] = make_int4(c, mode, add, rem);
+        stab[s] = make_int4(c, mode, add * 4 * W, rem * 4 * W);  // scratch offsets
     }
     for (int b = tid; b < 256; b += S7_THREADS) {
         uint32_t v[4];
@@ -226,11 +237,11 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
             __syncwarp();
         }
+        __syncthreads();  // scratch rows complete; the prefix rows' region is free
         if (g.fref) {
             // ======== the reference (median-quan) from this plane's own window
             // counts: the cumulative counts A_i(s) at the stride-grid samples
             // (reference.cu's statistic: V_i = the (S-1-m)-th smallest A_i(s))
-            __syncthreads();  // scratch rows complete
             const int nsx = g.nsx, nsy = g.nsy, sd_ = g.stride;
             const int cols = 4 * nsx;
             const int nsub = max(1, S7_THREADS / cols);
@@ -250,10 +261,10 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             l16 += w & 0x00FF00FFu;
                             h16 += (w >> 8) & 0x00FF00FFu;
                         }
-                    } else {
-                        for (int d = 0; d < sd_; ++d) {
-                            const uint32_t wa = col[(size_t)map_coord(cy + R - sd_ + 1 + d, h, g.pad) * 4 * W];
-                            const uint32_t wr = col[(size_t)map_coord(cy - sd_ - R + d, h, g.pad) * 4 * W];
+                    } else {  // centres cy - stride + 1 .. cy: stream rows + R (slides)
+                        for (int d = cy - sd_ + 1 + R; d <= cy + R; ++d) {
+                            const int4 st = stab[d];
+                            const uint32_t wa = col[st.z], wr = col[st.w];
                             l16 += (wa & 0x00FF00FFu) - (wr & 0x00FF00FFu);
                             h16 += ((wa >> 8) & 0x00FF00FFu) - ((wr >> 8) & 0x00FF00FFu);
                         }
@@ -297,7 +308,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
             sPJ[qq + 1] = (float)a;
         }
-        for (int i = tid; i < g.nsnap * W; i += S7_THREADS) snap[i] = 0.0;
+        if (tid < W) snap[tid] = 0.0;  // row 0's window starts before the stream
         __syncthreads();
         if (warp == 0) {
             float carry = 0.f;
@@ -328,6 +339,16 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             sd[i] = d;
         }
         __syncthreads();  // scratch rows, PJ, (vm, d) ready
+        if (GT) {  // G_i(v) for every bin and count (score6.cu's table)
+            float* const sG = reinterpret_cast<float*>(sm + g.o_gt);
+            for (int idx = tid; idx < 16 * GP; idx += S7_THREADS) {
+                const int i = idx / GP, v = idx - i * GP;
+                const float fv = (float)v;
+                const float nu = fmaf((float)i, fv, -sPJ[v]);
+                sG[idx] = fv < svm[i] ? nu : sd[i] - nu;
+            }
+            __syncthreads();
+        }
 
         // ======== phase 4: stream the padded centre rows
         {
@@ -349,8 +370,11 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             for (int k = 0; k < CPL; ++k) q[k] = 0.0;
             const int xl = tid & (W - 1);  // snapshot / finish roles: tid < 2 W
             float pold = 0.f;
+            const uint32_t gaddr =
+                (uint32_t)__cvta_generic_to_shared(sm + g.o_gt) + grp * 4 * GP * 4 + g.moff;
+            int sf = (g.nsnap - 2 * R) % g.nsnap;  // snapshot slot of row s - 2R
+            int4 st = stab[0];
             for (int s = 0; s < g.S; ++s) {
-                const int4 st = stab[s];
                 // ---- vertical slide (or recount) of the window counts
                 if (st.y == 1) {
                     alo += (na & 0x00FF00FFu) - (nr & 0x00FF00FFu);
@@ -364,10 +388,10 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     }
                 }
                 if (s + 1 < g.S) {  // prefetch the next row's entering / leaving windows
-                    const int4 sn = stab[s + 1];
-                    if (sn.y == 1) {
-                        na = rwt[(size_t)sn.z * 4 * W];
-                        nr = rwt[(size_t)sn.w * 4 * W];
+                    st = stab[s + 1];
+                    if (st.y == 1) {
+                        na = rwt[st.z];
+                        nr = rwt[st.w];
                     }
                 }
                 // ---- E of the 4 bins (G from the shared PJ prefix table)
@@ -376,7 +400,25 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 int a_1 = __shfl_up_sync(FULL, a3, 1);
                 if (grp == 0) a_1 = 0;
                 float E[4] = {0.f, 0.f, 0.f, 0.f};
-                if (__any_sync(FULL, a3 != a_1)) {
+                if (GT) {
+                    if (__any_sync(FULL, a3 != a_1)) {
+                        const int av[5] = {a_1, a0, a1, a2, a3};
+                        uint32_t ma = 0x4B000000u | (uint32_t)av[0];
+                        uint32_t aa = gaddr + 4u * ma;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t mb = 0x4B000000u | (uint32_t)av[j + 1];
+                            const uint32_t ab = gaddr + 4u * mb;
+                            float gb, ga;
+                            asm("ld.shared.f32 %0, [%1];" : "=f"(gb) : "r"(ab + j * GP * 4));
+                            asm("ld.shared.f32 %0, [%1];" : "=f"(ga) : "r"(aa + j * GP * 4));
+                            const float pc = __uint_as_float(mb) - __uint_as_float(ma);
+                            E[j] = (gb - ga) * rcp_approx7(fmaxf(pc, 1.f));
+                            ma = mb;
+                            aa = ab;
+                        }
+                    }
+                } else if (__any_sync(FULL, a3 != a_1)) {
                     const int av[5] = {a_1, a0, a1, a2, a3};
                     float pj[5];
 #pragma unroll
@@ -426,20 +468,23 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 __syncthreads();  // Q(s, .) published
                 // ---- snapshots (pixels whose window starts at s + 1) and the
                 //      pixels whose window ended at s
+                // (slots: row y -> y mod nsnap; row s + 1's slot is row s - 2R's - 1)
                 if (tid < W) {
                     const int ys = s + 1;
                     if (ys < h) {
                         const int b = sb[ys * W + xl];
                         const double* const qr = Qrow + b * WP;
-                        snap[(ys % g.nsnap) * W + xl] = qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0);
+                        snap[(sf == 0 ? g.nsnap - 1 : sf - 1) * W + xl] =
+                            qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0);
                     }
                 } else if (tid < 2 * W && yf >= 0 && yf < h) {
                     const int b = sb[yf * W + xl];
                     const double* const qr = Qrow + b * WP;
                     const double sc = (qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0)) -
-                                      snap[(yf % g.nsnap) * W + xl];
+                                      snap[sf * W + xl];
                     part[yf * W + xl] = pold + fmaf((float)sc, scale, 0.f);
                 }
+                sf = sf + 1 == g.nsnap ? 0 : sf + 1;
             }
         }
         __syncthreads();
@@ -449,8 +494,9 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 int sample_stride(int h, int w, int budget);
 
 template <int T>
-static int s7_total(Score7Geom& g) {
-    score7_layout<T>(g);
+static int s7_total(Score7Geom& g, bool gt) {
+    if (gt) score7_layout<T, true>(g);
+    else score7_layout<T, false>(g);
     return g.total;
 }
 
@@ -487,16 +533,21 @@ static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
         g.srow = (g.nsamp + 3) & ~3;
         if (g.nsamp > 4096) return QFCA_ERR_UNSUPPORTED;
     }
+    g.moff = 0u - 4u * 0x4B000000u;
     size_t bytes = 0;
-    switch (t) {
-#define S7C(TT) case TT: bytes = s7_total<TT>(g); break;
-        S7C(17) S7C(19) S7C(21) S7C(23) S7C(25) S7C(27) S7C(29) S7C(31) S7C(33) S7C(35)
-        S7C(37) S7C(39) S7C(41) S7C(43) S7C(45) S7C(47) S7C(49) S7C(51) S7C(53) S7C(55)
-        S7C(57) S7C(59) S7C(61) S7C(63) S7C(65)
+    for (int gt = t <= S7_GT_MAXT ? 1 : 0; gt >= 0; --gt) {
+        g.gt = gt;
+        switch (t) {
+#define S7C(TT) case TT: bytes = s7_total<TT>(g, gt != 0); break;
+            S7C(17) S7C(19) S7C(21) S7C(23) S7C(25) S7C(27) S7C(29) S7C(31) S7C(33) S7C(35)
+            S7C(37) S7C(39) S7C(41) S7C(43) S7C(45) S7C(47) S7C(49) S7C(51) S7C(53) S7C(55)
+            S7C(57) S7C(59) S7C(61) S7C(63) S7C(65)
 #undef S7C
-        default: return QFCA_ERR_UNSUPPORTED;
+            default: return QFCA_ERR_UNSUPPORTED;
+        }
+        if (bytes <= (size_t)S7_SMEM_MAX - 4096) break;  // + static TH
     }
-    if (bytes > (size_t)S7_SMEM_MAX - 4096) return QFCA_ERR_UNSUPPORTED;  // + static TH
+    if (bytes > (size_t)S7_SMEM_MAX - 4096) return QFCA_ERR_UNSUPPORTED;
     int groups = groups_hint;
     if (groups <= 0) groups = balanced_groups(images, C, 1, 1);
     groups = groups < 1 ? 1 : (groups > C ? C : groups);
@@ -534,7 +585,7 @@ int launch_score7(const void* bins, int bins_bytes, const float* lo, const float
     void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score7Geom,
                  uint32_t*, float*) = nullptr;
     switch (t) {
-#define S7K(TT) case TT: kern = k_score7<TT>; break;
+#define S7K(TT) case TT: kern = g.gt ? k_score7<TT, (TT <= S7_GT_MAXT)> : k_score7<TT, false>; break;
         S7K(17) S7K(19) S7K(21) S7K(23) S7K(25) S7K(27) S7K(29) S7K(31) S7K(33) S7K(35)
         S7K(37) S7K(39) S7K(41) S7K(43) S7K(45) S7K(47) S7K(49) S7K(51) S7K(53) S7K(55)
         S7K(57) S7K(59) S7K(61) S7K(63) S7K(65)
