@@ -96,7 +96,7 @@ static void score7_layout(Score7Geom& g) {
     off = (int)((uend + 15) & ~15LL);
     g.o_erow = take(16LL * S7_EST * 4);
     g.o_xmap = take((long long)WP * 4);
-    g.o_stab = take((long long)g.S * 16);
+    g.o_stab = take((long long)(g.S + 1) * 16);
     g.o_misc = take(1024);
     g.total = off;
 }
@@ -140,19 +140,19 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 
     // ---- per-CTA tables
     for (int p = tid; p < WP; p += S7_THREADS) xmap[p] = map_coord(p - R, W, g.pad);
-    // stream row s = padded centre row, centre c = map(s - R): how the window
-    // counts move from row s - 1 (x = +1 / -1: slide, add / remove row;
-    // x = 0: recount all rows around the centre)
-    for (int s = tid; s < g.S; s += S7_THREADS) {
+    // stream row s = padded centre row, centre c = map(s - R).  For h >= 2 the
+    // centre moves by one row (mod h for wrap) at every s >= 1, so the window
+    // slides: (.z, .w) = scratch offsets of the entering / leaving row; entry
+    // S is a harmless pad for the one-ahead prefetch
+    for (int s = tid; s <= g.S; s += S7_THREADS) {
+        int add = 0, rem = 0;
         const int c = map_coord(s - R, h, g.pad);
-        int mode = 0, add = 0, rem = 0;
-        if (s > 0) {
+        if (s > 0 && s < g.S) {
             const int cp = map_coord(s - 1 - R, h, g.pad);
-            if (c == cp + 1) { mode = 1; add = map_coord(c + R, h, g.pad); rem = map_coord(cp - R, h, g.pad); }
-            else if (c == cp - 1) { mode = 1; add = map_coord(c - R, h, g.pad); rem = map_coord(cp + R, h, g.pad); }
-            else if (c == cp) { mode = 2; }
+            if (c == cp - 1) { add = map_coord(c - R, h, g.pad); rem = map_coord(cp + R, h, g.pad); }
+            else { add = map_coord(c + R, h, g.pad); rem = map_coord(cp - R, h, g.pad); }
         }
-        stab[s] = make_int4(c, mode, add * 4 * W, rem * 4 * W);  // scratch offsets
+        stab[s] = make_int4(c, 1, add * 4 * W, rem * 4 * W);
     }
     for (int b = tid; b < 256; b += S7_THREADS) {
         uint32_t v[4];
@@ -373,26 +373,26 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             const uint32_t gaddr =
                 (uint32_t)__cvta_generic_to_shared(sm + g.o_gt) + grp * 4 * GP * 4 + g.moff;
             int sf = (g.nsnap - 2 * R) % g.nsnap;  // snapshot slot of row s - 2R
-            int4 st = stab[0];
+            {  // the first centre's window: all its rows
+                const int c0 = stab[0].x;
+                for (int dy = -R; dy <= R; ++dy) {
+                    const uint32_t wa = rwt[(size_t)map_coord(c0 + dy, h, g.pad) * 4 * W];
+                    alo += wa & 0x00FF00FFu;
+                    ahi += (wa >> 8) & 0x00FF00FFu;
+                }
+                const int4 st = stab[1];
+                na = rwt[st.z];
+                nr = rwt[st.w];
+            }
+            const bool fin_warp = warp >= W / 32 && warp < 2 * W / 32;  // finished-pixel roles
             for (int s = 0; s < g.S; ++s) {
-                // ---- vertical slide (or recount) of the window counts
-                if (st.y == 1) {
+                // ---- vertical slide of the window counts (rows prefetched one ahead)
+                if (s > 0) {
                     alo += (na & 0x00FF00FFu) - (nr & 0x00FF00FFu);
                     ahi += ((na >> 8) & 0x00FF00FFu) - ((nr >> 8) & 0x00FF00FFu);
-                } else if (st.y == 0) {
-                    alo = ahi = 0;
-                    for (int dy = -R; dy <= R; ++dy) {
-                        const uint32_t wa = rwt[(size_t)map_coord(st.x + dy, h, g.pad) * 4 * W];
-                        alo += wa & 0x00FF00FFu;
-                        ahi += (wa >> 8) & 0x00FF00FFu;
-                    }
-                }
-                if (s + 1 < g.S) {  // prefetch the next row's entering / leaving windows
-                    st = stab[s + 1];
-                    if (st.y == 1) {
-                        na = rwt[st.z];
-                        nr = rwt[st.w];
-                    }
+                    const int4 st = stab[s + 1];
+                    na = rwt[st.z];
+                    nr = rwt[st.w];
                 }
                 // ---- E of the 4 bins (G from the shared PJ prefix table)
                 const int a0 = (int)(alo & 0xFFFFu), a1 = (int)(ahi & 0xFFFFu),
@@ -436,7 +436,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 for (int j = 0; j < 4; ++j) Erow[(grp * 4 + j) * EST + x] = E[j];
                 // partial map of the pixel that finishes at this row (fetched early)
                 const int yf = s - 2 * R;
-                if (tid >= W && tid < 2 * W && yf >= 0 && yf < h) pold = part[yf * W + xl];
+                if (fin_warp && yf >= 0 && yf < h) pold = part[yf * W + xl];
                 __syncthreads();  // E row complete; the previous row's Q readers done
                 // ---- one warp per bin: the padded E row's prefix (fp32 within the
                 //      row), added to the fp64 running prefixes Q
