@@ -42,6 +42,7 @@ constexpr int S7_W = 128;
 constexpr int S7_EST = S7_W + 2;  // E row stride (conflict-free stores)
 constexpr int S7_SMEM_MAX = 227 * 1024;
 constexpr int S7_GT_MAXT = 43;  // largest T whose 16 x (T^2 + 1) G table is built
+constexpr int S7_NFL = 4;       // stream rows between fp32 -> fp64 prefix flushes
 
 struct Score7Geom {
     int h, n_bins, pad, C, groups, cpg;
@@ -49,7 +50,7 @@ struct Score7Geom {
     int nsnap;  // snapshot rows 2R + 2
     // in-kernel reference (median-quan, quantize.py:150-200): sample grid
     int fref, stride, nsy, nsx, nsamp, srow;
-    int o_sb, o_pj, o_gt, o_erow, o_qrow, o_prow, o_snap, o_sa, o_xmap, o_stab, o_misc, total;
+    int o_sb, o_pj, o_gt, o_erow, o_qrow, o_qf, o_prow, o_snap, o_sa, o_xmap, o_stab, o_misc, total;
     int gt;         // 1: the G_i(v) table (T <= 43 and it fits), else G from PJ
     uint32_t moff;  // G-table address of the magic float 2^23 + v is base + 4 v
 };
@@ -82,6 +83,7 @@ static void score7_layout(Score7Geom& g) {
     g.o_pj = take((long long)(T * T + 1) * 4);
     g.o_gt = GT ? take(16LL * (T * T + 1) * 4) : 0;
     g.o_qrow = take(16LL * WP * 8);
+    g.o_qf = take(16LL * WP * 4);
     g.o_snap = take((long long)g.nsnap * S7_W * 8);
     const int p4end = off;
     g.o_prow = ubase;  // one padded prefix row per warp (RW phase)
@@ -118,7 +120,8 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     uint8_t* const sb = sm + g.o_sb;
     float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
     float* const Erow = reinterpret_cast<float*>(sm + g.o_erow);     // [16][EST]
-    double* const Qrow = reinterpret_cast<double*>(sm + g.o_qrow);   // [16][WP]
+    double* const Qrow = reinterpret_cast<double*>(sm + g.o_qrow);   // [16][WP] (flushed)
+    float* const Qf = reinterpret_cast<float*>(sm + g.o_qf);         // [16][WP] (recent)
     uint4* const Prow = reinterpret_cast<uint4*>(sm + g.o_prow);     // [16 warps][WP]
     double* const snap = reinterpret_cast<double*>(sm + g.o_snap);   // [nsnap][W]
     int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
@@ -309,6 +312,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             sPJ[qq + 1] = (float)a;
         }
         if (tid < W) snap[tid] = 0.0;  // row 0's window starts before the stream
+        for (int i = tid; i < 16 * WP; i += S7_THREADS) Qrow[i] = 0.0;
         __syncthreads();
         if (warp == 0) {
             float carry = 0.f;
@@ -365,9 +369,15 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             // neighbour lane's top lane
             uint32_t alo = 0, ahi = 0;
             uint32_t na = 0, nr = 0;  // entering / leaving row windows of row s (prefetched)
-            double q[CPL];  // scan lane's running column prefixes Q(s, p) of bin `warp`
+            // scan lane's running column prefixes Q(s, p) of bin `warp`: fp64 up to
+            // the last flush + fp32 since (at most S7_NFL rows of row prefixes)
+            double q[CPL];
+            float qf[CPL];
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) q[k] = 0.0;
+            for (int k = 0; k < CPL; ++k) {
+                q[k] = 0.0;
+                qf[k] = 0.f;
+            }
             const int xl = tid & (W - 1);  // snapshot / finish roles: tid < 2 W
             float pold = 0.f;
             const uint32_t gaddr =
@@ -458,30 +468,37 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     }
                     off -= run;
                     double* const qr = Qrow + warp * WP;
+                    float* const qfr = Qf + warp * WP;
+                    const bool flush = (s % S7_NFL) == S7_NFL - 1;
 #pragma unroll
                     for (int k = 0; k < CPL; ++k) {
                         const int p = lane * CPL + k;
-                        q[k] += (double)(rp[k] + off);
-                        if (p < WP) qr[p] = q[k];
+                        qf[k] += rp[k] + off;
+                        if (flush) {
+                            q[k] += (double)qf[k];
+                            qf[k] = 0.f;
+                            if (p < WP) qr[p] = q[k];
+                        }
+                        if (p < WP) qfr[p] = qf[k];
                     }
                 }
                 __syncthreads();  // Q(s, .) published
                 // ---- snapshots (pixels whose window starts at s + 1) and the
                 //      pixels whose window ended at s
                 // (slots: row y -> y mod nsnap; row s + 1's slot is row s - 2R's - 1)
+                // D_b(s, x) = Q_b(s, x + 2R) - Q_b(s, x - 1), own bin b
+                auto dwin = [&](int b) -> double {
+                    const double* const qr = Qrow + b * WP;
+                    const float* const qfr = Qf + b * WP;
+                    const double d64 = qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0);
+                    const float d32 = qfr[xl + 2 * R] - (xl > 0 ? qfr[xl - 1] : 0.f);
+                    return d64 + (double)d32;
+                };
                 if (tid < W) {
                     const int ys = s + 1;
-                    if (ys < h) {
-                        const int b = sb[ys * W + xl];
-                        const double* const qr = Qrow + b * WP;
-                        snap[(sf == 0 ? g.nsnap - 1 : sf - 1) * W + xl] =
-                            qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0);
-                    }
+                    if (ys < h) snap[(sf == 0 ? g.nsnap - 1 : sf - 1) * W + xl] = dwin(sb[ys * W + xl]);
                 } else if (tid < 2 * W && yf >= 0 && yf < h) {
-                    const int b = sb[yf * W + xl];
-                    const double* const qr = Qrow + b * WP;
-                    const double sc = (qr[xl + 2 * R] - (xl > 0 ? qr[xl - 1] : 0.0)) -
-                                      snap[sf * W + xl];
+                    const double sc = dwin(sb[yf * W + xl]) - snap[sf * W + xl];
                     part[yf * W + xl] = pold + fmaf((float)sc, scale, 0.f);
                 }
                 sf = sf + 1 == g.nsnap ? 0 : sf + 1;

@@ -40,6 +40,8 @@ def test_score7_vs_oracle(t, h, n, pad):
     ref, img, _ = O.detect(x[0], n_bins=n, patch_size=t, pad=pad)
     got = res.scores[0].cpu().numpy()
     assert np.abs(ref).max() > 0
+    print(f"T={t} h={h} N={n} {pad}: max|err| / max|ref| = "
+          f"{np.abs(got - ref).max() / np.abs(ref).max():.2e}")
     assert np.abs(got - ref).max() <= TOL * np.abs(ref).max()
     assert abs(float(res.image_scores[0]) - img) <= TOL * np.abs(ref).max()
 
