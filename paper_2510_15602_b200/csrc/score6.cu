@@ -45,7 +45,7 @@ constexpr int S6_BAND = 8;                 // H1 steps per band (x 4 quarters = 
 constexpr int S6_SLOTS = 4 * S6_BAND;      // staging rows
 constexpr int S6_SEG = 8;                  // H2 columns per task
 constexpr int S6_SMEM_MAX = 227 * 1024;
-constexpr int S6_MAXNB = 76;               // table bins of 5 passes (N <= 76)
+constexpr int S6_MAXNB = 256;              // bins (17 passes)
 // Vb row pitch: the 128 columns plus mirrored copies of the R <= 7 edge
 // columns on both sides (padded to a multiple of 32 floats, so lanes reading
 // different bins' rows at consecutive columns stay in distinct banks)
@@ -58,7 +58,7 @@ struct Score6Geom {
     int qrows;  // H1 rows per quarter, ceil(h / 4)
     int fref, stride, sshift, nsx, nsamp;  // sshift = log2(stride) or -1
     int dbsb;   // bins double-buffered (next channel prefetched)
-    int passes, nbt;  // bin passes (16 lanes each, 15 new bins after the first), table bins
+    int passes;  // bin passes (16 lanes each, 15 new bins after the first)
     uint32_t moff;
     int o_sb, o_sa, o_stg, o_gt, o_th, o_xmap, o_rmap, o_stab, o_pj, o_misc, total;
 };
@@ -116,7 +116,7 @@ static void score6_layout(Score6Geom& g) {
     const long long vb = 2LL * CH * 16 * S6_VP * 4;
     g.o_sa = take(sa > vb ? sa : vb);
     g.o_stg = take((long long)S6_SLOTS * wpp * 16);
-    g.o_gt = take((long long)g.nbt * GP * 4);
+    g.o_gt = take(16LL * GP * 4);  // the current pass's 16 bins
     g.o_pj = take((long long)GP * 4);
     g.o_th = take(256 * 16);
     g.o_xmap = take((long long)(S6_W + 2 * R) * 4);
@@ -124,7 +124,7 @@ static void score6_layout(Score6Geom& g) {
     const int n_chunks = (g.S + P - 1) / P;
     g.o_rmap = take((long long)(n_chunks * P + 2 * CH) * 4);
     g.o_stab = take((long long)g.h * 8);
-    g.o_misc = take(2048);  // scale, V, search brackets / mids / per-warp counts
+    g.o_misc = take(2048);  // scale, V[256], search brackets / mids / per-warp counts
     g.total = off;
 }
 
@@ -155,10 +155,10 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     int2* const stab = reinterpret_cast<int2*>(sm + g.o_stab);
     float* const sscale = reinterpret_cast<float*>(sm + g.o_misc);      // [1]
     int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);         // [S6_MAXNB]
-    int* const blo = reinterpret_cast<int*>(sm + g.o_misc + 352);       // [16]
-    int* const bhi = reinterpret_cast<int*>(sm + g.o_misc + 416);       // [16]
-    uint8_t* const qm8 = sm + g.o_misc + 480;                            // [16]
-    uint32_t* const cnt = reinterpret_cast<uint32_t*>(sm + g.o_misc + 512);  // [16 warps][8]
+    int* const blo = reinterpret_cast<int*>(sm + g.o_misc + 1088);      // [16]
+    int* const bhi = reinterpret_cast<int*>(sm + g.o_misc + 1152);      // [16]
+    uint8_t* const qm8 = sm + g.o_misc + 1216;                           // [16]
+    uint32_t* const cnt = reinterpret_cast<uint32_t*>(sm + g.o_misc + 1280);  // [16 warps][8]
 
     const int tid = threadIdx.x;
     const int h = g.h;
@@ -465,19 +465,22 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             }
         }
         __syncthreads();
-        for (int idx = tid; idx < g.nbt * GP; idx += S6_THREADS) {
-            const int i = idx / GP, v = idx - i * GP;
-            float vm = 0.f, d = 0.f;
-            if (i < g.n_bins) {
-                const int vmi = i > 0 ? sV[i - 1] : 0;
-                vm = (float)vmi;
-                d = 2.f * ((float)i * vm - sPJ[vmi]);
+        // G_i(v) of the pass's 16 bins tb .. tb + 15 (rebuilt per bin pass)
+        auto build_gt = [&](int tb) {
+            for (int idx = tid; idx < 16 * GP; idx += S6_THREADS) {
+                const int j = idx / GP, v = idx - j * GP, i = tb + j;
+                float vm = 0.f, d = 0.f;
+                if (i < g.n_bins) {
+                    const int vmi = i > 0 ? sV[i - 1] : 0;
+                    vm = (float)vmi;
+                    d = 2.f * ((float)i * vm - sPJ[vmi]);
+                }
+                const float fv = (float)v;
+                const float nu = fmaf((float)i, fv, -sPJ[v]);
+                GT[idx] = fv < vm ? nu : d - nu;
             }
-            const float fv = (float)v;
-            const float nu = fmaf((float)i, fv, -sPJ[v]);
-            GT[idx] = fv < vm ? nu : d - nu;
-        }
-        __syncthreads();  // GT ready; SA4 free (Vb aliases it)
+            __syncthreads();  // GT ready; SA4 free (Vb aliases it)
+        };
 
         // ======== phase 4: E (register ring) + own-bin box, one barrier per sub-chunk.
         // The count rows of sub-chunk u + 2 are copied (cp.async) from the scratch
@@ -486,7 +489,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         // is in [bin_lo, bin_hi]; its lanes are bins tb .. tb + 15.
         auto phase4 = [&](int tb, int bin_lo, int bin_hi) {
             const uint32_t gaddr =
-                (uint32_t)__cvta_generic_to_shared(GT + (tb + grp * 4) * GP) + g.moff;
+                (uint32_t)__cvta_generic_to_shared(GT + grp * 4 * GP) + g.moff;
             uint32_t* const cring = reinterpret_cast<uint32_t*>(STG);
             constexpr int SLOT = CH * 4 * W;  // uint32 per slot
             const int n_sub = n_chunks * NSUB;
@@ -660,6 +663,8 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 build_th(15 * p);
                 phase1(false);
             }
+            if (MP && p != npass - 1) __syncthreads();  // the previous pass's GT readers done
+            build_gt(15 * p);
             phase4(15 * p, p == 0 ? 0 : 15 * p + 1, min(15 * p + 15, g.n_bins - 1));
         }
         __syncthreads();
@@ -709,7 +714,7 @@ static int s6_total(Score6Geom& g) {
 
 static int score6_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
                        int pad, int budget, bool has_ref, Score6Geom* out, size_t* smem_out) {
-    if (w != S6_W || t < 1 || t > 15 || (t & 1) == 0 || n_bins < 1 || n_bins > 64)
+    if (w != S6_W || t < 1 || t > 15 || (t & 1) == 0 || n_bins < 1 || n_bins > S6_MAXNB)
         return QFCA_ERR_UNSUPPORTED;
     if (h < 1 || h > 256 || (h * w) % 16) return QFCA_ERR_UNSUPPORTED;
     if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
@@ -722,7 +727,6 @@ static int score6_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.moff = 0u - 4u * 0x4B000000u;
     // pass p covers lanes 15p .. 15p + 15: bins 0..15, then 15 new bins per pass
     g.passes = n_bins <= 16 ? 1 : 1 + (n_bins - 16 + 14) / 15;
-    g.nbt = 15 * (g.passes - 1) + 16;
     if (!has_ref) {
         if (t * t > 255 || budget < 1) return QFCA_ERR_UNSUPPORTED;
         g.fref = 1;

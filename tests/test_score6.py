@@ -85,10 +85,12 @@ def test_score6_vs_oracle_where_v3_cannot(t, pad):
 
 @pytest.mark.parametrize("n,t,pad", [(17, 9, "reflect"), (31, 9, "reflect"), (32, 9, "wrap"),
                                      (46, 5, "reflect"), (64, 9, "reflect"), (64, 3, "wrap"),
-                                     (48, 11, "reflect")])
+                                     (48, 11, "reflect"), (100, 9, "reflect"),
+                                     (128, 9, "wrap"), (256, 9, "reflect"), (256, 15, "reflect")])
 def test_score6_bin_passes_vs_oracle(n, t, pad):
     """N > 16 on v6: bins in passes of 16 thermometer lanes (15 new bins per
-    pass after the first); maps match the oracle, the detect path uses v6."""
+    pass after the first, the G table rebuilt per pass, up to N = 256); maps
+    match the oracle, the detect path uses v6."""
     import torch
     import paper_2510_15602_b200 as Q
     from paper_2510_15602_b200 import _native as N
