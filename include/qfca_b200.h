@@ -129,8 +129,8 @@ int qfca_channel_sum(const double* score, int64_t images, int32_t channels, int6
 int qfca_count_used(const float* lo, const float* hi, int64_t images, int32_t channels,
                     int32_t* used, void* stream);
 
-/* which fused scoring kernel qfca_score picks for this shape (host-only):
- * 4 / 3 / 2 / 1 = score4.cu / score3.cu / score2.cu / score.cu, -1 none. */
+/* which fused scoring kernel qfca_detect / qfca_score_ex (with a scratch) pick
+ * for this shape (host-only): N = scoreN.cu (1 = score.cu), -1 none. */
 int qfca_score_version(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
                        int32_t channels, int64_t images, int32_t pad, int32_t sample_budget,
                        int32_t with_reference);
@@ -142,12 +142,12 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
                       int64_t images, int32_t groups_hint, int32_t pad, int32_t sample_budget,
                       int32_t with_reference);
 
-/* select the fused scoring kernel: 0 = auto (the first that applies of v4
- * score4.cu -- plane-resident windows, T <= 11, w in {32, 64, 128}, stride-1
- * sampling when it selects the reference; v3 score3.cu -- pipelined
- * warp-specialised, T <= 15; v2 score2.cu; v1 score.cu -- any shape),
- * 1..4 = force that version (unsupported shapes then return status 3).
- * Process-global. */
+/* select the fused scoring kernel: 0 = auto, the first that applies of
+ * v6 score6.cu (128-wide planes / tiles, T <= 15, N <= 256; needs the
+ * caller's scratch), v7 score7.cu (128-wide, T = 17..65, N <= 16; scratch),
+ * v4 score4.cu (planes <= 64 wide), v3 score3.cu, v5 score5.cu (any odd T),
+ * v2 score2.cu, v1 score.cu (any shape); 1..7 = force that version
+ * (unsupported shapes then return status 3).  Process-global. */
 int qfca_set_score_kernel(int32_t version);
 
 /* THE HOT PATH: _channel_score_kernel + channel accumulation
@@ -162,8 +162,9 @@ int qfca_score(const void* bins, int32_t bins_bytes, const float* lo, const floa
                int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
                int32_t groups, float* partial, void* stream);
 
-/* qfca_score with a caller-owned global scratch: the 128-column kernel (v6,
- * csrc/score6.cu) keeps each plane's window counts in an L2-resident scratch;
+/* qfca_score with a caller-owned global scratch: the 128-column kernels (v6
+ * csrc/score6.cu, v7 csrc/score7.cu) keep each plane's window counts in an
+ * L2-resident scratch;
  * qfca_score_scratch_bytes gives its size for a configuration (0: the chosen
  * kernel needs none, -1: unsupported) and qfca_score_groups_ex the channel
  * groups of the kernel chosen with (with_scratch = 1) or without a scratch. */
