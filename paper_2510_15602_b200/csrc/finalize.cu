@@ -91,12 +91,13 @@ __global__ void k_image_score(const double* __restrict__ scores, int h, int w, i
 
 // bilinear resize with half-pixel centres (tensor_io.py:127-151), fp64 math,
 // float32 result.  Source is fp64 (the score map).  One CTA per (image, band
-// of UP_ROWS output rows): the column weights are computed once per CTA into
-// shared memory, the row weights once per row, so each output costs four
-// loads and the six rounded products / three sums of the reference formula.
+// of UP_ROWS output rows, UP_CHUNK columns); thread = 4 consecutive columns
+// (weights in registers), one float4 store per output row; each output costs
+// four (cached) loads and the six rounded products / three sums of the
+// reference formula.
 constexpr int UP_THREADS = 256;
 constexpr int UP_ROWS = 32;
-constexpr int UP_CHUNK = 1024;  // output columns per CTA (shared weight table)
+constexpr int UP_CHUNK = 4 * UP_THREADS;  // output columns per CTA (4 per thread)
 
 __device__ __forceinline__ void up_coord(int o, int n, int on, int& i0, int& i1, double& f) {
     const double s = ((double)o + 0.5) * (double)n / (double)on - 0.5;
@@ -109,8 +110,6 @@ __device__ __forceinline__ void up_coord(int o, int n, int on, int& i0, int& i1,
 __global__ void __launch_bounds__(UP_THREADS)
 k_upsample(const double* __restrict__ in, int h, int w, int oh, int ow, int bands, int chunks,
            float* __restrict__ out) {
-    __shared__ int sx0[UP_CHUNK], sx1[UP_CHUNK];
-    __shared__ double sfx[UP_CHUNK], sgx[UP_CHUNK];
     __shared__ int sy0[UP_ROWS], sy1[UP_ROWS];
     __shared__ double sfy[UP_ROWS], sgy[UP_ROWS];
     const int b = blockIdx.x / (bands * chunks);
@@ -119,16 +118,6 @@ k_upsample(const double* __restrict__ in, int h, int w, int oh, int ow, int band
     const int oy0 = band * UP_ROWS, nrows = min(oh, oy0 + UP_ROWS) - oy0;
     const double* p = in + (int64_t)b * h * w;
     float* o = out + (int64_t)b * oh * ow + cx0;
-    // column and row weights once per CTA (fp64 divisions are the costly part)
-    for (int i = threadIdx.x; i < cw; i += UP_THREADS) {
-        int x0, x1;
-        double fx;
-        up_coord(cx0 + i, w, ow, x0, x1, fx);
-        sx0[i] = x0;
-        sx1[i] = x1;
-        sfx[i] = fx;
-        sgx[i] = 1.0 - fx;
-    }
     for (int i = threadIdx.x; i < nrows; i += UP_THREADS) {
         int y0, y1;
         double fy;
@@ -138,19 +127,53 @@ k_upsample(const double* __restrict__ in, int h, int w, int oh, int ow, int band
         sfy[i] = fy;
         sgy[i] = 1.0 - fy;
     }
+    // this thread's 4 consecutive output columns: weights in registers (the
+    // fp64 divisions once per CTA), then one float4 per output row
+    const int c0 = 4 * threadIdx.x;
+    int x0[4], x1[4];
+    double fx[4], gx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ox = min(c0 + k, cw - 1);
+        up_coord(cx0 + ox, w, ow, x0[k], x1[k], fx[k]);
+        gx[k] = 1.0 - fx[k];
+    }
     __syncthreads();
-    const int per = nrows * cw;
-    for (int e = threadIdx.x; e < per; e += UP_THREADS) {
-        const int r = e / cw, ox = e - r * cw;
-        const double* r0 = p + (int64_t)sy0[r] * w;
-        const double* r1 = p + (int64_t)sy1[r] * w;
-        const int x0 = sx0[ox], x1 = sx1[ox];
-        const double fx = sfx[ox], gx = sgx[ox];
-        // explicit rounding (no FMA contraction) to match NumPy bit for bit
-        const double top = __dadd_rn(__dmul_rn(__ldg(r0 + x0), gx), __dmul_rn(__ldg(r0 + x1), fx));
-        const double bot = __dadd_rn(__dmul_rn(__ldg(r1 + x0), gx), __dmul_rn(__ldg(r1 + x1), fx));
-        o[(int64_t)(oy0 + r) * ow + ox] =
-            (float)__dadd_rn(__dmul_rn(top, sgy[r]), __dmul_rn(bot, sfy[r]));
+    if (c0 >= cw) return;
+    const bool vec = c0 + 4 <= cw && ((ow | cx0) & 3) == 0;
+    // the horizontal interpolations of the two source rows are shared by every
+    // output row between the same pair (8 rows at 8x): recomputed only when the
+    // pair changes (CTA-uniform), so an output row costs the vertical blend only
+    int py0 = -1, py1 = -1;
+    double top[4], bot[4];
+    for (int r = 0; r < nrows; ++r) {
+        const int y0 = sy0[r], y1 = sy1[r];
+        if (y0 != py0 || y1 != py1) {
+            const double* r0 = p + (int64_t)y0 * w;
+            const double* r1 = p + (int64_t)y1 * w;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // explicit rounding (no FMA contraction) to match NumPy bit for bit
+                top[k] = __dadd_rn(__dmul_rn(__ldg(r0 + x0[k]), gx[k]),
+                                   __dmul_rn(__ldg(r0 + x1[k]), fx[k]));
+                bot[k] = __dadd_rn(__dmul_rn(__ldg(r1 + x0[k]), gx[k]),
+                                   __dmul_rn(__ldg(r1 + x1[k]), fx[k]));
+            }
+            py0 = y0;
+            py1 = y1;
+        }
+        const double fy = sfy[r], gy = sgy[r];
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = (float)__dadd_rn(__dmul_rn(top[k], gy), __dmul_rn(bot[k], fy));
+        float* const orow = o + (int64_t)(oy0 + r) * ow + c0;
+        if (vec) {
+            *reinterpret_cast<float4*>(orow) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (c0 + k < cw) orow[k] = v[k];
+        }
     }
 }
 
