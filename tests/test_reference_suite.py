@@ -4,7 +4,9 @@ this package's drop-in API on the GPU.  Left out: `_lower_median` (a private
 NumPy helper), the PGM writer (out of scope) and the continuous-FCA
 convergence test (its oracle lives in the reference's tests/oracles.py; the
 quantized path is pinned to the reference's own outputs by the goldens).
-The naive counting oracle of test_patch_histograms_match_counting_oracle is
+The transport tests follow pkg/tests/test_transport.py:39-127 (their sorted-
+multiset oracle restated in a few lines).  The naive counting oracle of
+test_patch_histograms_match_counting_oracle is
 the C oracle's patch histograms (pinned to reference goldens)."""
 
 import math
@@ -328,3 +330,98 @@ def test_upsample_scores_shape():
     assert up.shape == (64, 64)
     np.testing.assert_allclose(up.reshape(16, 4, 16, 4).mean(axis=(1, 3)).mean(), s.mean(),
                                atol=1e-2)
+
+
+# ------------------------------------------------------------ test_transport.py
+
+def _random_equal_mass_instance(rng, max_bins=32, max_weight=8):
+    n = int(rng.integers(1, max_bins + 1))
+    p = rng.integers(0, max_weight + 1, n).astype(np.float64)
+    r = rng.integers(0, max_weight + 1, n).astype(np.float64)
+    diff = p.sum() - r.sum()
+    if diff > 0:
+        r[rng.integers(0, n)] += diff
+    elif diff < 0:
+        p[rng.integers(0, n)] += -diff
+    if p.sum() == 0:
+        p[0] += 1
+        r[0] += 1
+    q = np.cumsum(rng.random(n) + 1e-3)
+    return p, r, q
+
+
+def _oracle_bin_errors(p, r, q):
+    """Per-bin duplicate-averaged rank errors of the expanded sorted multisets
+    (the reference tests' sorted_mismatch_oracle + expand_histogram)."""
+    xs = np.repeat(q, p.astype(int))
+    ys = np.repeat(q, r.astype(int))
+    errs = np.abs(xs - ys)
+    out = np.zeros(p.size)
+    pos = 0
+    for i in range(p.size):
+        c = int(p[i])
+        if c:
+            out[i] = errs[pos:pos + c].mean()
+            pos += c
+    return out
+
+
+def _w1(p, r, q):
+    return float(np.sum(np.abs(np.cumsum(p) - np.cumsum(r))[:-1] * np.diff(q)))
+
+
+def test_transport_hand_examples_and_errors():
+    from paper_2510_15602_b200 import MassError, quantized_mismatch
+    np.testing.assert_array_equal(
+        quantized_mismatch(np.array([3.0, 2.0, 1.0]), np.array([3.0, 2.0, 1.0]),
+                           np.array([0.0, 1.0, 2.0])), 0.0)
+    np.testing.assert_allclose(quantized_mismatch([2, 1], [1, 2], [0, 1]), [0.5, 0.0])
+    np.testing.assert_allclose(quantized_mismatch([3, 0], [0, 3], [0, 2]), [2.0, 0.0])
+    e = quantized_mismatch([0, 2, 0, 2], [1, 1, 1, 1], [0.0, 1.0, 2.0, 3.0])
+    assert e[0] == 0.0 and e[2] == 0.0
+    with pytest.raises(MassError):
+        quantized_mismatch([1, 1], [1, 2], [0, 1])
+    with pytest.raises(ValueError):
+        quantized_mismatch([1, 1], [1, 1], [1, 1])
+
+
+def test_transport_equivalence_iteration_bound_and_cost_identity():
+    from paper_2510_15602_b200 import quantized_mismatch
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        p, r, q = _random_equal_mass_instance(rng)
+        e, iters = quantized_mismatch(p, r, q, return_iterations=True)
+        assert iters <= 2 * p.size - 1
+        np.testing.assert_allclose(e, _oracle_bin_errors(p, r, q), rtol=1e-9, atol=1e-12)
+        assert float(np.sum(e * p)) == pytest.approx(_w1(p, r, q), rel=1e-9, abs=1e-12)
+
+
+def test_transport_scale_equivariance_and_mass_invariance():
+    from paper_2510_15602_b200 import quantized_mismatch
+    p, r, q = _random_equal_mass_instance(np.random.default_rng(9))
+    e1 = quantized_mismatch(p, r, q)
+    np.testing.assert_allclose(quantized_mismatch(p, r, 3.5 * q), 3.5 * e1, rtol=1e-12)
+    p, r, q = _random_equal_mass_instance(np.random.default_rng(10))
+    np.testing.assert_allclose(quantized_mismatch(7.0 * p, 7.0 * r, q),
+                               quantized_mismatch(p, r, q), rtol=1e-12)
+
+
+def test_transport_batch_kernel_matches_scalar():
+    from paper_2510_15602_b200 import mismatch_batch, quantized_mismatch
+    rng = np.random.default_rng(11)
+    n = 16
+    q = np.cumsum(rng.random(n) + 0.01)
+    r = rng.integers(0, 9, n).astype(np.float64)
+    r[0] += 1
+    rows = []
+    for _ in range(50):
+        p = rng.integers(0, 9, n).astype(np.float64)
+        if p.sum() == 0:
+            p[0] = 1.0
+        rows.append(p)
+    pb = np.ascontiguousarray(np.array(rows))
+    out = np.empty_like(pb)
+    mismatch_batch(pb, r, q, out)
+    for p, e in zip(rows, out):
+        np.testing.assert_allclose(e, quantized_mismatch(p, r * (p.sum() / r.sum()), q),
+                                   rtol=1e-9, atol=1e-12)
