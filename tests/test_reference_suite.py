@@ -1,5 +1,5 @@
-"""The reference's own unit tests for the path (pkg/tests/test_quantize.py and
-pkg/tests/test_scoring.py), with the same inputs and assertions, run against
+"""The reference's own unit tests for the path (pkg/tests/test_quantize.py,
+test_scoring.py, test_transport.py, test_pooling.py), with the same inputs and assertions, run against
 this package's drop-in API on the GPU.  Left out: `_lower_median` (a private
 NumPy helper), the PGM writer (out of scope) and the continuous-FCA
 convergence test (its oracle lives in the reference's tests/oracles.py; the
@@ -425,3 +425,51 @@ def test_transport_batch_kernel_matches_scalar():
     for p, e in zip(rows, out):
         np.testing.assert_allclose(e, quantized_mismatch(p, r * (p.sum() / r.sum()), q),
                                    rtol=1e-9, atol=1e-12)
+
+
+# ------------------------------------------------------------ test_pooling.py
+# (the hand values and error cases are in tests/test_pooling.py)
+
+def test_box_average_k1_identity_and_naive_identities():
+    from paper_2510_15602_b200 import box_average, naive_box_average
+    p = np.random.default_rng(0).random((7, 5))
+    for pad in ("zero", "reflect"):
+        np.testing.assert_allclose(box_average(p, 1, pad), p)
+    for k in (1, 3, 5):
+        np.testing.assert_allclose(naive_box_average(np.array([[3.5]]), k, "reflect"), [[3.5]])
+    np.testing.assert_array_equal(naive_box_average(np.zeros((4, 4)), 3, "reflect"),
+                                  np.zeros((4, 4)))
+
+
+@pytest.mark.parametrize("k", [3, 9, 31])
+@pytest.mark.parametrize("pad", ["zero", "reflect"])
+def test_box_average_matches_naive_256(k, pad):
+    from paper_2510_15602_b200 import box_average, naive_box_average
+    p = np.random.default_rng(k).random((256, 256)).astype(np.float32)
+    assert np.max(np.abs(box_average(p, k, pad) - naive_box_average(p, k, pad))) <= 1e-4
+
+
+def test_box_average_linearity():
+    from paper_2510_15602_b200 import box_average
+    rng = np.random.default_rng(1)
+    x, y = rng.random((16, 16)), rng.random((16, 16))
+    lhs = box_average(2.5 * x - 1.25 * y, 5, "reflect")
+    rhs = 2.5 * box_average(x, 5, "reflect") - 1.25 * box_average(y, 5, "reflect")
+    np.testing.assert_allclose(lhs, rhs, atol=1e-10)
+
+
+@pytest.mark.parametrize("pad", ["zero", "reflect", "wrap"])
+def test_box_average_stack_matches_single(pad):
+    from paper_2510_15602_b200 import box_average, box_average_stack
+    planes = np.random.default_rng(2).random((4, 12, 10)).astype(np.float32)
+    stacked = box_average_stack(planes, 5, pad)
+    for i in range(4):
+        np.testing.assert_allclose(stacked[i], box_average(planes[i], 5, pad), atol=1e-12)
+
+
+def test_wrap_padding_is_toroidal():
+    from paper_2510_15602_b200 import box_average
+    p = np.random.default_rng(3).random((8, 8))
+    a = box_average(p, 3, "wrap")
+    b = box_average(np.roll(p, (3, 2), axis=(0, 1)), 3, "wrap")
+    np.testing.assert_allclose(np.roll(a, (3, 2), axis=(0, 1)), b, atol=1e-12)
