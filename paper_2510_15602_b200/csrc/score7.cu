@@ -411,7 +411,8 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 if (grp == 0) a_1 = 0;
                 float E[4] = {0.f, 0.f, 0.f, 0.f};
                 if (GT) {
-                    if (__any_sync(FULL, a3 != a_1)) {
+                    {  // (every warp holds bin group 0, which has mass in nearly every
+                       // window: no vote; a bin without mass gets E = 0 / 1 = 0)
                         const int av[5] = {a_1, a0, a1, a2, a3};
                         uint32_t ma = 0x4B000000u | (uint32_t)av[0];
                         uint32_t aa = gaddr + 4u * ma;
