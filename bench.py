@@ -488,12 +488,13 @@ def run_batch(args, ws, rank, local, config, size, pca_k, per_rank, mp_per_image
     peak, peak_src = peak_hbm()
     alg_launch = alg_bytes_per_image(size, pca_k > 0) * CHUNK
     achieved = alg_launch / (score_ms_launch / 1e3) / 1e9
-    traffic, issue = None, None
+    traffic, issue, kname = None, None, "k_score"
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
             traffic = tj.get("dram_bytes_per_launch")
+            kname = tj.get("kernel", kname)
             # K4 is issue-bound, not HBM-bound: its instruction-issue
             # utilisation from the same ncu capture is the kernel-quality figure
             issue = {"issue_active_frac": tj.get("issue_active_frac"), "ipc": tj.get("ipc"),
@@ -503,7 +504,7 @@ def run_batch(args, ws, rank, local, config, size, pca_k, per_rank, mp_per_image
     alg_step = alg_bytes_per_image(size, pca_k > 0) * b
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-            "kernel": "k_score (fused histogram/transport/association/channel-sum)",
+            "kernel": kname + " (fused histogram/transport/association/channel-sum)",
             "alg_bytes_per_launch": alg_launch, "images_per_launch": CHUNK,
             "kernel_ms_per_launch": score_ms_launch, "launches_per_step": len(chunks),
             "step_ms": ms_per_step, "kernel_share_of_step": score_ms_step / ms_per_step,
