@@ -19,7 +19,7 @@
 //   phase 2  the median-quan reference of all bins by lock-step binary search
 //            over SA4 (score4.cu's packed compares);
 //   phase 3  the transport tables G_i(v);
-//   phase 4  stream rows in sub-chunks of CH rows (CH divides T, so the E
+//   phase 4  stream rows in sub-chunks of CH = 4 rows (period lcm(T, CH), so the E
 //            ring stays in registers with static indices): thread (x, group
 //            g) loads its two count words straight from the scratch (loads of
 //            the next sub-chunk in flight during this one), computes E for
@@ -93,10 +93,13 @@ __host__ __device__ constexpr int s6_elem(int p) { return p + (p >> 3); }
 
 // stream rows per sub-chunk (one barrier each) and rows per unrolled period:
 // the period is a multiple of T, so the E ring keeps static register slots
+// (4 rows: one own-bin box row per bin group and a quarter fewer barriers than
+// 3; T = 15 keeps 3, its 60-row period with 4 measured slower)
 template <int T>
-__host__ __device__ constexpr int s6_ch() { return 3; }
+__host__ __device__ constexpr int s6_ch() { return T == 15 ? 3 : 4; }
+__host__ __device__ constexpr int s6_gcd(int a, int b) { return b == 0 ? a : s6_gcd(b, a % b); }
 template <int T>
-__host__ __device__ constexpr int s6_period() { return T % 3 == 0 ? T : 3 * T; }
+__host__ __device__ constexpr int s6_period() { return T / s6_gcd(T, s6_ch<T>()) * s6_ch<T>(); }
 
 template <int T>
 static void score6_layout(Score6Geom& g) {
