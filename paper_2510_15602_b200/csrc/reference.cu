@@ -29,6 +29,8 @@ constexpr int REF_NW = 5;  // 4 packed count words + 1 "below chunk" word
 struct RefGeom {
     int h, w, t, r, wp, stride, ny, nx, S, G;
     int stage;  // 1: the plane's bins are staged in shared memory first
+    int compact;  // 1 (stride >= t): only the sample windows' columns are counted,
+                  // wp = nx * t of them, column q = padded (q / t) * stride + q % t
 };
 
 template <int LANE>
@@ -112,7 +114,8 @@ k_reference(const BT* __restrict__ bins, const float* __restrict__ lo,
             const int gn = min(g.G, g.ny - j0);
             // ---- vertical: packed column counts of each sample row's window
             for (int xp = tid; xp < g.wp; xp += REF_THREADS) {
-                const int xx = pad_plane_index(xp - g.r, g.w, pad, edge);
+                const int xpad = g.compact ? (xp / g.t) * g.stride + xp % g.t : xp;
+                const int xx = pad_plane_index(xpad - g.r, g.w, pad, edge);
                 uint32_t st[REF_NW];
 #pragma unroll
                 for (int k = 0; k < REF_NW; ++k) st[k] = j0 == 0 ? 0u : state[k * g.wp + xp];
@@ -180,7 +183,7 @@ k_reference(const BT* __restrict__ bins, const float* __restrict__ lo,
                 const int jx = task % g.nx;
                 const int row = task / g.nx;  // gi * NW + k
                 const uint32_t* rp = CC + (size_t)row * g.wp;
-                const int xs = jx * g.stride;  // padded window cols [xs, xs + t)
+                const int xs = jx * (g.compact ? g.t : g.stride);  // window cols [xs, xs + t)
                 WS[(size_t)row * g.nx + jx] = rp[xs + g.t - 1] - (xs > 0 ? rp[xs - 1] : 0u);
             }
             __syncthreads();
@@ -263,6 +266,8 @@ static int launch_reference_t(const BT* bins, const float* lo, const float* hi, 
     g.stride = sample_stride(h, w, budget);
     g.ny = (h + g.stride - 1) / g.stride;
     g.nx = (w + g.stride - 1) / g.stride;
+    g.compact = g.stride >= t ? 1 : 0;
+    if (g.compact) g.wp = g.nx * t;  // the sample windows' columns only
     g.S = g.ny * g.nx;
     const int t2 = t * t;
     if (t2 > 32767) return QFCA_ERR_UNSUPPORTED;
