@@ -173,6 +173,20 @@ int qfca_score_ex(const void* bins, int32_t bins_bytes, const float* lo, const f
                   int32_t n_bins, int32_t patch_size, int32_t pad, int32_t sample_budget,
                   int32_t groups, void* scratch, int64_t scratch_bytes, float* partial,
                   void* stream);
+/* qfca_score_ex over tiles of wide planes read in place (no gathered copy):
+ * "image" i of the launch is tile (i / ncs, i % ncs) of the channels x hbig x
+ * wbig bins planes -- rows rst[i / ncs] .., columns cst[i % ncs] .. (device
+ * int32 arrays; every column start and wbig a multiple of col_align bytes,
+ * 4 / 8 / 16), th x tw (tw = 128) each; lo / hi / ref_cum per (tile, channel)
+ * as qfca_score.  The 128-column kernel v6 only (status 3 otherwise: gather
+ * the tiles and call qfca_score_ex).  sharding.py:_strip_partial, the
+ * wide-plane route of detect (scoring.py:235-299 on 1024 x 1024 planes). */
+int qfca_score_tiles(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
+                     const int32_t* ref_cum, int32_t channels, int32_t hbig, int32_t wbig,
+                     const int32_t* rst, int32_t nr, const int32_t* cst, int32_t ncs,
+                     int32_t col_align, int32_t th, int32_t tw, int32_t n_bins,
+                     int32_t patch_size, int32_t pad, int32_t sample_budget, int32_t groups,
+                     void* scratch, int64_t scratch_bytes, float* partial, void* stream);
 int64_t qfca_score_scratch_bytes(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size,
                                  int32_t channels, int64_t images, int32_t groups_hint,
                                  int32_t pad, int32_t sample_budget, int32_t with_reference);

@@ -59,6 +59,8 @@ _SIGNATURES = {
                     _P, _P], _I32),
     "qfca_score_ex": ([_P, _I32, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                        _I32, _P, _I64, _P, _P], _I32),
+    "qfca_score_tiles": ([_P, _I32, _P, _P, _P, _I32, _I32, _I32, _P, _I32, _P, _I32, _I32,
+                          _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P], _I32),
     "qfca_score_scratch_bytes": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32],
                                  _I64),
     "qfca_score_groups_ex": ([_I32, _I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32, _I32],

@@ -91,6 +91,9 @@ int launch_reference_weights(const float*, const void*, int, const float*, const
 int64_t score6_scratch_bytes(int);
 int launch_score6(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
                   int, int, int, int, int, int, void*, int64_t, float*, cudaStream_t);
+int launch_score6_src(const void*, int, const float*, const float*, const int32_t*, int64_t, int,
+                      int, int, int, int, int, int, int, void*, int64_t, float*, cudaStream_t,
+                      const int*, const int*, int, int, int, int);
 int score7_query(int, int, int, int, int, int64_t, int, int, int, int, int*);
 int64_t score7_scratch_bytes(int);
 int launch_score7(const void*, int, const float*, const float*, const int32_t*, int64_t, int, int,
@@ -377,6 +380,31 @@ int qfca_score_ex(const void* bins, int32_t bins_bytes, const float* lo, const f
     return counted(launch_score_any(ch, bins, bins_bytes, lo, hi, ref_cum, images, channels, h,
                                     w, n_bins, patch_size, pad, sample_budget, partial, S(stream),
                                     scratch, scratch_bytes),
+                   1);
+}
+
+int qfca_score_tiles(const void* bins, int32_t bins_bytes, const float* lo, const float* hi,
+                     const int32_t* ref_cum, int32_t channels, int32_t hbig, int32_t wbig,
+                     const int32_t* rst, int32_t nr, const int32_t* cst, int32_t ncs,
+                     int32_t col_align, int32_t th, int32_t tw, int32_t n_bins,
+                     int32_t patch_size, int32_t pad, int32_t sample_budget, int32_t groups,
+                     void* scratch, int64_t scratch_bytes, float* partial, void* stream) {
+    if (!bins || !ref_cum || !rst || !cst || nr < 1 || ncs < 1 || th < 1 || th > hbig ||
+        tw > wbig)
+        return QFCA_ERR_ARG;
+    const int64_t images = (int64_t)nr * ncs;
+    const ScoreChoice ch = score_choose(th, tw, n_bins, patch_size, channels, images, groups,
+                                        bins_bytes, pad, sample_budget, 0,
+                                        scratch != nullptr && scratch_bytes > 0);
+    if (ch.ver != 6 || ch.fref) return QFCA_ERR_UNSUPPORTED;  // the in-place read is v6's
+    if (groups > 0 && ch.groups != groups) return QFCA_ERR_ARG;
+    if (scratch_bytes < choice_scratch_bytes(ch, th)) return QFCA_ERR_ARG;
+    const int csz = col_align % 16 == 0 ? 16 : (col_align % 8 == 0 ? 8 : 4);
+    if (col_align % 4) return QFCA_ERR_UNSUPPORTED;
+    return counted(launch_score6_src(bins, bins_bytes, lo, hi, ref_cum, images, channels, th, tw,
+                                     n_bins, patch_size, pad, sample_budget, ch.groups, scratch,
+                                     scratch_bytes, partial, S(stream), rst, cst, ncs, hbig,
+                                     wbig, csz),
                    1);
 }
 

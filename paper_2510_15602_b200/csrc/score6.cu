@@ -61,7 +61,23 @@ struct Score6Geom {
     int passes;  // bin passes (16 lanes each, 15 new bins after the first)
     uint32_t moff;
     int o_sb, o_sa, o_stg, o_gt, o_th, o_xmap, o_rmap, o_stab, o_pj, o_misc, total;
+    // tile source (wide planes, sharding.py strips): "image" i of the launch is
+    // tile (i / ncs, i % ncs) of the C big planes (hbig x wbig) -- rows rst[.],
+    // columns cst[.] -- read in place (no gathered copy); csz = copy bytes
+    const int* rst;
+    const int* cst;
+    int tsrc, ncs, hbig, wbig, csz;
 };
+
+__device__ __forceinline__ void cp_async_n(void* smem, const void* gmem, int n) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    if (n == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+    else if (n == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
 
 __device__ __forceinline__ float rcp_approx6(float x) {
     float y;
@@ -191,13 +207,23 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
         }
     for (int i = tid; i < 4 * W; i += S6_THREADS) scr[(size_t)h * 4 * W + i] = 0u;
-    // bins of the first channel
-    {
-        const int64_t plane = (int64_t)img * g.C + c_begin;
-        if (c_begin < c_end)
-            for (int i = tid; i < hw / 16; i += S6_THREADS)
-                cp_async16(sbase + 16 * i, bins + plane * hw + 16 * i);
-    }
+    // the bins of channel c of this image / tile -> dst (asynchronous)
+    auto load_bins = [&](uint8_t* dst, int c) {
+        if (!g.tsrc) {
+            const uint8_t* const src = bins + ((int64_t)img * g.C + c) * hw;
+            for (int i = tid; i < hw / 16; i += S6_THREADS) cp_async16(dst + 16 * i, src + 16 * i);
+        } else {
+            const int r = img / g.ncs, s_ = img - r * g.ncs;
+            const uint8_t* const src =
+                bins + ((int64_t)c * g.hbig + g.rst[r]) * g.wbig + g.cst[s_];
+            const int per_row = W / g.csz;
+            for (int i = tid; i < h * per_row; i += S6_THREADS) {
+                const int y = i / per_row, k = i - y * per_row;
+                cp_async_n(dst + y * W + k * g.csz, src + (int64_t)y * g.wbig + k * g.csz, g.csz);
+            }
+        }
+    };
+    if (c_begin < c_end) load_bins(sbase, c_begin);  // bins of the first channel
 
     __syncthreads();  // xmap (read below by every thread) complete
     // phase-1 roles: H1 thread (column col, quarter q); H2 task (slot, segment)
@@ -252,21 +278,15 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         if (scale == 0.f) {  // degenerate channel: skipped (scoring.py:265-266)
             __syncthreads();  // every thread has read sscale before tid 0 rewrites it
             if (!g.dbsb) {
-                if (c + 1 < c_end)
-                    for (int i = tid; i < hw / 16; i += S6_THREADS)
-                        cp_async16(sbase + 16 * i, bins + (plane + 1) * hw + 16 * i);
+                if (c + 1 < c_end) load_bins(sbase, c + 1);
             } else {
                 buf ^= 1;
-                if (c + 1 < c_end)
-                    for (int i = tid; i < hw / 16; i += S6_THREADS)
-                        cp_async16(sbase + buf * hw + 16 * i, bins + (plane + 1) * hw + 16 * i);
+                if (c + 1 < c_end) load_bins(sbase + buf * hw, c + 1);
             }
             continue;
         }
         // prefetch the next channel's bins into the other buffer
-        if (g.dbsb && c + 1 < c_end)
-            for (int i = tid; i < hw / 16; i += S6_THREADS)
-                cp_async16(sbase + (buf ^ 1) * hw + 16 * i, bins + (plane + 1) * hw + 16 * i);
+        if (g.dbsb && c + 1 < c_end) load_bins(sbase + (buf ^ 1) * hw, c + 1);
 
         // ======== phase 1: window counts -> scratch (word-major rows) + SA4 samples
         auto phase1 = [&](bool samples) {
@@ -674,8 +694,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         if (g.dbsb) {
             buf ^= 1;
         } else if (c + 1 < c_end) {
-            for (int i = tid; i < hw / 16; i += S6_THREADS)
-                cp_async16(sbase + 16 * i, bins + (plane + 1) * hw + 16 * i);
+            load_bins(sbase, c + 1);
         }
     }
     cp_async_wait_all();
@@ -778,10 +797,26 @@ int64_t score6_scratch_bytes(int h) {
     return (int64_t)nsmid_cached() * (h + 1) * 4 * S6_W * 4;
 }
 
+int launch_score6_src(const void* bins, int bins_bytes, const float* lo, const float* hi,
+                      const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
+                      int pad, int budget, int groups, void* scratch, int64_t scratch_bytes,
+                      float* partial, cudaStream_t st, const int* rst, const int* cst, int ncs,
+                      int hbig, int wbig, int csz);
+
 int launch_score6(const void* bins, int bins_bytes, const float* lo, const float* hi,
                   const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
                   int pad, int budget, int groups, void* scratch, int64_t scratch_bytes,
                   float* partial, cudaStream_t st) {
+    return launch_score6_src(bins, bins_bytes, lo, hi, V, images, C, h, w, n_bins, t, pad, budget,
+                             groups, scratch, scratch_bytes, partial, st, nullptr, nullptr, 0, 0,
+                             0, 0);
+}
+
+int launch_score6_src(const void* bins, int bins_bytes, const float* lo, const float* hi,
+                      const int32_t* V, int64_t images, int C, int h, int w, int n_bins, int t,
+                      int pad, int budget, int groups, void* scratch, int64_t scratch_bytes,
+                      float* partial, cudaStream_t st, const int* rst, const int* cst, int ncs,
+                      int hbig, int wbig, int csz) {
     if (bins_bytes != 1) return QFCA_ERR_UNSUPPORTED;
     if (!scratch || scratch_bytes < score6_scratch_bytes(h)) return QFCA_ERR_ARG;
     Score6Geom g;
@@ -789,6 +824,16 @@ int launch_score6(const void* bins, int bins_bytes, const float* lo, const float
     int rc = score6_plan(h, w, n_bins, t, C, images, groups, pad, budget, V != nullptr, &g, &smem);
     if (rc != QFCA_OK) return rc;
     if (groups > 0 && g.groups != groups) return QFCA_ERR_ARG;
+    g.rst = rst;
+    g.cst = cst;
+    g.tsrc = rst != nullptr;
+    g.ncs = ncs;
+    g.hbig = hbig;
+    g.wbig = wbig;
+    g.csz = csz;
+    if (g.tsrc && (ncs < 1 || (csz != 4 && csz != 8 && csz != 16) || wbig % csz ||
+                   (reinterpret_cast<uintptr_t>(bins) % csz)))
+        return QFCA_ERR_ARG;
     void (*kern)(const uint8_t*, const float*, const float*, const int32_t*, const Score6Geom,
                  uint32_t*, float*) = nullptr;
     const bool mp = g.passes > 1;

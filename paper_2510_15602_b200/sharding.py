@@ -165,22 +165,32 @@ def _channel_partial(values: torch.Tensor, cfg):
 
 
 _SCRATCH: dict = {}
+TILES_IN_PLACE = True  # v6 reads the tiles of wide planes in place (False: gather first)
+
+
+def _scratch(bins, h, w, cfg, c, images, groups, with_ref):
+    """The cached per-stream scratch of the 128-column kernels (None: the chosen
+    kernel needs none)."""
+    L = N.lib()
+    pad = N.PAD_CODES[cfg.pad]
+    nbytes = L.qfca_score_scratch_bytes(h, w, cfg.n_bins, cfg.patch_size, c, images, groups, pad,
+                                        cfg.sample_budget, 1 if with_ref else 0)
+    if nbytes <= 0:
+        return None
+    key = (bins.device.index, torch.cuda.current_stream(bins.device).cuda_stream)
+    scr = _SCRATCH.get(key)
+    if scr is None or scr.numel() < nbytes:
+        scr = torch.empty((nbytes,), dtype=torch.uint8, device=bins.device)
+        _SCRATCH[key] = scr
+    return scr
 
 
 def score_call(bins, lo, hi, ref, images, c, h, w, cfg, groups, partial):
     """qfca_score_ex with a cached per-stream scratch (the 128-column kernel
     keeps each plane's window counts in it)."""
-    L = N.lib()
     pad = N.PAD_CODES[cfg.pad]
-    nbytes = L.qfca_score_scratch_bytes(h, w, cfg.n_bins, cfg.patch_size, c, images, groups, pad,
-                                        cfg.sample_budget, 0 if ref is None else 1)
-    scr = None
-    if nbytes > 0:
-        key = (bins.device.index, torch.cuda.current_stream(bins.device).cuda_stream)
-        scr = _SCRATCH.get(key)
-        if scr is None or scr.numel() < nbytes:
-            scr = torch.empty((nbytes,), dtype=torch.uint8, device=bins.device)
-            _SCRATCH[key] = scr
+    scr = _scratch(bins, h, w, cfg, c, images, groups, ref is not None)
+    nbytes = 0 if scr is None else scr.numel()
     N.call("qfca_score_ex", bins.data_ptr(), bins.element_size(), lo.data_ptr(), hi.data_ptr(),
            None if ref is None else ref.data_ptr(), images, c, h, w, cfg.n_bins, cfg.patch_size,
            pad, cfg.sample_budget, groups, None if scr is None else scr.data_ptr(),
@@ -210,13 +220,6 @@ def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
            ref.data_ptr(), s)
     ro, rl, co, cl, rst_d, cst_d = _tile_index(h, w, cfg.patch_size, bins.device, rst, rown,
                                                rloc, cst, cown, cloc)
-    sb = empty((nt, c, th, STRIP_W), torch.uint8)
-    if w % 4 == 0:
-        N.call("qfca_gather_tiles", bins.data_ptr(), c, h, w, rst_d.data_ptr(), len(rst),
-               cst_d.data_ptr(), len(cst), th, STRIP_W, sb.data_ptr(), s)
-    else:
-        b3 = bins.view(c, h, w)
-        sb.copy_(torch.stack([b3[:, r:r + th, a:a + STRIP_W] for r in rst for a in cst]))
     lo_r = lo.repeat(nt).contiguous()
     hi_r = hi.repeat(nt).contiguous()
     ref_r = ref.repeat(nt, 1).contiguous()
@@ -227,7 +230,29 @@ def _strip_partial(bins, lo, hi, cfg, c, h, w) -> torch.Tensor:
         raise NotImplementedError("no fused kernel for the tile shape")
     hw = th * STRIP_W
     partial = zeros((nt * groups, hw), torch.float32)
-    score_call(sb, lo_r, hi_r, ref_r, nt, c, th, STRIP_W, cfg, groups, partial)
+    # the 128-column kernel reads the tiles in place; else gather them first
+    align = next((a for a in (16, 8, 4) if w % a == 0 and all(x % a == 0 for x in cst)), 0)
+    st = N.QFCA_ERR_UNSUPPORTED
+    if TILES_IN_PLACE and align and bins.element_size() == 1:
+        scr = _scratch(bins, th, STRIP_W, cfg, c, nt, groups, True)
+        nbytes = 0 if scr is None else scr.numel()
+        st = L.qfca_score_tiles(bins.data_ptr(), 1, lo_r.data_ptr(), hi_r.data_ptr(),
+                                ref_r.data_ptr(), c, h, w, rst_d.data_ptr(), len(rst),
+                                cst_d.data_ptr(), len(cst), align, th, STRIP_W, cfg.n_bins,
+                                cfg.patch_size, pad, cfg.sample_budget, groups,
+                                None if scr is None else scr.data_ptr(), nbytes,
+                                partial.data_ptr(), s)
+    if st == N.QFCA_ERR_UNSUPPORTED:
+        sb = empty((nt, c, th, STRIP_W), torch.uint8)
+        if w % 4 == 0:
+            N.call("qfca_gather_tiles", bins.data_ptr(), c, h, w, rst_d.data_ptr(), len(rst),
+                   cst_d.data_ptr(), len(cst), th, STRIP_W, sb.data_ptr(), s)
+        else:
+            b3 = bins.view(c, h, w)
+            sb.copy_(torch.stack([b3[:, r:r + th, a:a + STRIP_W] for r in rst for a in cst]))
+        score_call(sb, lo_r, hi_r, ref_r, nt, c, th, STRIP_W, cfg, groups, partial)
+    else:
+        N.check(st, "qfca_score_tiles")
     ones = torch.ones((nt,), dtype=torch.int32, device=bins.device)
     acc = empty((nt, hw), torch.float64)
     N.call("qfca_reduce_partials", partial.data_ptr(), nt, groups, hw, ones.data_ptr(),

@@ -450,6 +450,24 @@ def test_wide_plane_strips_match_whole_plane(Q, c, h, w, t):
     assert rel_err(got, ref_map) <= TOL
 
 
+@pytest.mark.parametrize("c,h,w,t", [(4, 64, 1024, 9), (3, 200, 300, 5), (2, 130, 520, 3)])
+def test_wide_plane_tiles_in_place_equal_gathered(Q, c, h, w, t):
+    """qfca_score_tiles (v6 reading the tiles of the wide planes in place, 16 /
+    8 / 4-byte copies by the column alignment) gives the partial maps of the
+    gathered-tile route bit for bit."""
+    from paper_2510_15602_b200 import sharding
+    rng = np.random.default_rng(c * w + t + 1)
+    xt = torch.from_numpy(np.maximum(rng.standard_normal((c, h, w)), 0).astype(np.float32)).cuda()
+    cfg = Q.PipelineConfig(patch_size=t)
+    a, _ = sharding.channel_partial(xt, cfg)
+    sharding.TILES_IN_PLACE = False
+    try:
+        b, _ = sharding.channel_partial(xt, cfg)
+    finally:
+        sharding.TILES_IN_PLACE = True
+    assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("planes,h,w,n", [(37, 64, 64, 16), (5, 128, 128, 16), (9, 32, 32, 2),
                                           (4, 20, 24, 65), (3, 128, 128, 64), (2, 300, 300, 16),
                                           (6, 7, 9, 16)])
