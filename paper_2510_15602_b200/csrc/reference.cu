@@ -287,6 +287,10 @@ static int launch_reference_t(const BT* bins, const float* lo, const float* hi, 
         while (g.G > 2 && ref_smem_bytes(g, st_bytes, nbc, bt) > 110 * 1024) g.G >>= 1;
         if (ref_smem_bytes(g, st_bytes, nbc, bt) > 110 * 1024) { g.stage = 0; g.G = 8; }
     }
+    // unstaged planes read their rows from global memory: prefer two CTAs per SM
+    // (more loads in flight) over more sample rows per pass
+    if (!g.stage)
+        while (g.G > 1 && ref_smem_bytes(g, st_bytes, nbc, bt) > 110 * 1024) g.G >>= 1;
     while (g.G > 1 && ref_smem_bytes(g, st_bytes, nbc, bt) > limit) g.G >>= 1;
     const size_t smem = ref_smem_bytes(g, st_bytes, nbc, bt);
     if (smem > limit) return QFCA_ERR_UNSUPPORTED;
