@@ -60,7 +60,7 @@ struct Score6Geom {
     int dbsb;   // bins double-buffered (next channel prefetched)
     int passes;  // bin passes (16 lanes each, 15 new bins after the first)
     uint32_t moff;
-    int o_sb, o_sa, o_stg, o_gt, o_th, o_xmap, o_rmap, o_stab, o_pj, o_misc, total;
+    int o_sb, o_sa, o_stg, o_gt, o_xmap, o_rmap, o_stab, o_pj, o_misc, total;
     // tile source (wide planes, sharding.py strips): "image" i of the launch is
     // tile (i / ncs, i % ncs) of the C big planes (hbig x wbig) -- rows rst[.],
     // columns cst[.] -- read in place (no gathered copy); csz = copy bytes
@@ -89,6 +89,17 @@ __device__ __forceinline__ float lds6_f32(uint32_t addr) {
     float v;
     asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
     return v;
+}
+// thermometer words of bin b for a pass whose lanes count bins <= tb .. tb + 15
+// (lane j of word q = [b <= tb + 4q + j]) by ALU: 0x01010101 shifted left by
+// 8 (b - tb - 4q) bytes, clamped (shf.l.clamp gives 0 past 32 bits) -- no
+// shared-memory table lookup on the phase-1 critical path
+__device__ __forceinline__ uint4 thermo6(int b, int tb) {
+    const int s = 8 * (b - tb);
+    return make_uint4(__funnelshift_lc(0u, 0x01010101u, max(s, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 32, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 64, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 96, 0)));
 }
 __device__ __forceinline__ uint32_t smid6() {
     uint32_t r;
@@ -137,7 +148,6 @@ static void score6_layout(Score6Geom& g) {
     g.o_stg = take((long long)S6_SLOTS * wpp * 16);
     g.o_gt = take(16LL * GP * 4);  // the current pass's 16 bins
     g.o_pj = take((long long)GP * 4);
-    g.o_th = take(256 * 16);
     g.o_xmap = take((long long)(S6_W + 2 * R) * 4);
     constexpr int P = s6_period<T>();
     const int n_chunks = (g.S + P - 1) / P;
@@ -168,7 +178,6 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     uint4* const STG = reinterpret_cast<uint4*>(sm + g.o_stg);
     float* const GT = reinterpret_cast<float*>(sm + g.o_gt);
     float* const sPJ = reinterpret_cast<float*>(sm + g.o_pj);
-    uint4* const TH = reinterpret_cast<uint4*>(sm + g.o_th);
     int* const xmap = reinterpret_cast<int*>(sm + g.o_xmap);
     int* const rmap = reinterpret_cast<int*>(sm + g.o_rmap);
     int2* const stab = reinterpret_cast<int2*>(sm + g.o_stab);
@@ -196,16 +205,6 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         rmap[s] = s < g.S ? map_coord(s - R, h, g.pad) : h;
     for (int e = tid; e < h; e += S6_THREADS)
         stab[e] = make_int2(map_coord(e + R, h, g.pad) * W, map_coord(e - 1 - R, h, g.pad) * W);
-    if (!MP)
-        for (int b = tid; b < 256; b += S6_THREADS) {
-            uint32_t v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
-                const int d = b - 4 * q;
-                v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
-            }
-            TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
-        }
     for (int i = tid; i < 4 * W; i += S6_THREADS) scr[(size_t)h * 4 * W + i] = 0u;
     // the bins of channel c of this image / tile -> dst (asynchronous)
     auto load_bins = [&](uint8_t* dst, int c) {
@@ -241,21 +240,11 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     const int t_q = t_slot >> 3, t_k = t_slot & 7;
     // phase-4 roles: thread (column x, bin group grp)
     const int x = tid & (W - 1), grp = tid >> 7;
-    // thermometer words of a pass whose 16 lanes count bins <= tb .. tb + 15:
-    // lane j of word q = [b <= tb + 4q + j]
+    // a pass's 16 thermometer lanes count bins <= tb .. tb + 15 (thermo6)
+    int thb = 0;
     auto build_th = [&](int tb) {
-        if (!MP) return;  // built once below
-        __syncthreads();  // the previous pass's readers are done
-        for (int b = tid; b < 256; b += S6_THREADS) {
-            uint32_t v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int d = b - tb - 4 * q;
-                v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
-            }
-            TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
-        }
-        __syncthreads();
+        thb = tb;
+        if (MP) __syncthreads();  // the previous pass's readers of the scratch are done
     };
 
     int buf = 0;
@@ -295,7 +284,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             if (hy0 < hy1) {  // window sum of row hy0 - 1: the slide starts there
 #pragma unroll
                 for (int dy = -R; dy <= R; ++dy) {
-                    const uint4 a = TH[pb[map_coord(hy0 - 1 + dy, h, g.pad) * W]];
+                    const uint4 a = thermo6(pb[map_coord(hy0 - 1 + dy, h, g.pad) * W], thb);
                     cst.x += a.x;
                     cst.y += a.y;
                     cst.z += a.z;
@@ -310,7 +299,7 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     const int y = hy0 + kb + kk;
                     if (y < hy1) {
                         const int2 st = stab[y];
-                        const uint4 a = TH[pb[st.x]], r = TH[pb[st.y]];
+                        const uint4 a = thermo6(pb[st.x], thb), r = thermo6(pb[st.y], thb);
                         cst.x += a.x - r.x;
                         cst.y += a.y - r.y;
                         cst.z += a.z - r.z;
