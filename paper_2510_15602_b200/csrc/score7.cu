@@ -60,6 +60,15 @@ __device__ __forceinline__ float rcp_approx7(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// thermometer words of bin b (lane j of word q = [b <= 4q + j]) by ALU: see
+// score6.cu's thermo6
+__device__ __forceinline__ uint4 thermo7(int b) {
+    const int s = 8 * b;
+    return make_uint4(__funnelshift_lc(0u, 0x01010101u, s),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 32, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 64, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 96, 0)));
+}
 __device__ __forceinline__ uint32_t smid7() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -131,7 +140,6 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);       // [16]
     float* const svm = reinterpret_cast<float*>(sm + g.o_misc + 80);  // [16]
     float* const sd = reinterpret_cast<float*>(sm + g.o_misc + 144);  // [16]
-    __shared__ uint4 TH[256];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int h = g.h;
@@ -156,15 +164,6 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             else { add = map_coord(c + R, h, g.pad); rem = map_coord(cp - R, h, g.pad); }
         }
         stab[s] = make_int4(c, 1, add * 4 * W, rem * 4 * W);
-    }
-    for (int b = tid; b < 256; b += S7_THREADS) {
-        uint32_t v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
-            const int d = b - 4 * q;
-            v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
-        }
-        TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
     }
     __syncthreads();
 
@@ -208,7 +207,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
                 const int p = lane * CPL + k;
-                const uint4 v = p < WP ? TH[brow[scol[k]]] : make_uint4(0, 0, 0, 0);
+                const uint4 v = p < WP ? thermo7(brow[scol[k]]) : make_uint4(0, 0, 0, 0);
                 run.x += v.x; run.y += v.y; run.z += v.z; run.w += v.w;
                 pre[k] = run;
             }
@@ -563,9 +562,9 @@ static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
 #undef S7C
             default: return QFCA_ERR_UNSUPPORTED;
         }
-        if (bytes <= (size_t)S7_SMEM_MAX - 4096) break;  // + static TH
+        if (bytes <= (size_t)S7_SMEM_MAX) break;
     }
-    if (bytes > (size_t)S7_SMEM_MAX - 4096) return QFCA_ERR_UNSUPPORTED;
+    if (bytes > (size_t)S7_SMEM_MAX) return QFCA_ERR_UNSUPPORTED;
     int groups = groups_hint;
     if (groups <= 0) groups = balanced_groups(images, C, 1, 1);
     groups = groups < 1 ? 1 : (groups > C ? C : groups);
