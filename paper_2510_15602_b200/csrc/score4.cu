@@ -55,7 +55,7 @@ struct Score4Geom {
     uint32_t moff;  // -4 * 0x4B000000 (mod 2^32): magic-float -> G-table byte offset
     int o_sb, o_sa, o_gt, o_xmap, o_rmap, o_stab, o_scale, o_sv, o_alias, total;
     // inside the alias region (offsets from o_alias)
-    int a_chp, a_th, a_cnt, a_qm, a_lo, a_hi, a_pj;
+    int a_chp, a_cnt, a_qm, a_lo, a_hi, a_pj;
 };
 
 __device__ __forceinline__ float rcp_approx4(float x) {
@@ -84,6 +84,16 @@ __host__ __device__ constexpr int s4_rounds(int t2) {
     return r;
 }
 
+// thermometer words of bin b (lane j of word q = [b <= 4q + j]) by ALU: see
+// score6.cu's thermo6
+__device__ __forceinline__ uint4 thermo4(int b) {
+    const int s = 8 * b;
+    return make_uint4(__funnelshift_lc(0u, 0x01010101u, s),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 32, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 64, 0)),
+                      __funnelshift_lc(0u, 0x01010101u, max(s - 96, 0)));
+}
+
 template <int T, int W, int NCOL>
 static void score4_layout(Score4Geom& g) {
     constexpr int CPB = NCOL / W;
@@ -110,7 +120,7 @@ static void score4_layout(Score4Geom& g) {
     g.o_stab = take((long long)g.h * 8);
     g.o_scale = take((long long)CPB * 4);
     g.o_sv = take((long long)CPB * 16 * 4);
-    // alias region: pass 0 (CHp, TH) | search (cnt, qm, lo, hi) + PJ | pass 1 (Vb)
+    // alias region: pass 0 (CHp) | search (cnt, qm, lo, hi) + PJ | pass 1 (Vb)
     int a = 0;
     auto atake = [&](long long bytes) {
         const int o = a;
@@ -118,7 +128,6 @@ static void score4_layout(Score4Geom& g) {
         return o;
     };
     g.a_chp = atake((long long)2 * T * CPB * g.WPP * 16);  // pass-0 H2 staging: 2T padded rows
-    g.a_th = atake(256 * 16);
     const int pass0 = a;
     a = 0;
     g.a_cnt = atake((long long)(4 * NCOL / 32) * 8 * 4);  // per-warp search counts
@@ -161,7 +170,6 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     int* const sV = reinterpret_cast<int*>(sm + g.o_sv);
     uint8_t* const al = sm + g.o_alias;
     uint4* const CHp = reinterpret_cast<uint4*>(al + g.a_chp);
-    uint4* const TH = reinterpret_cast<uint4*>(al + g.a_th);
     uint32_t* const cnt = reinterpret_cast<uint32_t*>(al + g.a_cnt);
     uint8_t* const qm8 = al + g.a_qm;
     const uint32_t* const qm = reinterpret_cast<const uint32_t*>(al + g.a_qm);
@@ -221,15 +229,6 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 for (int i = tid; i < 16; i += S4_THREADS) sV[k * 16 + i] = T2;
             }
         }
-        for (int b = tid; b < 256; b += S4_THREADS) {
-            uint32_t v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // lane j of word q = [b <= 4q + j]
-                const int d = b - 4 * q;
-                v[q] = d <= 0 ? 0x01010101u : (d < 4 ? (0x01010101u << (8 * d)) : 0u);
-            }
-            TH[b] = make_uint4(v[0], v[1], v[2], v[3]);
-        }
         __syncthreads();
 
         // ---- pass 0: window counts of every pixel -> SA4, all warps.
@@ -245,7 +244,7 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 uint4 cst = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
                 for (int dy = -R; dy <= R; ++dy) {
-                    const uint4 a = TH[pb[map_coord(y0 + dy, h, g.pad) * W]];
+                    const uint4 a = thermo4(pb[map_coord(y0 + dy, h, g.pad) * W]);
                     cst.x += a.x;
                     cst.y += a.y;
                     cst.z += a.z;
@@ -254,7 +253,7 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 dst[y0 * W] = cst;
                 for (int y = y0 + 1; y < y1; ++y) {
                     const int2 st = stab[y];
-                    const uint4 a = TH[pb[st.x]], r = TH[pb[st.y]];
+                    const uint4 a = thermo4(pb[st.x]), r = thermo4(pb[st.y]);
                     cst.x += a.x - r.x;
                     cst.y += a.y - r.y;
                     cst.z += a.z - r.z;
