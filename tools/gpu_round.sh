@@ -9,7 +9,7 @@ timeout 1500 python -m pytest tests -m gpu -q > $O/${T}_pytest_gpu.log 2>&1; tai
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/${T}_smoke.log 2>&1; tail -1 $O/${T}_smoke.log
 timeout 1200 python bench.py > $O/${T}_bench_1024.json 2> $O/${T}_bench_1024.err; tail -c 300 $O/${T}_bench_1024.json
 timeout 900 python bench.py --workload qfca_plus512 > $O/${T}_bench_plus512.json 2> $O/${T}_bench_plus512.err; tail -c 300 $O/${T}_bench_plus512.json
-timeout 900 python bench.py --workload qfca8192 --steps 5 > $O/${T}_bench_8192.json 2> $O/${T}_bench_8192.err; tail -c 300 $O/${T}_bench_8192.json
+timeout 900 python bench.py --workload qfca8192 --steps 20 > $O/${T}_bench_8192.json 2> $O/${T}_bench_8192.err; tail -c 300 $O/${T}_bench_8192.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/${T}_bench_ref.json 2> $O/${T}_bench_ref.err; tail -c 300 $O/${T}_bench_ref.json
 timeout 600 python tools/sweep.py --batch 8 > $O/${T}_sweep_1024.json 2> $O/${T}_sweep.err
 for W in qfca1024 qfca_plus512; do
