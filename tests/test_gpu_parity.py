@@ -425,7 +425,8 @@ def test_topk_eigh_lanczos_vs_eigh(Q):
 
 
 @pytest.mark.parametrize("c,h,w,t", [(6, 96, 300, 9), (4, 64, 1024, 9), (5, 130, 257, 3),
-                                     (3, 40, 420, 15), (3, 600, 200, 9), (2, 257, 129, 5)])
+                                     (3, 40, 420, 15), (3, 600, 200, 9), (2, 257, 129, 5),
+                                     (2, 100, 300, 33), (2, 140, 260, 17)])
 def test_wide_plane_strips_match_whole_plane(Q, c, h, w, t):
     """sharding.channel_partial on planes wider than 128 columns (configs[4]:
     1024^2 feature planes) runs the fused kernel on 128-column strips; it must
