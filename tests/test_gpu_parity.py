@@ -451,11 +451,12 @@ def test_wide_plane_strips_match_whole_plane(Q, c, h, w, t):
     assert rel_err(got, ref_map) <= TOL
 
 
-@pytest.mark.parametrize("c,h,w,t", [(4, 64, 1024, 9), (3, 200, 300, 5), (2, 130, 520, 3)])
+@pytest.mark.parametrize("c,h,w,t", [(4, 64, 1024, 9), (3, 200, 300, 5), (2, 130, 520, 3),
+                                     (2, 64, 248, 5)])
 def test_wide_plane_tiles_in_place_equal_gathered(Q, c, h, w, t):
     """qfca_score_tiles (v6 reading the tiles of the wide planes in place, 16 /
-    8 / 4-byte copies by the column alignment) gives the partial maps of the
-    gathered-tile route bit for bit."""
+    8 / 4-byte copies by the column alignment: 1024 -> 16, 248 -> 8, 300 /
+    520 -> 4) gives the partial maps of the gathered-tile route bit for bit."""
     from paper_2510_15602_b200 import sharding
     rng = np.random.default_rng(c * w + t + 1)
     xt = torch.from_numpy(np.maximum(rng.standard_normal((c, h, w)), 0).astype(np.float32)).cuda()
