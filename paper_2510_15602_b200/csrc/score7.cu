@@ -254,6 +254,42 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 uint16_t* const sa = SA + (size_t)(4 * gq) * g.srow;
                 const int j0 = sub * per, j1 = min(nsy, j0 + per);
                 uint32_t l16 = 0, h16 = 0;
+                auto store = [&](int j) {
+                    const int si = j * nsx + jx;
+                    sa[si] = (uint16_t)(l16 & 0xFFFFu);
+                    sa[g.srow + si] = (uint16_t)(h16 & 0xFFFFu);
+                    sa[2 * g.srow + si] = (uint16_t)(l16 >> 16);
+                    sa[3 * g.srow + si] = (uint16_t)(h16 >> 16);
+                };
+                if (sd_ == 2 && j0 < j1) {
+                    // stride 2 (the 128^2 planes): a recount at the segment start,
+                    // then two slides per sample row with the next row's four row
+                    // windows loaded one sample row ahead
+                    const int cy0 = j0 * 2;
+                    for (int dy = -R; dy <= R; ++dy) {
+                        const uint32_t w = col[(size_t)map_coord(cy0 + dy, h, g.pad) * 4 * W];
+                        l16 += w & 0x00FF00FFu;
+                        h16 += (w >> 8) & 0x00FF00FFu;
+                    }
+                    store(j0);
+                    uint32_t a1 = 0, r1 = 0, a2 = 0, r2 = 0;
+                    auto fetch = [&](int j) {  // centres 2j - 1, 2j: stream rows + R
+                        const int4 s1 = stab[2 * j - 1 + R], s2 = stab[2 * j + R];
+                        a1 = col[s1.z];
+                        r1 = col[s1.w];
+                        a2 = col[s2.z];
+                        r2 = col[s2.w];
+                    };
+                    if (j0 + 1 < j1) fetch(j0 + 1);
+                    for (int j = j0 + 1; j < j1; ++j) {
+                        l16 += (a1 & 0x00FF00FFu) - (r1 & 0x00FF00FFu) + (a2 & 0x00FF00FFu) -
+                               (r2 & 0x00FF00FFu);
+                        h16 += ((a1 >> 8) & 0x00FF00FFu) - ((r1 >> 8) & 0x00FF00FFu) +
+                               ((a2 >> 8) & 0x00FF00FFu) - ((r2 >> 8) & 0x00FF00FFu);
+                        if (j + 1 < j1) fetch(j + 1);
+                        store(j);
+                    }
+                } else
                 for (int j = j0; j < j1; ++j) {
                     const int cy = j * sd_;
                     if (j == j0 || sd_ >= T) {
@@ -271,11 +307,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             h16 += ((wa >> 8) & 0x00FF00FFu) - ((wr >> 8) & 0x00FF00FFu);
                         }
                     }
-                    const int si = j * nsx + jx;
-                    sa[si] = (uint16_t)(l16 & 0xFFFFu);
-                    sa[g.srow + si] = (uint16_t)(h16 & 0xFFFFu);
-                    sa[2 * g.srow + si] = (uint16_t)(l16 >> 16);
-                    sa[3 * g.srow + si] = (uint16_t)(h16 >> 16);
+                    store(j);
                 }
             }
             // pad the sample rows so packed compares see values > any query
