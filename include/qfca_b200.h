@@ -144,7 +144,7 @@ int qfca_score_groups(int32_t h, int32_t w, int32_t n_bins, int32_t patch_size, 
 
 /* select the fused scoring kernel: 0 = auto, the first that applies of
  * v6 score6.cu (128-wide planes / tiles, T <= 15, N <= 256; needs the
- * caller's scratch), v7 score7.cu (128-wide, T = 17..65, N <= 16; scratch),
+ * caller's scratch), v7 score7.cu (128-wide, T = 17..65, N <= 256; scratch),
  * v4 score4.cu (planes <= 64 wide), v3 score3.cu, v5 score5.cu (any odd T),
  * v2 score2.cu, v1 score.cu (any shape); 1..7 = force that version
  * (unsupported shapes then return status 3).  Process-global. */

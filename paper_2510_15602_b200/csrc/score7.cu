@@ -52,6 +52,7 @@ struct Score7Geom {
     int fref, stride, nsy, nsx, nsamp, srow;
     int o_sb, o_pj, o_gt, o_erow, o_qrow, o_qf, o_prow, o_snap, o_sa, o_xmap, o_stab, o_misc, total;
     int gt;         // 1: the G_i(v) table (T <= 43 and it fits), else G from PJ
+    int passes;     // bin passes: 16 lanes each, 15 new bins after the first (N <= 256)
     uint32_t moff;  // G-table address of the magic float 2^23 + v is base + 4 v
 };
 
@@ -62,9 +63,9 @@ __device__ __forceinline__ float rcp_approx7(float x) {
 }
 // thermometer words of bin b (lane j of word q = [b <= 4q + j]) by ALU: see
 // score6.cu's thermo6
-__device__ __forceinline__ uint4 thermo7(int b) {
-    const int s = 8 * b;
-    return make_uint4(__funnelshift_lc(0u, 0x01010101u, s),
+__device__ __forceinline__ uint4 thermo7(int b, int tb) {  // lanes: bins tb .. tb + 15
+    const int s = 8 * (b - tb);
+    return make_uint4(__funnelshift_lc(0u, 0x01010101u, max(s, 0)),
                       __funnelshift_lc(0u, 0x01010101u, max(s - 32, 0)),
                       __funnelshift_lc(0u, 0x01010101u, max(s - 64, 0)),
                       __funnelshift_lc(0u, 0x01010101u, max(s - 96, 0)));
@@ -108,7 +109,7 @@ static void score7_layout(Score7Geom& g) {
     g.o_erow = take(16LL * S7_EST * 4);
     g.o_xmap = take((long long)WP * 4);
     g.o_stab = take((long long)(g.S + 1) * 16);
-    g.o_misc = take(1024);
+    g.o_misc = take(2048);  // scale, V[256], (vm, d) of the pass's 16 bins
     g.total = off;
 }
 
@@ -137,9 +138,9 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
     int4* const stab = reinterpret_cast<int4*>(sm + g.o_stab);        // per stream row
     uint16_t* const SA = reinterpret_cast<uint16_t*>(sm + g.o_sa);     // [16][srow] (fref)
     float* const sscale = reinterpret_cast<float*>(sm + g.o_misc);    // [1]
-    int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);       // [16]
-    float* const svm = reinterpret_cast<float*>(sm + g.o_misc + 80);  // [16]
-    float* const sd = reinterpret_cast<float*>(sm + g.o_misc + 144);  // [16]
+    int* const sV = reinterpret_cast<int*>(sm + g.o_misc + 16);         // [256]
+    float* const svm = reinterpret_cast<float*>(sm + g.o_misc + 1040);  // [16] (pass)
+    float* const sd = reinterpret_cast<float*>(sm + g.o_misc + 1104);   // [16] (pass)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int h = g.h;
@@ -189,7 +190,8 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                              (double)T2);
             sscale[0] = sc;
         }
-        if (tid < 16) sV[tid] = (tid < g.n_bins && !g.fref) ? __ldg(Vref + plane * g.n_bins + tid) : T2;
+        for (int i = tid; i < 256; i += S7_THREADS)
+            sV[i] = (i < g.n_bins && !g.fref) ? __ldg(Vref + plane * g.n_bins + i) : T2;
         for (int i = tid; i < hw / 16; i += S7_THREADS)
             reinterpret_cast<uint4*>(sb)[i] = __ldg(reinterpret_cast<const uint4*>(bins + plane * hw) + i);
         __syncthreads();
@@ -199,7 +201,9 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             continue;
         }
 
-        // ======== phase RW: row windows of every plane row -> scratch, one warp per row
+        // ======== phase RW: row windows of every plane row -> scratch, one warp per
+        // row, thermometer lanes of the pass's bins tb .. tb + 15
+        auto rw_phase = [&](int tb) {
         for (int y = warp; y < h; y += S7_THREADS / 32) {
             const uint8_t* const brow = sb + y * W;
             uint4 pre[CPL];
@@ -207,7 +211,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
                 const int p = lane * CPL + k;
-                const uint4 v = p < WP ? thermo7(brow[scol[k]]) : make_uint4(0, 0, 0, 0);
+                const uint4 v = p < WP ? thermo7(brow[scol[k]], tb) : make_uint4(0, 0, 0, 0);
                 run.x += v.x; run.y += v.y; run.z += v.z; run.w += v.w;
                 pre[k] = run;
             }
@@ -240,10 +244,12 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             __syncwarp();
         }
         __syncthreads();  // scratch rows complete; the prefix rows' region is free
-        if (g.fref) {
-            // ======== the reference (median-quan) from this plane's own window
-            // counts: the cumulative counts A_i(s) at the stride-grid samples
-            // (reference.cu's statistic: V_i = the (S-1-m)-th smallest A_i(s))
+        };
+        // ======== the reference (median-quan) from this plane's own window counts:
+        // the cumulative counts A_i(s) at the stride-grid samples (reference.cu's
+        // statistic: V_i = the (S-1-m)-th smallest A_i(s)) of the pass's lanes
+        // klo .. 15 (lane 0 of a later pass is the previous pass's last bin)
+        auto fref_pass = [&](int tb, int klo) {
             const int nsx = g.nsx, nsy = g.nsy, sd_ = g.stride;
             const int cols = 4 * nsx;
             const int nsub = max(1, S7_THREADS / cols);
@@ -317,7 +323,8 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             __syncthreads();
             const int m = (g.nsamp - 1) / 2, c0 = g.nsamp - m;
             const int words = g.srow / 2;
-            for (int bi = warp; bi < g.n_bins; bi += S7_THREADS / 32) {
+            for (int bi = warp; bi < 16; bi += S7_THREADS / 32) {
+                if (bi < klo || tb + bi >= g.n_bins) continue;
                 const uint32_t* const row = reinterpret_cast<const uint32_t*>(SA + (size_t)bi * g.srow);
                 int a = 0, b = T2;
                 while (a < b) {  // smallest v with #{A <= v} >= c0
@@ -329,11 +336,13 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     cnt = __reduce_add_sync(FULL, cnt);
                     if (cnt >= c0) b = mid; else a = mid + 1;
                 }
-                if (lane == 0) sV[bi] = a;
+                if (lane == 0) sV[tb + bi] = a;
             }
             __syncthreads();  // sV ready; the sample store is free again
-        }
-        // ======== tables: PJ = prefix of J; (V_{i-1}, D_i) per bin
+        };
+        // ======== tables: PJ = prefix of J (all bins); (V_{i-1}, D_i) and G_i of
+        // the pass's bins tb .. tb + 15
+        auto pass_tables = [&](int tb) {
         for (int qq = tid; qq < T2; qq += S7_THREADS) {
             int a = 0, bnd = g.n_bins - 1;
             while (a < bnd) {
@@ -363,37 +372,39 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         }
         __syncthreads();
         if (tid < 16) {
-            const int i = tid;
+            const int i = tb + tid;
             float vm = 0.f, d = 0.f;
             if (i < g.n_bins) {
                 const int vmi = i > 0 ? sV[i - 1] : 0;
                 vm = (float)vmi;
                 d = 2.f * ((float)i * vm - sPJ[vmi]);
             }
-            svm[i] = vm;
-            sd[i] = d;
+            svm[tid] = vm;
+            sd[tid] = d;
         }
         __syncthreads();  // scratch rows, PJ, (vm, d) ready
         if (GT) {  // G_i(v) for every bin and count (score6.cu's table)
             float* const sG = reinterpret_cast<float*>(sm + g.o_gt);
             for (int idx = tid; idx < 16 * GP; idx += S7_THREADS) {
-                const int i = idx / GP, v = idx - i * GP;
+                const int j = idx / GP, v = idx - j * GP;
                 const float fv = (float)v;
-                const float nu = fmaf((float)i, fv, -sPJ[v]);
-                sG[idx] = fv < svm[i] ? nu : sd[i] - nu;
+                const float nu = fmaf((float)(tb + j), fv, -sPJ[v]);
+                sG[idx] = fv < svm[j] ? nu : sd[j] - nu;
             }
             __syncthreads();
         }
+        };
 
-        // ======== phase 4: stream the padded centre rows
-        {
-            // this thread's 4 bins: i = 4 grp + j
+        // ======== phase 4: stream the padded centre rows; scores the pixels whose
+        // bin is in [bin_lo, bin_hi]
+        auto phase4 = [&](int tb, int bin_lo, int bin_hi) {
+            // this thread's 4 lanes: bins i = tb + 4 grp + j
             float vmj[4], dj[4], fi[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 vmj[j] = svm[grp * 4 + j];
                 dj[j] = sd[grp * 4 + j];
-                fi[j] = (float)(grp * 4 + j);
+                fi[j] = (float)(tb + grp * 4 + j);
             }
             // vertical window counts, 16-bit lanes: lo = lanes (4g, 4g+2), hi =
             // (4g+1, 4g+3); the count below the group (lane 4g-1) is the
@@ -528,15 +539,36 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 };
                 if (tid < W) {
                     const int ys = s + 1;
-                    if (ys < h) snap[(sf == 0 ? g.nsnap - 1 : sf - 1) * W + xl] = dwin(sb[ys * W + xl]);
+                    if (ys < h) {
+                        const int b = sb[ys * W + xl];
+                        if (b >= bin_lo && b <= bin_hi)
+                            snap[(sf == 0 ? g.nsnap - 1 : sf - 1) * W + xl] = dwin(b - tb);
+                    }
                 } else if (tid < 2 * W && yf >= 0 && yf < h) {
-                    const double sc = dwin(sb[yf * W + xl]) - snap[sf * W + xl];
-                    part[yf * W + xl] = pold + fmaf((float)sc, scale, 0.f);
+                    const int b = sb[yf * W + xl];
+                    if (b >= bin_lo && b <= bin_hi) {
+                        const double sc = dwin(b - tb) - snap[sf * W + xl];
+                        part[yf * W + xl] = pold + fmaf((float)sc, scale, 0.f);
+                    }
                 }
                 sf = sf + 1 == g.nsnap ? 0 : sf + 1;
             }
+        };
+
+        // ======== the channel: reference passes, then scoring passes (the last
+        // reference pass's row windows are the first scoring pass's)
+        const int npass = g.passes;
+        if (g.fref)
+            for (int p = 0; p < npass; ++p) {
+                rw_phase(15 * p);
+                fref_pass(15 * p, p > 0 ? 1 : 0);
+            }
+        for (int p = npass - 1; p >= 0; --p) {
+            if (!(g.fref && p == npass - 1)) rw_phase(15 * p);
+            pass_tables(15 * p);
+            phase4(15 * p, p == 0 ? 0 : 15 * p + 1, min(15 * p + 15, g.n_bins - 1));
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -563,7 +595,7 @@ static int nsmid7() {
 
 static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, int groups_hint,
                        int pad, int budget, bool has_ref, Score7Geom* out, size_t* smem_out) {
-    if (w != S7_W || t < 17 || t > 65 || (t & 1) == 0 || n_bins < 1 || n_bins > 16)
+    if (w != S7_W || t < 17 || t > 65 || (t & 1) == 0 || n_bins < 1 || n_bins > 256)
         return QFCA_ERR_UNSUPPORTED;
     if (h < 2 || h > 128 || (h * w) % 16) return QFCA_ERR_UNSUPPORTED;
     if (pad != QFCA_PAD_REFLECT && pad != QFCA_PAD_WRAP) return QFCA_ERR_UNSUPPORTED;
@@ -572,6 +604,8 @@ static int score7_plan(int h, int w, int n_bins, int t, int C, int64_t images, i
     g.h = h; g.n_bins = n_bins; g.pad = pad; g.C = C;
     g.S = h + 2 * (t / 2);
     g.nsnap = 2 * (t / 2) + 2;
+    // pass p counts with lanes for bins 15p .. 15p + 15 (15 new bins after the first)
+    g.passes = n_bins <= 16 ? 1 : 1 + (n_bins - 16 + 14) / 15;
     if (!has_ref) {  // in-kernel reference: the sample store must fit shared memory
         if (budget < 1) return QFCA_ERR_ARG;
         g.fref = 1;

@@ -25,7 +25,10 @@ def _features(seed, images, C, h, w=128):
     (17, 128, 16, "reflect"), (33, 128, 16, "reflect"), (65, 128, 16, "reflect"),
     (21, 128, 16, "wrap"), (65, 128, 16, "wrap"), (33, 100, 16, "reflect"),
     (65, 40, 8, "reflect"), (25, 128, 5, "reflect"), (19, 128, 2, "reflect"),
-    (45, 77, 13, "wrap")])
+    (45, 77, 13, "wrap"),
+    # bin passes (N > 16): 15 new bins per pass after the first
+    (17, 128, 17, "reflect"), (33, 128, 32, "reflect"), (21, 100, 64, "wrap"),
+    (65, 40, 48, "reflect"), (33, 128, 100, "reflect")])
 def test_score7_vs_oracle(t, h, n, pad):
     import torch
     import paper_2510_15602_b200 as Q
@@ -98,7 +101,7 @@ def test_score7_batch_matches_single():
 
 @pytest.mark.parametrize("t,h,n,pad,budget", [
     (33, 128, 16, 1, 4096), (17, 128, 12, 2, 4096), (65, 100, 16, 1, 4096),
-    (21, 128, 16, 1, 1000), (45, 60, 7, 2, 4096)])
+    (21, 128, 16, 1, 1000), (45, 60, 7, 2, 4096), (33, 128, 40, 1, 4096)])
 def test_score7_inkernel_reference_equals_k3(t, h, n, pad, budget):
     """v7 selecting the reference itself (sample sweep over its own window
     counts + packed-compare order statistic) gives K3's reference exactly:
