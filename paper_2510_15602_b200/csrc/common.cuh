@@ -27,6 +27,22 @@ struct Taps {
 // images x groups CTAs, each scoring batches-per-CTA (bpc) batches, so the
 // run takes ceil(CTAs / resident slots) waves of bpc batch-times.  Minimise
 // waves * (bpc + per-CTA setup), ties to fewer groups (fewer partial maps).
+// The library's stream-ordered scratch (cudaMallocAsync, a few small buffers)
+// comes from the device's default memory pool; keep its freed memory mapped
+// (release threshold = max) so a synchronisation between calls does not
+// return it to the driver and make the next allocation map pages again.
+inline void keep_default_pool() {
+    static int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 inline int balanced_groups(int64_t images, int C, int cpb, int per_sm) {
     static int sms = 0;
     if (sms <= 0) {

@@ -261,6 +261,7 @@ int launch_image_score(const double* scores, int64_t images, int h, int w, int b
         int parts = (int)((148 * 2 + images - 1) / images);
         parts = parts > ih ? ih : (parts < 1 ? 1 : parts);
         double* tmp = nullptr;
+        keep_default_pool();
         if (cudaMallocAsync(&tmp, (size_t)images * parts * sizeof(double), st) != cudaSuccess)
             return QFCA_ERR_CUDA;
         k_image_score_part<<<(unsigned)(images * parts), 256, 0, st>>>(scores, h, w, border,

@@ -352,6 +352,7 @@ int launch_bin(const float* x, int64_t planes, int64_t plane_len, const float* l
     if (n_bins >= 2 && n_bins <= BT_MAXN + 1 && (out_bytes == 1 || out_bytes == 2)) {
         // thresholds in a stream-ordered scratch allocation
         float* tau = nullptr;
+        keep_default_pool();
         if (cudaMallocAsync(&tau, (size_t)planes * (n_bins - 1) * sizeof(float), st) !=
             cudaSuccess)
             return QFCA_ERR_CUDA;
