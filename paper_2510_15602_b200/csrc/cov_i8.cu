@@ -112,7 +112,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
 // (one HBM read), its mean is formed there when requested (fp64, fixed
 // order), then the fixed-point exponent and the four balanced base-256 digit
 // planes D[((img * 4 + k) * Cp + c) * Kp + p].
-constexpr int DG_THREADS = 256;
+constexpr int DG_THREADS = 128;
 
 __device__ __forceinline__ double block_reduce_dg(double v, bool is_max, double* red) {
 #pragma unroll
