@@ -459,9 +459,14 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                 }
             }
             {
+                // count rows loaded two stream rows ahead of their transport
+                uint4 vq0 = sacol[rmap[s0] * W];
+                uint4 vq1 = T > 1 ? sacol[rmap[s0 + 1] * W] : vq0;
 #pragma unroll
                 for (int rho = 0; rho < T; ++rho) {
-                    const uint4 v = sacol[rmap[s0 + rho] * W];
+                    const uint4 v = vq0;
+                    vq0 = vq1;
+                    if (rho + 2 < T) vq1 = sacol[rmap[s0 + rho + 2] * W];
                     // (word, prev) = words grp, grp - 1 (0 for grp 0): branch-free selects
                     const uint32_t wlo = g1 ? v.y : v.x, whi = g1 ? v.w : v.z;
                     const uint32_t plo = g1 ? v.x : 0u, phi = g1 ? v.z : v.y;
