@@ -495,29 +495,58 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
         };
 
         // ======== phase 4: E (register ring) + own-bin box, one barrier per sub-chunk.
-        // Each thread's count words of sub-chunk u + 2 are loaded from the scratch
-        // into registers while sub-chunk u runs.  A pass scores the pixels whose bin
+        // T = 5..11: each thread's count words of sub-chunk u + 2 are loaded from the
+        // L2-resident scratch into registers while sub-chunk u runs (-1 % at T = 9);
+        // T >= 13 (the E ring needs the registers) and T = 3 (measured +3 % with
+        // the register path): the count rows of sub-chunk
+        // u + 2 are copied (cp.async) from the scratch into a 3-slot ring in the
+        // (now free) staging region; each slot is [row][word][x].  A pass scores the pixels whose bin
         // is in [bin_lo, bin_hi]; its lanes are bins tb .. tb + 15.
         auto phase4 = [&](int tb, int bin_lo, int bin_hi) {
             const uint32_t gaddr =
                 (uint32_t)__cvta_generic_to_shared(GT + grp * 4 * GP) + g.moff;
-            // count words of this thread's (column, group) for the CH stream rows
-            // of sub-chunk SUB, straight from the L2-resident scratch (written by
-            // phase 1 of this CTA; .cg loads), two sub-chunks ahead of their use
-            const int n_sub = n_chunks * NSUB;
+            constexpr bool RP = T >= 5 && T <= 11;  // register prefetch (else the cp.async ring)
             const bool g1 = grp > 0;
             const uint32_t* const scol = scr + grp * W + x;
             auto load_words = [&](int sub, uint32_t (&wd)[CH], uint32_t (&pv)[CH]) {
 #pragma unroll
                 for (int rr = 0; rr < CH; ++rr) {
                     const uint32_t* const p_ = scol + (size_t)rmap[sub * CH + rr] * 4 * W;
-                    wd[rr] = __ldcg(p_);
+                    wd[rr] = __ldcg(p_);  // (written by phase 1 of this CTA: L2, not L1)
                     pv[rr] = g1 ? __ldcg(p_ - W) : 0u;
                 }
             };
             uint32_t wA[CH], pA[CH], wB[CH], pB[CH];
-            load_words(0, wA, pA);
-            load_words(1, wB, pB);
+            uint32_t* const cring = reinterpret_cast<uint32_t*>(STG);
+            constexpr int SLOT = CH * 4 * W;  // uint32 per slot
+            const int n_sub = n_chunks * NSUB;
+            // copy tasks (row of the sub-chunk, 16-byte piece): 128 pieces per 2 KB row
+            constexpr int NCP = (CH * 128 + S6_THREADS - 1) / S6_THREADS;
+#define S6_COPY(SUB)                                                            \
+    {                                                                           \
+        const int sub_ = (SUB);                                                 \
+        if (!RP && sub_ < n_sub) {                                              \
+            uint32_t* const dst_ = cring + (sub_ % 3) * SLOT;                   \
+            _Pragma("unroll") for (int k_ = 0; k_ < NCP; ++k_) {                \
+                const int task_ = (S6_THREADS - 1 - tid) + S6_THREADS * k_;     \
+                if (task_ < CH * 128) {                                         \
+                    const int rr_ = task_ >> 7, pc_ = 4 * (task_ & 127);        \
+                    const int row_ = rmap[sub_ * CH + rr_];                     \
+                    cp_async16(dst_ + rr_ * 4 * W + pc_, scr + (size_t)row_ * 4 * W + pc_); \
+                }                                                               \
+            }                                                                   \
+        }                                                                       \
+        asm volatile("cp.async.commit_group;" ::: "memory");                    \
+    }
+            if (RP) {
+                load_words(0, wA, pA);
+                load_words(1, wB, pB);
+            } else {
+                S6_COPY(0)
+                S6_COPY(1)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                __syncthreads();  // slot 0 visible
+            }
             float ring[T][4];
             bool mring[T];  // group mass of the last T stream rows (static slots)
             float vs[4];
@@ -568,6 +597,8 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
 #pragma unroll
                 for (int sc = 0; sc < NSUB; ++sc) {
                     const int u = ck * NSUB + sc;  // sub-chunk index
+                    if (!RP) S6_COPY(u + 2)
+                    const uint32_t* const cs = cring + (u % 3) * SLOT + grp * W + x;
                     float* const vbw = Vb + (size_t)((u & 1) * CH) * 16 * S6_VP + S6_VO;
                     // ---- E for CH stream rows (rows past the plane read zero counts):
                     // all rows' count words first, one warp vote per sub-chunk, then
@@ -577,12 +608,17 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     bool any = false;
 #pragma unroll
                     for (int rr = 0; rr < CH; ++rr) {
-                        word[rr] = wA[rr];
-                        prev[rr] = pA[rr];
-                        wA[rr] = wB[rr];
-                        pA[rr] = pB[rr];
+                        if (RP) {
+                            word[rr] = wA[rr];
+                            prev[rr] = pA[rr];
+                            wA[rr] = wB[rr];
+                            pA[rr] = pB[rr];
+                        } else {
+                            word[rr] = cs[rr * 4 * W];
+                            prev[rr] = g1 ? cs[rr * 4 * W - W] : 0u;
+                        }
                     }
-                    load_words(u + 2, wB, pB);  // (past the plane: the zero row h)
+                    if (RP) load_words(u + 2, wB, pB);  // (past the plane: the zero row h)
 #pragma unroll
                     for (int rr = 0; rr < CH; ++rr) {
                         mass[rr] = (word[rr] >> 24) != (prev[rr] >> 24);  // mass in the group
@@ -654,11 +690,13 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         const int y = u * CH + rr - 2 * R;
                         pold[a] = (rr < CH && y >= 0 && y < h) ? part[y * W + x] : 0.f;
                     }
+                    if (!RP) asm volatile("cp.async.wait_group 1;" ::: "memory");  // slot u + 1 landed
                     __syncthreads();
                 }
             }
             own_bin_box(n_sub - 1, pold, false);  // the last sub-chunk
         };
+#undef S6_COPY
         for (int p = npass - 1; p >= 0; --p) {
             if (!(g.fref && p == npass - 1)) {  // else the last search pass left them
                 build_th(15 * p);
