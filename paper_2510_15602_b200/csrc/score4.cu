@@ -251,9 +251,22 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     cst.w += a.w;
                 }
                 dst[y0 * W] = cst;
+                // the next row's bin bytes are loaded before this row's store (which
+                // the compiler cannot prove disjoint from them)
+                int na = 0, nr = 0;
+                if (y0 + 1 < y1) {
+                    const int2 st = stab[y0 + 1];
+                    na = pb[st.x];
+                    nr = pb[st.y];
+                }
                 for (int y = y0 + 1; y < y1; ++y) {
-                    const int2 st = stab[y];
-                    const uint4 a = thermo4(pb[st.x]), r = thermo4(pb[st.y]);
+                    const int ca = na, cr = nr;
+                    if (y + 1 < y1) {
+                        const int2 st = stab[y + 1];
+                        na = pb[st.x];
+                        nr = pb[st.y];
+                    }
+                    const uint4 a = thermo4(ca), r = thermo4(cr);
                     cst.x += a.x - r.x;
                     cst.y += a.y - r.y;
                     cst.z += a.z - r.z;

@@ -294,12 +294,32 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             for (int kb = 0; kb < g.qrows; kb += S6_BAND) {
                 // H1: S6_BAND rows of this quarter -> staging slots q1 * 8 + kk
                 // (cst enters as the window sum of row hy0 + kb - 1)
+                // T <= 11: the band's bin bytes first -- the staging stores below
+                // may alias them for the compiler, which would serialise each load
+                // after the previous row's store (-1.6 % at T = 9; T >= 13 keeps
+                // the registers for its E ring)
+                constexpr bool BP = T <= 11;
+                int ba[S6_BAND], br[S6_BAND];
+#pragma unroll
+                for (int kk = 0; kk < S6_BAND; ++kk) {
+                    const int y = hy0 + kb + kk;
+                    ba[kk] = br[kk] = 0;
+                    if (BP && y < hy1) {
+                        const int2 st = stab[y];
+                        ba[kk] = pb[st.x];
+                        br[kk] = pb[st.y];
+                    }
+                }
 #pragma unroll
                 for (int kk = 0; kk < S6_BAND; ++kk) {
                     const int y = hy0 + kb + kk;
                     if (y < hy1) {
-                        const int2 st = stab[y];
-                        const uint4 a = thermo6(pb[st.x], thb), r = thermo6(pb[st.y], thb);
+                        if (!BP) {
+                            const int2 st = stab[y];
+                            ba[kk] = pb[st.x];
+                            br[kk] = pb[st.y];
+                        }
+                        const uint4 a = thermo6(ba[kk], thb), r = thermo6(br[kk], thb);
                         cst.x += a.x - r.x;
                         cst.y += a.y - r.y;
                         cst.z += a.z - r.z;
