@@ -272,6 +272,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                     // then two slides per sample row with the next row's four row
                     // windows loaded one sample row ahead
                     const int cy0 = j0 * 2;
+#pragma unroll 8
                     for (int dy = -R; dy <= R; ++dy) {
                         const uint32_t w = col[(size_t)map_coord(cy0 + dy, h, g.pad) * 4 * W];
                         l16 += w & 0x00FF00FFu;
@@ -427,6 +428,7 @@ k_score7(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             int sf = (g.nsnap - 2 * R) % g.nsnap;  // snapshot slot of row s - 2R
             {  // the first centre's window: all its rows
                 const int c0 = stab[0].x;
+#pragma unroll 8
                 for (int dy = -R; dy <= R; ++dy) {
                     const uint32_t wa = rwt[(size_t)map_coord(c0 + dy, h, g.pad) * 4 * W];
                     alo += wa & 0x00FF00FFu;
