@@ -502,6 +502,14 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                         S4_E(0) S4_E(1) S4_E(2) S4_E(3)
 #undef S4_E
                     }
+                    // the previous row's vertical sums are stored only now, after
+                    // this row's loads (a store before them would keep the compiler
+                    // from issuing them early: it cannot prove the two disjoint)
+                    if (rho >= 1 && s0 + rho - 1 >= 2 * R) {
+                        float* vb = Vb + (((rho - 1) * CPB + cs) * 16 + grp4) * W + x;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
+                    }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         vs[j] += E[j] - ring[rho][j];
@@ -516,11 +524,11 @@ k_score4(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
                             vs[j] = s;
                         }
                     }
-                    if (s0 + rho >= 2 * R) {
-                        float* vb = Vb + ((rho * CPB + cs) * 16 + grp4) * W + x;
+                }
+                if (s0 + T - 1 >= 2 * R) {
+                    float* vb = Vb + (((T - 1) * CPB + cs) * 16 + grp4) * W + x;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
-                    }
+                    for (int j = 0; j < 4; ++j) vb[j * W] = vs[j];
                 }
             }
             __syncthreads();  // Vb complete
