@@ -294,40 +294,39 @@ k_score6(const uint8_t* __restrict__ bins, const float* __restrict__ lo,
             for (int kb = 0; kb < g.qrows; kb += S6_BAND) {
                 // H1: S6_BAND rows of this quarter -> staging slots q1 * 8 + kk
                 // (cst enters as the window sum of row hy0 + kb - 1)
-                // T <= 11: the band's bin bytes first -- the staging stores below
-                // may alias them for the compiler, which would serialise each load
-                // after the previous row's store (-1.6 % at T = 9; T >= 13 keeps
-                // the registers for its E ring)
-                constexpr bool BP = T <= 11;
-                int ba[S6_BAND], br[S6_BAND];
+                // the bin bytes of BPG rows first, then their windows and staging
+                // stores -- a store before a load keeps the compiler from issuing the
+                // load early (it cannot prove the two disjoint): the whole band at
+                // T <= 11 (-1.6 % at T = 9), half bands at T >= 13 (registers)
+                constexpr int BPG = T <= 11 ? S6_BAND : S6_BAND / 2;
 #pragma unroll
-                for (int kk = 0; kk < S6_BAND; ++kk) {
-                    const int y = hy0 + kb + kk;
-                    ba[kk] = br[kk] = 0;
-                    if (BP && y < hy1) {
-                        const int2 st = stab[y];
-                        ba[kk] = pb[st.x];
-                        br[kk] = pb[st.y];
-                    }
-                }
+                for (int k0 = 0; k0 < S6_BAND; k0 += BPG) {
+                    int ba[BPG], br[BPG];
 #pragma unroll
-                for (int kk = 0; kk < S6_BAND; ++kk) {
-                    const int y = hy0 + kb + kk;
-                    if (y < hy1) {
-                        if (!BP) {
+                    for (int e = 0; e < BPG; ++e) {
+                        const int y = hy0 + kb + k0 + e;
+                        ba[e] = br[e] = 0;
+                        if (y < hy1) {
                             const int2 st = stab[y];
-                            ba[kk] = pb[st.x];
-                            br[kk] = pb[st.y];
+                            ba[e] = pb[st.x];
+                            br[e] = pb[st.y];
                         }
-                        const uint4 a = thermo6(ba[kk], thb), r = thermo6(br[kk], thb);
-                        cst.x += a.x - r.x;
-                        cst.y += a.y - r.y;
-                        cst.z += a.z - r.z;
-                        cst.w += a.w - r.w;
-                        uint4* row = STG + (q1 * S6_BAND + kk) * WPP;
-                        row[s6_elem(col + R)] = cst;
-                        if (halo0 >= 0) row[s6_elem(halo0)] = cst;
-                        if (halo1 >= 0) row[s6_elem(halo1)] = cst;
+                    }
+#pragma unroll
+                    for (int e = 0; e < BPG; ++e) {
+                        const int kk = k0 + e;
+                        const int y = hy0 + kb + kk;
+                        if (y < hy1) {
+                            const uint4 a = thermo6(ba[e], thb), r = thermo6(br[e], thb);
+                            cst.x += a.x - r.x;
+                            cst.y += a.y - r.y;
+                            cst.z += a.z - r.z;
+                            cst.w += a.w - r.w;
+                            uint4* row = STG + (q1 * S6_BAND + kk) * WPP;
+                            row[s6_elem(col + R)] = cst;
+                            if (halo0 >= 0) row[s6_elem(halo0)] = cst;
+                            if (halo1 >= 0) row[s6_elem(halo1)] = cst;
+                        }
                     }
                 }
                 __syncthreads();
